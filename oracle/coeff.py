@@ -1,0 +1,63 @@
+"""Coefficient fields c(x) -- ORACLE (test infrastructure only).
+
+The paper assembles with c == 1.  BASELINE.json's configs multiply the
+integrands of both M and K by a coefficient c (reading R4); each row
+samples c at its own quadrature nodes.  Kinds (descriptor dicts, inputs/configs.py):
+
+  const        c = c0
+  trig_sep     c = c0 + amp * prod_a trig_a(2 pi k_a x_a)            (C2, C4; reading R13)
+  fourier_logn c = exp(sum_m a_m cos(2 pi (kx x + ky y + kz z) + theta_m))   (C3; R13)
+  grid         multilinear interpolation of vertex values, vertex (a,b,c) at (a,b,c)/n  (C5; R6)
+"""
+import math
+
+import numpy as np
+
+
+def evaluate(desc, n, pts, grid=None, plane0=0):
+    """c at points ``pts`` = list of d coordinate arrays (same shape)."""
+    kind = desc["kind"]
+    d = len(pts)
+    if kind == "const":
+        return np.full(np.shape(pts[0]), float(desc["c0"]))
+    if kind == "trig_sep":
+        prod = np.ones(np.shape(pts[0]))
+        for a in range(d):
+            f = np.sin if desc["trig"][a] == "sin" else np.cos
+            prod = prod * f(2.0 * math.pi * desc["wavenum"][a] * pts[a])
+        return desc["c0"] + desc["amp"] * prod
+    if kind == "fourier_logn":
+        s = np.zeros(np.shape(pts[0]))
+        for a_m, kx, ky, kz, th in desc["modes"]:
+            arg = kx * pts[0]
+            if d > 1:
+                arg = arg + ky * pts[1]
+            if d > 2:
+                arg = arg + kz * pts[2]
+            s = s + a_m * np.cos(2.0 * math.pi * arg + th)
+        return np.exp(s)
+    if kind == "grid":
+        return _multilinear(grid, n, pts, plane0)
+    raise ValueError(kind)
+
+
+def _multilinear(grid, n, pts, plane0):
+    """Vertex field interpolation.  grid is indexed [slowest] ... [x]; its slowest axis
+    starts at vertex plane ``plane0``.  Cell = element containing the point."""
+    d = len(pts)
+    cells, fracs = [], []
+    for a in range(d):
+        s = np.asarray(pts[a], dtype=np.float64) * n
+        e = np.clip(np.floor(s), 0, n - 1).astype(np.int64)
+        cells.append(e)
+        fracs.append(s - e)
+    out = np.zeros(np.shape(pts[0]))
+    for corner in range(2 ** d):
+        bits = [(corner >> a) & 1 for a in range(d)]
+        wgt = np.ones(np.shape(pts[0]))
+        for a in range(d):
+            wgt = wgt * (fracs[a] if bits[a] else 1.0 - fracs[a])
+        idx = [cells[a] + bits[a] for a in range(d)]
+        idx[d - 1] = idx[d - 1] - plane0          # slowest axis is slab-local
+        out = out + wgt * grid[tuple(idx[::-1])]
+    return out
