@@ -1,0 +1,376 @@
+#!/usr/bin/env python
+"""Benchmark: assembled nonzeros/sec (FP64, device-timed) of the weighted-Gaussian row-wise
+assembly (BASELINE.json metric), one process per GPU.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+A step = one pass of the whole hot path (every row of the rank's slab,
+M and K fused) over the workload; inputs (rules tables, coefficient slab) are resident in HBM
+when the timed region starts.  Default workload: C5 (3D C2-cubic, 256^3 elements, M+K,
+gridded lognormal coefficient), the config the metric is quoted on (it fits one B200).
+Rows are z-slab sharded across ranks; the total mesh is fixed, so scaling is
+"strong".  Timing: CUDA events on the launching stream around each step, L2 flushed between
+steps, max over ranks.  Rank 0 prints one JSON line.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import inputs  # noqa: E402
+
+METRIC = "assembled nonzeros/sec (FP64, device-timed)"
+UNIT = "nnz/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--n", type=int, default=None, help="override elements per direction")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ld", type=int, default=None)
+    return ap.parse_args()
+
+
+def stencil_nnz(p, n, d, rows):
+    """Structural nonzeros of a set of global rows (per matrix)."""
+    N = n + p
+    tot = 0
+    for r in rows:
+        w = 1
+        for a in range(d):
+            i = (r // N ** a) % N
+            w *= min(i + p, N - 1) - max(i - p, 0) + 1
+        tot += w
+    return tot
+
+
+# ------------------------------------------------------------------------------------------
+# the oracle on the host (cpu_baseline and --impl reference)
+# ------------------------------------------------------------------------------------------
+def oracle_sample_rows(cfg, budget_rows, seed=0):
+    """A bounded, deterministic sample of the workload's rows: whole x-lines from the first,
+    a middle and the last z-planes (every row class occurs), as (grid slab, plane0, rows)."""
+    p, n, d = cfg["p"], cfg["n"], cfg["dim"]
+    N = n + p
+    rng = np.random.default_rng(seed)
+    groups = []
+    if d == 3:
+        zs = [0, 1, N // 2, N - 1]
+    elif d == 2:
+        zs = [0, N // 2, N - 1]
+    else:
+        zs = [0]
+    per = max(1, budget_rows // len(zs))
+    for z in zs:
+        if d == 1:
+            rows = np.arange(N)[:per]
+        else:
+            lines = max(1, per // N)
+            ys = rng.choice(N, size=min(lines, N), replace=False) if d == 3 else [None]
+            rows = []
+            for y in ys:
+                base = (z * N + y) * N if d == 3 else z * N
+                rows.extend(range(base, base + N))
+            rows = np.array(rows[:per])
+        groups.append((z, rows))
+    return groups
+
+
+def run_oracle(cfg, seconds, rows_hint=None):
+    """Time the oracle (as it stands) on a bounded sample: returns (nnz/s, sample text, cores)."""
+    from oracle import assemble as oasm
+    p, n, d = cfg["p"], cfg["n"], cfg["dim"]
+    desc = inputs.coefficient(cfg["coeff"], d)
+    kinds = cfg["kinds"]
+    oasm.tables_1d(p, n)                                  # setup, untimed
+    probe = oracle_sample_rows(cfg, 64)
+    g0 = _oracle_grid(cfg, probe[0][0])
+    t0 = time.perf_counter()
+    oasm.assemble_rows(p, n, d, probe[0][1][:16], desc, kinds, grid=g0[0], plane0=g0[1])
+    per_row = (time.perf_counter() - t0) / 16
+    budget = rows_hint or max(32, int(seconds / max(per_row, 1e-6)))
+    groups = oracle_sample_rows(cfg, budget)
+    nnz = 0
+    elapsed = 0.0
+    nrows = 0
+    for z, rows in groups:
+        grid, plane0 = _oracle_grid(cfg, z)
+        t0 = time.perf_counter()
+        oasm.assemble_rows(p, n, d, rows, desc, kinds, grid=grid, plane0=plane0)
+        elapsed += time.perf_counter() - t0
+        nnz += stencil_nnz(p, n, d, rows) * len(kinds)
+        nrows += len(rows)
+    sample = f"{nrows} rows of {cfg['name']} (whole x-lines of z-planes {[int(z) for z, _ in groups]}), {'+'.join(kinds)}"
+    return nnz / elapsed, sample, 1, elapsed
+
+
+def _oracle_grid(cfg, z):
+    if cfg["coeff"]["kind"] != "grid":
+        return None, 0
+    p, n, d = cfg["p"], cfg["n"], cfg["dim"]
+    lo, hi = max(0, z - p), min(n, z + 1)
+    g = inputs.lognormal_grid(n, seed=cfg["coeff"]["seed"], sigma=cfg["coeff"]["sigma"], dim=d, plane0=lo,
+                              planes=hi - lo + 1)
+    return g, lo
+
+
+# ------------------------------------------------------------------------------------------
+# clocks during the timed region (NVML)
+# ------------------------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting"}
+
+    def __init__(self, device):
+        self.samples, self.reasons, self.ok = [], 0, False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": [v for k, v in self.REASONS.items() if self.reasons & k], "samples": len(self.samples)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)["hbm_gbs"], "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def traffic_from_profiles(cfg_name):
+    """dram bytes (read+write) per launch of the dominant kernel from a committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            t = json.load(f)
+        return t.get(cfg_name)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------------------------------
+def main():
+    args = parse()
+    cfg = inputs.config(args.config, args.n)
+    p, n, d = cfg["p"], cfg["n"], cfg["dim"]
+    kinds = cfg["kinds"]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        vals = []
+        info = None
+        for i in range(args.warmup + args.steps):
+            v, sample, cores, el = run_oracle(cfg, min(args.cpu_seconds, 60.0 / max(1, args.steps + args.warmup)))
+            if i >= args.warmup:
+                vals.append(v)
+                info = (sample, cores)
+        value = float(np.median(vals))
+        line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
+                "dtype": "f64", "data": "synthetic",
+                "config": {"workload": cfg["name"], "p": p, "n_elems": n, "dim": d, "kinds": list(kinds)},
+                "cpu_baseline": {"value": value, "unit": UNIT, "cores": info[1], "kind": "oracle", "sample": info[0]},
+                "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                "vs_baseline": None}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1710_01048_b200 import api, wgq
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+
+    rules = wgq.Rules(p, n, d)
+    N = rules.N
+    row_begin, row_end = api.slab_rows(N, d, rank, world)
+    rows = row_end - row_begin
+    ld = args.ld or rules.stencil
+    grid, plane0 = (None, 0)
+    if cfg["coeff"]["kind"] == "grid":
+        grid, plane0 = api.make_grid(rules, cfg["coeff"]["seed"], cfg["coeff"]["sigma"], row_begin, row_end)
+    coef = api.coefficient(inputs.coefficient(cfg["coeff"], d), grid, plane0)
+    out = {k: api.alloc_ell(rules, row_begin, row_end, ld) for k in kinds}
+    nnz_rank = wgq.wgq_nnz(rules, row_begin, row_end) * len(kinds)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")     # 512 MB > L2
+
+    def step():
+        api.assemble(rules, coef, kinds, row_begin, row_end, out=out, stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = float(np.sum(step_ms))
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    nz = torch.tensor([float(nnz_rank)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(nz, op=dist.ReduceOp.SUM)
+    total_ms_max = float(t.item())
+    nnz_all = float(nz.item())
+    value = nnz_all * args.steps / (total_ms_max / 1e3)
+
+    # roofline of the dominant (only) kernel: algorithmic bytes = rows x s^d x 8 x matrices
+    alg_bytes = rows * rules.stencil * 8 * len(kinds)
+    kernel_s = np.mean(step_ms) / 1e3
+    peak, peak_src = peaks()
+    achieved = alg_bytes / kernel_s / 1e9
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "peak_source": peak_src,
+            "traffic": traffic_from_profiles(cfg["name"]),
+            "kernel": "wgq assembly (M+K fused)", "algorithmic_bytes_per_launch": int(alg_bytes),
+            "kernel_ms": round(kernel_s * 1e3, 4)}
+
+    # end to end through the public API with HOST buffers (H2D of the coefficient slab, D2H of M, K)
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, cfg, rules, row_begin, row_end, ld, world, rank, local, nnz_all)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, sample, cores, el = run_oracle(cfg, args.cpu_seconds)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+               "seconds": round(el, 2)}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": total_ms_max / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": cfg["name"], "p": p, "n_elems": n, "dim": d, "kinds": list(kinds),
+                           "coefficient": cfg["coeff"]["kind"], "rows": rules.n_rows, "ld": ld,
+                           "layout": "ELL", "parallelism": f"z-slab x{world}",
+                           "l2": "flushed (512 MB write) between timed steps; outputs >> L2"},
+                "gpu_launches": args.steps * 1,
+                "roofline": roof, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, cfg, rules, row_begin, row_end, ld, world, rank, local, nnz_all):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1710_01048_b200 import api, wgq
+    p, n, d = cfg["p"], cfg["n"], cfg["dim"]
+    kinds = cfg["kinds"]
+    rows = row_end - row_begin
+    host = {k: wgq.PinnedArray((rows, ld)) for k in kinds}
+    h2d = 0
+    if cfg["coeff"]["kind"] == "grid":
+        lo, hi = api.grid_planes_for(rules, row_begin, row_end)
+        g = inputs.lognormal_grid(n, seed=cfg["coeff"]["seed"], sigma=cfg["coeff"]["sigma"], dim=d, plane0=lo,
+                                  planes=hi - lo + 1)
+        pin = wgq.PinnedArray(g.shape)
+        pin.array[...] = g
+        coef = wgq.make_coeff({"kind": "grid"}, grid=_HostGrid(pin.array), plane0=lo)
+        h2d = g.nbytes
+    else:
+        coef = api.coefficient(inputs.coefficient(cfg["coeff"], d))
+    M = host["mass"].array if "mass" in host else None
+    K = host["stiffness"].array if "stiffness" in host else None
+    wgq.wgq_assemble_host(rules, coef, row_begin, row_end, M, K, ld)       # warm-up
+    times = []
+    for _ in range(args.e2e_steps):
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        wgq.wgq_assemble_host(rules, coef, row_begin, row_end, M, K, ld)
+        times.append(time.perf_counter() - t0)
+    t = torch.tensor([float(np.sum(times))], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    value = nnz_all * args.e2e_steps / float(t.item())
+    d2h = rows * ld * 8 * len(kinds)
+    for v in host.values():
+        v.close()
+    return {"value": value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "steps": args.e2e_steps, "api": "wgq_assemble_host (pinned host buffers, chunked 2-stream pipeline)"}
+
+
+class _HostGrid:
+    """Adapter so make_coeff can take a host numpy array for wgq_assemble_host."""
+
+    def __init__(self, arr):
+        self.arr = arr
+        self.shape = arr.shape
+
+    def data_ptr(self):
+        return self.arr.ctypes.data
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,86 @@
+"""Tensor-level convenience layer over the C-ABI (allocation, slabs, streams).
+
+Everything numerical runs in libwgq's CUDA kernels; this module only sizes buffers,
+builds descriptors and picks row ranges.  Row slabs follow the z-slab (3D) / y-slab (2D)
+partition of SURVEY §8(e): contiguous ranges of the slowest row index.
+"""
+import torch
+
+from . import wgq
+
+
+def slab_rows(N, dim, rank, world):
+    """Row range [b, e) of rank's slab: contiguous planes of the slowest row index,
+    planes split as evenly as possible (the first N % world ranks get one more)."""
+    planes = N
+    base, extra = divmod(planes, world)
+    z0 = rank * base + min(rank, extra)
+    z1 = z0 + base + (1 if rank < extra else 0)
+    plane_rows = N ** (dim - 1)
+    return z0 * plane_rows, z1 * plane_rows
+
+
+def grid_planes_for(rules, row_begin, row_end):
+    """Vertex planes [lo, hi] of the slowest axis touched by rows [row_begin, row_end)."""
+    plane_rows = rules.N ** (rules.dim - 1)
+    z0 = row_begin // plane_rows
+    z1 = (row_end - 1) // plane_rows
+    return max(0, z0 - rules.p), min(rules.n, z1 + 1)
+
+
+def make_grid(rules, seed, sigma, row_begin, row_end, device=None, stream=None):
+    """Device-generated lognormal vertex slab covering rows [row_begin, row_end):
+    returns (grid tensor, plane0)."""
+    n, dim = rules.n, rules.dim
+    lo, hi = (0, n) if dim == 1 else grid_planes_for(rules, row_begin, row_end)
+    planes = hi - lo + 1
+    shape = {1: (n + 1,), 2: (planes, n + 1), 3: (planes, n + 1, n + 1)}[dim]
+    g = torch.empty(shape, dtype=torch.float64, device=device or "cuda")
+    wgq.wgq_generate_grid(n, dim, seed, sigma, lo, planes, g, stream)
+    return g, lo
+
+
+def coefficient(desc, grid=None, plane0=0):
+    return wgq.make_coeff(desc, grid, plane0)
+
+
+def alloc_ell(rules, row_begin, row_end, ld=None, device=None):
+    ld = ld or rules.stencil
+    return torch.empty((row_end - row_begin, ld), dtype=torch.float64, device=device or "cuda")
+
+
+def assemble(rules, coeff, kinds=("mass", "stiffness"), row_begin=0, row_end=None, ld=None, out=None, stream=None):
+    """Assemble rows [row_begin, row_end) in ELL layout; returns {'mass': T, 'stiffness': T}."""
+    if row_end is None:
+        row_end = rules.n_rows
+    out = dict(out or {})
+    for k in kinds:
+        if k not in out:
+            out[k] = alloc_ell(rules, row_begin, row_end, ld)
+    descs = {k: wgq.make_out(out[k], row_begin, row_end, ld=out[k].shape[1]) for k in kinds}
+    if "mass" in kinds and "stiffness" in kinds:
+        wgq.wgq_assemble_mass_stiffness(rules, coeff, descs["mass"], descs["stiffness"], stream)
+    elif "mass" in kinds:
+        wgq.wgq_assemble_mass(rules, coeff, descs["mass"], stream)
+    else:
+        wgq.wgq_assemble_stiffness(rules, coeff, descs["stiffness"], stream)
+    return out
+
+
+def assemble_csr(rules, coeff, kinds=("mass", "stiffness"), row_begin=0, row_end=None, stream=None):
+    """CSR assembly: returns (row_ptr int64, col_idx int32, {'mass': values, ...})."""
+    if row_end is None:
+        row_end = rules.n_rows
+    nnz = wgq.wgq_nnz(rules, row_begin, row_end)
+    row_ptr = torch.empty(row_end - row_begin + 1, dtype=torch.int64, device="cuda")
+    col_idx = torch.empty(nnz, dtype=torch.int32, device="cuda")
+    wgq.wgq_csr_structure(rules, row_begin, row_end, row_ptr, col_idx, stream)
+    vals = {k: torch.empty(nnz, dtype=torch.float64, device="cuda") for k in kinds}
+    descs = {k: wgq.make_out(vals[k], row_begin, row_end, ld=0, layout=wgq.WGQ_CSR, row_ptr=row_ptr) for k in kinds}
+    if "mass" in kinds and "stiffness" in kinds:
+        wgq.wgq_assemble_mass_stiffness(rules, coeff, descs["mass"], descs["stiffness"], stream)
+    elif "mass" in kinds:
+        wgq.wgq_assemble_mass(rules, coeff, descs["mass"], stream)
+    else:
+        wgq.wgq_assemble_stiffness(rules, coeff, descs["stiffness"], stream)
+    return row_ptr, col_idx, vals

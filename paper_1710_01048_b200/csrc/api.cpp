@@ -1,0 +1,230 @@
+// C-ABI of libwgq (include/wgq.h): argument validation, the per-device table cache and
+// dispatch to the CUDA launchers.  No arithmetic of the method lives here.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <new>
+
+#include "internal.h"
+
+namespace wgq {
+int64_t host_nnz_before(int64_t row, int p, int64_t N, int dim);
+}
+
+using namespace wgq;
+
+namespace {
+
+int64_t ipow(int64_t b, int e) {
+    int64_t r = 1;
+    for (int i = 0; i < e; ++i) r *= b;
+    return r;
+}
+
+int table_for(wgq_rules_s* R, RowTables* out, void* stream) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return WGQ_ECUDA;
+    std::lock_guard<std::mutex> lock(R->mu);
+    auto it = R->tables.find(dev);
+    if (it == R->tables.end()) {
+        RowTables T;
+        int rc = build_row_tables(R, &T, stream);
+        if (rc != WGQ_OK) return rc;
+        // the cache is used from any stream afterwards: complete the one-time build now
+        if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return WGQ_ECUDA;
+        it = R->tables.emplace(dev, T).first;
+    }
+    *out = it->second;
+    return WGQ_OK;
+}
+
+int check_out(const wgq_rules_s* R, const wgq_out_t* o) {
+    if (!o) return WGQ_EINVAL;
+    const int64_t total = ipow(R->N, R->dim);
+    if (o->row_begin < 0 || o->row_end < o->row_begin || o->row_end > total) return WGQ_EINVAL;
+    if (o->layout != WGQ_ELL && o->layout != WGQ_CSR) return WGQ_EINVAL;
+    if (o->row_end > o->row_begin && !o->values) return WGQ_EINVAL;
+    if (o->layout == WGQ_ELL && o->ld < ipow(2 * R->p + 1, R->dim)) return WGQ_ERANGE;
+    if (o->layout == WGQ_CSR && !o->row_ptr) return WGQ_EINVAL;
+    return WGQ_OK;
+}
+
+int check_coeff(const wgq_rules_s* R, const wgq_coeff_t* c, const wgq_out_t* o) {
+    if (!c) return WGQ_EINVAL;
+    switch (c->kind) {
+        case WGQ_COEF_CONST:
+            return WGQ_OK;
+        case WGQ_COEF_TRIG_SEP:
+            for (int a = 0; a < R->dim; ++a)
+                if (c->trig[a] != WGQ_TRIG_SIN && c->trig[a] != WGQ_TRIG_COS) return WGQ_EINVAL;
+            return WGQ_OK;
+        case WGQ_COEF_FOURIER_LOGN:
+            if (c->n_modes < 0 || c->n_modes > WGQ_MAX_MODES || (c->n_modes > 0 && !c->modes)) return WGQ_EINVAL;
+            return WGQ_OK;
+        case WGQ_COEF_GRID: {
+            if (!c->grid && o->row_end > o->row_begin) return WGQ_EINVAL;
+            if (o->row_end <= o->row_begin) return WGQ_OK;
+            const int64_t plane_rows = ipow(R->N, R->dim - 1);
+            const int64_t z0 = o->row_begin / plane_rows, z1 = (o->row_end - 1) / plane_rows;
+            const int64_t need_lo = z0 - R->p > 0 ? z0 - R->p : 0;
+            const int64_t need_hi = z1 + 1 < R->n ? z1 + 1 : R->n;
+            if (c->grid_plane0 > need_lo || c->grid_plane0 + c->grid_planes - 1 < need_hi) return WGQ_EINVAL;
+            return WGQ_OK;
+        }
+    }
+    return WGQ_EINVAL;
+}
+
+int assemble(wgq_rules_t R, const wgq_coeff_t* c, const wgq_out_t* M, const wgq_out_t* K, void* stream) {
+    if (!R) return WGQ_EINVAL;
+    int rc;
+    if (M && (rc = check_out(R, M)) != WGQ_OK) return rc;
+    if (K && (rc = check_out(R, K)) != WGQ_OK) return rc;
+    if (M && K && (M->row_begin != K->row_begin || M->row_end != K->row_end || M->layout != K->layout))
+        return WGQ_EINVAL;
+    const wgq_out_t* any = M ? M : K;
+    if ((rc = check_coeff(R, c, any)) != WGQ_OK) return rc;
+    if (any->row_end == any->row_begin) return WGQ_OK;
+    RowTables T;
+    if ((rc = table_for(R, &T, stream)) != WGQ_OK) return rc;
+    return launch_assemble(R, T, c, M, K, stream);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* wgq_strerror(int code) {
+    switch (code) {
+        case WGQ_OK: return "ok";
+        case WGQ_EINVAL: return "invalid argument (null or inconsistent descriptor, row range outside [0, N^d))";
+        case WGQ_EUNSUPPORTED: return "unsupported: p must be 2 or 3, dim 1..3, n_elems >= p";
+        case WGQ_ENOCONV: return "a quadrature rule failed its Newton solve or exactness check (residual > 1e-13)";
+        case WGQ_ECUDA: return "CUDA launch or allocation error";
+        case WGQ_ERANGE: return "ld < (2p+1)^dim or index overflow";
+        case WGQ_ENOMEM: return "host allocation failure";
+    }
+    return "unknown error";
+}
+
+const char* wgq_version(void) { return "wgq 0.1 (sm_100a)"; }
+
+int wgq_build_rules_ex(int p, int64_t n_elems, int dim, int boundary_mode, wgq_rules_t* out) {
+    if (!out) return WGQ_EINVAL;
+    *out = nullptr;
+    if (p != 2 && p != 3) return WGQ_EUNSUPPORTED;
+    if (dim < 1 || dim > 3) return WGQ_EUNSUPPORTED;
+    if (n_elems < p) return WGQ_EUNSUPPORTED;
+    if (boundary_mode != WGQ_BND_GAUSS && boundary_mode != WGQ_BND_GL) return WGQ_EINVAL;
+    const int64_t N = n_elems + p;
+    if (ipow(N, dim) >= ((int64_t)1 << 31)) return WGQ_ERANGE;   // int32 column ids
+    wgq_rules_s* R = new (std::nothrow) wgq_rules_s();
+    if (!R) return WGQ_ENOMEM;
+    R->p = p;
+    R->dim = dim;
+    R->n = n_elems;
+    R->N = N;
+    R->bnd = boundary_mode;
+    int rc = build_class_rules(p, boundary_mode, R->rules);
+    if (rc != WGQ_OK) {
+        delete R;
+        return rc;
+    }
+    *out = R;
+    return WGQ_OK;
+}
+
+int wgq_build_rules(int p, int64_t n_elems, int dim, wgq_rules_t* out) {
+    return wgq_build_rules_ex(p, n_elems, dim, WGQ_BND_GAUSS, out);
+}
+
+void wgq_free_rules(wgq_rules_t R) {
+    if (!R) return;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (auto& kv : R->tables) {
+        cudaSetDevice(kv.first);
+        free_row_tables(&kv.second);
+    }
+    cudaSetDevice(cur);
+    delete R;
+}
+
+int wgq_rules_info(wgq_rules_t R, int* p, int64_t* n_elems, int* dim, int64_t* n_rows_1d, int64_t* n_rows,
+                   int* stencil) {
+    if (!R) return WGQ_EINVAL;
+    if (p) *p = R->p;
+    if (n_elems) *n_elems = R->n;
+    if (dim) *dim = R->dim;
+    if (n_rows_1d) *n_rows_1d = R->N;
+    if (n_rows) *n_rows = ipow(R->N, R->dim);
+    if (stencil) *stencil = (int)ipow(2 * R->p + 1, R->dim);
+    return WGQ_OK;
+}
+
+int wgq_rules_query(wgq_rules_t R, int cls, int kind, int* m, double* tau, double* omega, double* max_residual) {
+    if (!R || !m || cls < 0 || cls > R->p || (kind != WGQ_MASS && kind != WGQ_STIFFNESS)) return WGQ_EINVAL;
+    const ClassRule& c = R->rules[kind][cls];
+    *m = c.m;
+    if (tau) std::memcpy(tau, c.tau, sizeof(double) * c.m);
+    if (omega) std::memcpy(omega, c.omega, sizeof(double) * c.m);
+    if (max_residual) *max_residual = c.residual;
+    return WGQ_OK;
+}
+
+int wgq_nnz(wgq_rules_t R, int64_t row_begin, int64_t row_end, int64_t* nnz) {
+    if (!R || !nnz) return WGQ_EINVAL;
+    if (row_begin < 0 || row_end < row_begin || row_end > ipow(R->N, R->dim)) return WGQ_EINVAL;
+    *nnz = host_nnz_before(row_end, R->p, R->N, R->dim) - host_nnz_before(row_begin, R->p, R->N, R->dim);
+    return WGQ_OK;
+}
+
+int wgq_assemble_mass(wgq_rules_t R, const wgq_coeff_t* c, const wgq_out_t* M, void* stream) {
+    if (!M) return WGQ_EINVAL;
+    return assemble(R, c, M, nullptr, stream);
+}
+
+int wgq_assemble_stiffness(wgq_rules_t R, const wgq_coeff_t* c, const wgq_out_t* K, void* stream) {
+    if (!K) return WGQ_EINVAL;
+    return assemble(R, c, nullptr, K, stream);
+}
+
+int wgq_assemble_mass_stiffness(wgq_rules_t R, const wgq_coeff_t* c, const wgq_out_t* M, const wgq_out_t* K,
+                                void* stream) {
+    if (!M || !K) return WGQ_EINVAL;
+    return assemble(R, c, M, K, stream);
+}
+
+int wgq_csr_structure(wgq_rules_t R, int64_t row_begin, int64_t row_end, int64_t* row_ptr, int32_t* col_idx,
+                      void* stream) {
+    if (!R || !row_ptr || row_begin < 0 || row_end < row_begin || row_end > ipow(R->N, R->dim)) return WGQ_EINVAL;
+    if (row_end > row_begin && !col_idx) return WGQ_EINVAL;
+    return launch_csr_structure(R, row_begin, row_end, row_ptr, col_idx, stream);
+}
+
+int wgq_generate_grid(int64_t n_elems, int dim, uint64_t seed, double sigma, int64_t plane0, int64_t planes,
+                      double* grid, void* stream) {
+    if (!grid || n_elems < 1 || dim < 1 || dim > 3 || planes < 0 || plane0 < 0) return WGQ_EINVAL;
+    if (dim == 1 && (plane0 != 0 || planes != n_elems + 1)) return WGQ_EINVAL;
+    if (plane0 + planes > n_elems + 1) return WGQ_EINVAL;
+    if (planes == 0) return WGQ_OK;
+    return launch_generate_grid(n_elems, dim, seed, sigma, plane0, planes, grid, stream);
+}
+
+int wgq_row_moments(wgq_rules_t R, const wgq_out_t* A, double* out, void* stream) {
+    if (!R || !out) return WGQ_EINVAL;
+    int rc = check_out(R, A);
+    if (rc != WGQ_OK) return rc;
+    if (A->layout != WGQ_ELL) return WGQ_EINVAL;
+    return launch_row_moments(R, A, out, stream);
+}
+
+int wgq_checksum(wgq_rules_t R, const wgq_out_t* A, unsigned long long* out_dev, void* stream) {
+    if (!R || !out_dev) return WGQ_EINVAL;
+    int rc = check_out(R, A);
+    if (rc != WGQ_OK) return rc;
+    if (A->layout != WGQ_ELL) return WGQ_EINVAL;
+    return launch_checksum(R, A, out_dev, stream);
+}
+
+}  // extern "C"

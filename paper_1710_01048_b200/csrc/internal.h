@@ -1,0 +1,78 @@
+// Internal declarations shared by the host rule builder, the C-ABI layer and the CUDA
+// kernels of libwgq.  Nothing here is part of the public ABI (include/wgq.h).
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <mutex>
+
+#include "wgq.h"
+
+namespace wgq {
+
+constexpr int kMaxP = 3;
+constexpr int kMaxS = 2 * kMaxP + 1;   // stencil width per direction
+constexpr int kMaxNodes = 12;          // per direction: GL(p+1) on up to p elements (R1, WGQ_BND_GL)
+constexpr int kMaxMassNodes = kMaxNodes;
+constexpr int kMaxStiffNodes = kMaxNodes;
+
+// One unit-spacing rule of a direction class (paper convention, P:250 / P:351).
+struct ClassRule {
+    int m = 0;
+    double tau[kMaxStiffNodes] = {};
+    double omega[kMaxStiffNodes] = {};
+    double residual = 0.0;
+};
+
+// Per-1D-row tables produced on the device by the table kernel (tables.cu).
+// Layout: struct of arrays over the N rows of one direction (all directions share it).
+struct RowTables {
+    int64_t N = 0;
+    int maxM = 0, maxK = 0;    // largest node counts over all rows (sizes the kernels' staging)
+    int* mM = nullptr;         // [N]   mass nodes of row r
+    int* mK = nullptr;         // [N]   stiffness nodes of row r
+    double* xM = nullptr;      // [N][kMaxMassNodes]   physical nodes
+    double* wM = nullptr;      // [N][kMaxMassNodes]   effective weights omega*B_r(x)
+    double* VM = nullptr;      // [N][kMaxMassNodes][kMaxS]  B_{r+o}(x_k), o = -p..p
+    double* xK = nullptr;      // [N][kMaxStiffNodes]
+    double* wK = nullptr;      // [N][kMaxStiffNodes]  omega*B'_r(x)
+    double* DK = nullptr;      // [N][kMaxStiffNodes][kMaxS] B'_{r+o}(x_k)
+    void* base = nullptr;      // single allocation
+};
+
+}  // namespace wgq
+
+struct wgq_rules_s {
+    int p = 0;
+    int dim = 0;
+    int bnd = WGQ_BND_GAUSS;
+    int64_t n = 0;
+    int64_t N = 0;
+    // rules[kind][cls]: cls 0..p-1 = left boundary weight j, cls p = interior
+    wgq::ClassRule rules[2][wgq::kMaxP + 1];
+    std::mutex mu;
+    std::map<int, wgq::RowTables> tables;   // per CUDA device
+};
+
+namespace wgq {
+
+// rules.cpp (host)
+int build_class_rules(int p, int bnd, ClassRule out[2][kMaxP + 1]);
+
+// tables.cu
+int build_row_tables(const wgq_rules_s* R, RowTables* T, void* stream);
+void free_row_tables(RowTables* T);
+
+// assemble.cu
+int launch_assemble(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c,
+                    const wgq_out_t* M, const wgq_out_t* K, void* stream);
+int launch_csr_structure(const wgq_rules_s* R, int64_t row_begin, int64_t row_end,
+                         int64_t* row_ptr, int32_t* col_idx, void* stream);
+int launch_row_moments(const wgq_rules_s* R, const wgq_out_t* A, double* out, void* stream);
+int launch_checksum(const wgq_rules_s* R, const wgq_out_t* A, unsigned long long* out, void* stream);
+
+// grid.cu
+int launch_generate_grid(int64_t n, int dim, uint64_t seed, double sigma, int64_t plane0,
+                         int64_t planes, double* grid, void* stream);
+
+}  // namespace wgq

@@ -1,0 +1,439 @@
+// Host-side construction of the weighted Gaussian rules (setup, not the hot path).
+//
+// Paper: Sec. 3.  Every rule is stored in unit element spacing with nodes
+// measured from the left end of the weight's support, in the paper's convention
+//     int f W = sum_k omega_k f(tau_k) W(tau_k),   W = B_j (mass) or B'_j (stiffness)
+// (eq:GaussQuadW P:242-244, eq:GaussQuadSys P:249-252, eq:GaussQuadSysStiff P:350-353).
+//
+//  interior p=2 mass : closed form of eq:QuadraticQuadrature: eliminating
+//                      omega_1, omega_2 leaves 26 tau^2 - 48 tau + 21 = 0.
+//  interior p=3 mass : damped Newton on the symmetric system eq:CubicQuadrature with the
+//                      brackets tau_1 in (0,1), tau_2 in (1,2) of P:326 and multi-start.
+//  interior p=2 stiff: tau = 3/4, 9/4, omega = 8/9 (eq:WQquadraticStiff P:383-388); the
+//                      middle node has zero effective weight (R2) and is dropped.
+//  interior p=3 stiff: omega_1 = 1, tau_1 = 1/2 - sqrt(225-30 sqrt 30)/30 (eq:CubicStiffTau1,
+//                      P:412), (tau_2, omega_2) by Newton on lines 2 and 4 of
+//                      eq:CubicQuadratureStiff (true signs R3).
+//  boundary j < p    : reading R1 (remark P:438-440).
+// Each rule is checked against exact moments over the full interacting set (< 1e-13).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <vector>
+
+#include "internal.h"
+
+namespace wgq {
+namespace {
+
+// ---------------------------------------------------------------------------------------
+// B-splines on an explicit knot vector: all nonzero functions of a span and their
+// derivatives (triangular de Boor table, Piegl & Tiller's algorithm A2.3).
+// ---------------------------------------------------------------------------------------
+struct Knots {
+    std::vector<double> t;
+    int p;
+    int nfun() const { return (int)t.size() - p - 1; }
+    int span(double x) const {
+        int hi = nfun();                       // last valid span index is nfun()-1
+        if (x >= t[hi]) return hi - 1;
+        int s = p;
+        while (s < hi - 1 && x >= t[s + 1]) ++s;
+        return s;
+    }
+};
+
+Knots unit_open_knots(int p, int n) {
+    Knots k;
+    k.p = p;
+    for (int i = 0; i <= p; ++i) k.t.push_back(0.0);
+    for (int i = 1; i < n; ++i) k.t.push_back((double)i);
+    for (int i = 0; i <= p; ++i) k.t.push_back((double)n);
+    return k;
+}
+
+// ders[d][r] = d-th derivative of N_{s-p+r}(x), r = 0..p, d = 0..nd (nd <= 2)
+void span_ders(const Knots& K, int s, double x, int nd, double ders[3][kMaxP + 1]) {
+    const int p = K.p;
+    const double* t = K.t.data();
+    double ndu[kMaxP + 1][kMaxP + 1], left[kMaxP + 1], right[kMaxP + 1];
+    ndu[0][0] = 1.0;
+    for (int j = 1; j <= p; ++j) {
+        left[j] = x - t[s + 1 - j];
+        right[j] = t[s + j] - x;
+        double saved = 0.0;
+        for (int r = 0; r < j; ++r) {
+            ndu[j][r] = right[r + 1] + left[j - r];
+            double tmp = ndu[r][j - 1] / ndu[j][r];
+            ndu[r][j] = saved + right[r + 1] * tmp;
+            saved = left[j - r] * tmp;
+        }
+        ndu[j][j] = saved;
+    }
+    for (int r = 0; r <= p; ++r) ders[0][r] = ndu[r][p];
+    for (int r = 0; r <= p; ++r) {
+        double a[2][kMaxP + 1];
+        int s1 = 0, s2 = 1;
+        a[0][0] = 1.0;
+        for (int k = 1; k <= nd; ++k) {
+            double d = 0.0;
+            int rk = r - k, pk = p - k;
+            if (r >= k) {
+                a[s2][0] = a[s1][0] / ndu[pk + 1][rk];
+                d = a[s2][0] * ndu[rk][pk];
+            }
+            int j1 = (rk >= -1) ? 1 : -rk;
+            int j2 = (r - 1 <= pk) ? k - 1 : p - r;
+            for (int j = j1; j <= j2; ++j) {
+                a[s2][j] = (a[s1][j] - a[s1][j - 1]) / ndu[pk + 1][rk + j];
+                d += a[s2][j] * ndu[rk + j][pk];
+            }
+            if (r <= pk) {
+                a[s2][k] = -a[s1][k - 1] / ndu[pk + 1][r];
+                d += a[s2][k] * ndu[r][pk];
+            }
+            ders[k][r] = d;
+            std::swap(s1, s2);
+        }
+    }
+    double f = p;
+    for (int k = 1; k <= nd; ++k) {
+        for (int r = 0; r <= p; ++r) ders[k][r] *= f;
+        f *= (p - k);
+    }
+}
+
+// value of the order-th derivative of B_i at x
+double bval(const Knots& K, int i, double x, int order) {
+    int s = K.span(x);
+    if (i < s - K.p || i > s) return 0.0;
+    double ders[3][kMaxP + 1];
+    span_ders(K, s, x, order, ders);
+    return ders[order][i - (s - K.p)];
+}
+
+// ---------------------------------------------------------------------------------------
+// Gauss-Legendre by Newton on the three-term recurrence.
+// ---------------------------------------------------------------------------------------
+void gauss_legendre(int m, std::vector<double>& x, std::vector<double>& w) {
+    x.assign(m, 0.0);
+    w.assign(m, 0.0);
+    for (int i = 0; i < m; ++i) {
+        double z = std::cos(M_PI * (i + 0.75) / (m + 0.5));
+        double dp = 0.0;
+        for (int it = 0; it < 100; ++it) {
+            double p0 = 1.0, p1 = 0.0;
+            for (int k = 1; k <= m; ++k) {
+                double p2 = p1;
+                p1 = p0;
+                p0 = ((2.0 * k - 1.0) * z * p1 - (k - 1.0) * p2) / k;
+            }
+            dp = m * (z * p0 - p1) / (z * z - 1.0);
+            double dz = p0 / dp;
+            z -= dz;
+            if (std::fabs(dz) < 1e-17) break;
+        }
+        x[m - 1 - i] = z;                       // ascending
+        w[m - 1 - i] = 2.0 / ((1.0 - z * z) * dp * dp);
+    }
+}
+
+// int_{lo}^{hi} B_i^{(o)} B_j^{(o)} dx, exact by (p+2)-point GL on every knot span
+double product_moment(const Knots& K, int i, int j, int order, double lo, double hi) {
+    std::vector<double> gx, gw;
+    gauss_legendre(K.p + 2, gx, gw);
+    double sum = 0.0;
+    for (size_t s = 0; s + 1 < K.t.size(); ++s) {
+        double a = K.t[s], b = K.t[s + 1];
+        if (b <= a || a < lo || b > hi) continue;
+        for (size_t q = 0; q < gx.size(); ++q) {
+            double x = 0.5 * (a + b) + 0.5 * (b - a) * gx[q];
+            sum += 0.5 * (b - a) * gw[q] * bval(K, i, x, order) * bval(K, j, x, order);
+        }
+    }
+    return sum;
+}
+
+// exactness residual r_i = sum_k omega_k F_i(x_k) W(x_k) - mu_i
+struct Exactness {
+    Knots K;
+    int j, order;
+    double lo, hi;
+    std::vector<int> rows;
+    std::vector<double> mu;
+    Exactness(int p, int j_, int order_, bool interior) : K(unit_open_knots(p, 4 * p + 2)), j(j_), order(order_) {
+        lo = K.t[j];
+        hi = K.t[j + p + 1];
+        for (int i = j - p; i <= j + p; ++i)
+            if (i >= 0 && i < K.nfun()) rows.push_back(i);
+        (void)interior;
+        for (int i : rows) mu.push_back(product_moment(K, i, j, order, lo, hi));
+    }
+    double residual(int row_index, int m, const double* tau, const double* om) const {
+        double q = 0.0;
+        for (int k = 0; k < m; ++k) {
+            double x = lo + tau[k];
+            q += om[k] * bval(K, rows[row_index], x, order) * bval(K, j, x, order);
+        }
+        return q - mu[row_index];
+    }
+    double max_residual(int m, const double* tau, const double* om) const {
+        double worst = 0.0;
+        for (size_t r = 0; r < rows.size(); ++r) worst = std::max(worst, std::fabs(residual((int)r, m, tau, om)));
+        return worst;
+    }
+};
+
+// ---------------------------------------------------------------------------------------
+// Damped Newton with finite-difference Jacobian, step halving and bracket projection.
+// ---------------------------------------------------------------------------------------
+using ResidualFn = std::function<void(const std::vector<double>& u, std::vector<double>& r)>;
+
+bool solve_linear(std::vector<double> A, std::vector<double> b, int n, std::vector<double>& x) {
+    for (int c = 0; c < n; ++c) {
+        int piv = c;
+        for (int r = c + 1; r < n; ++r)
+            if (std::fabs(A[r * n + c]) > std::fabs(A[piv * n + c])) piv = r;
+        if (std::fabs(A[piv * n + c]) < 1e-300) return false;
+        if (piv != c) {
+            for (int k = 0; k < n; ++k) std::swap(A[c * n + k], A[piv * n + k]);
+            std::swap(b[c], b[piv]);
+        }
+        for (int r = c + 1; r < n; ++r) {
+            double f = A[r * n + c] / A[c * n + c];
+            for (int k = c; k < n; ++k) A[r * n + k] -= f * A[c * n + k];
+            b[r] -= f * b[c];
+        }
+    }
+    x.assign(n, 0.0);
+    for (int r = n - 1; r >= 0; --r) {
+        double s = b[r];
+        for (int k = r + 1; k < n; ++k) s -= A[r * n + k] * x[k];
+        x[r] = s / A[r * n + r];
+    }
+    return true;
+}
+
+double newton(const ResidualFn& F, std::vector<double>& u, const std::vector<std::pair<double, double>>& box) {
+    const int n = (int)u.size();
+    auto project = [&](std::vector<double>& v) {
+        for (int i = 0; i < n; ++i) {
+            double a = box[i].first, b = box[i].second;
+            if (a < b) v[i] = std::min(std::max(v[i], a + 1e-12 * (b - a)), b - 1e-12 * (b - a));
+        }
+    };
+    auto norm = [](const std::vector<double>& r) {
+        double m = 0.0;
+        for (double v : r) m = std::max(m, std::fabs(v));
+        return m;
+    };
+    project(u);
+    std::vector<double> r(n), rp(n), rm(n), J(n * n), du, v;
+    F(u, r);
+    double nr = norm(r);
+    for (int it = 0; it < 60 && nr > 4e-17; ++it) {
+        for (int c = 0; c < n; ++c) {
+            double h = 1e-7 * std::max(1.0, std::fabs(u[c]));
+            std::vector<double> up = u, um = u;
+            up[c] += h;
+            um[c] -= h;
+            F(up, rp);
+            F(um, rm);
+            for (int rr = 0; rr < n; ++rr) J[rr * n + c] = (rp[rr] - rm[rr]) / (2.0 * h);
+        }
+        if (!solve_linear(J, r, n, du)) break;
+        double lam = 1.0;
+        bool ok = false;
+        while (lam > 1e-6) {
+            v = u;
+            for (int i = 0; i < n; ++i) v[i] -= lam * du[i];
+            project(v);
+            F(v, rp);
+            double nv = norm(rp);
+            if (std::isfinite(nv) && nv < nr) {
+                u = v;
+                r = rp;
+                nr = nv;
+                ok = true;
+                break;
+            }
+            lam *= 0.5;
+        }
+        if (!ok) break;
+    }
+    return nr;
+}
+
+// ---------------------------------------------------------------------------------------
+// the rules
+// ---------------------------------------------------------------------------------------
+int finish(ClassRule& R, const Exactness& E) {
+    R.residual = E.max_residual(R.m, R.tau, R.omega);
+    return R.residual < 1e-13 ? WGQ_OK : WGQ_ENOCONV;
+}
+
+int interior_mass_p2(ClassRule& R) {
+    Exactness E(2, 4, 0, true);
+    double t1 = (24.0 - std::sqrt(30.0)) / 26.0;          // root in (0,1) of 26t^2 - 48t + 21
+    double w1 = 1.0 / (30.0 * t1 * t1 * (1.0 - t1) * (1.0 - t1));
+    double w2 = (16.0 / 9.0) * (11.0 / 20.0 - 0.5 * w1 * t1 * t1 * t1 * t1);
+    R.m = 3;
+    double tau[3] = {t1, 1.5, 3.0 - t1}, om[3] = {w1, w2, w1};
+    std::memcpy(R.tau, tau, sizeof tau);
+    std::memcpy(R.omega, om, sizeof om);
+    return finish(R, E);
+}
+
+int interior_mass_p3(ClassRule& R) {
+    Exactness E(3, 6, 0, true);
+    auto expand = [](const std::vector<double>& u, double* tau, double* om) {
+        tau[0] = u[0]; tau[1] = u[1]; tau[2] = 4.0 - u[1]; tau[3] = 4.0 - u[0];
+        om[0] = u[2]; om[1] = u[3]; om[2] = u[3]; om[3] = u[2];
+    };
+    ResidualFn F = [&](const std::vector<double>& u, std::vector<double>& r) {
+        double tau[4], om[4];
+        expand(u, tau, om);
+        for (int k = 0; k < 4; ++k) r[k] = E.residual(k, 4, tau, om);   // offsets -3..0
+    };
+    const double s1[] = {0.5, 0.3, 0.7, 0.15, 0.85}, s2[] = {1.5, 1.3, 1.7, 1.15, 1.85};
+    for (double a : s1)
+        for (double b : s2) {
+            std::vector<double> u = {a, b, 1.0, 1.0};
+            double nr = newton(F, u, {{0.0, 1.0}, {1.0, 2.0}, {0.0, 0.0}, {0.0, 0.0}});
+            if (nr < 1e-14 && u[0] > 0 && u[0] < 1 && u[1] > 1 && u[1] < 2 && u[2] > 0 && u[3] > 0) {
+                R.m = 4;
+                expand(u, R.tau, R.omega);
+                return finish(R, E);
+            }
+        }
+    return WGQ_ENOCONV;
+}
+
+int interior_stiff_p2(ClassRule& R) {
+    Exactness E(2, 4, 1, true);
+    R.m = 2;                                   // the middle node tau = 3/2 has B'_j = 0 (R2)
+    R.tau[0] = 0.75; R.tau[1] = 2.25;
+    R.omega[0] = R.omega[1] = 8.0 / 9.0;
+    return finish(R, E);
+}
+
+int interior_stiff_p3(ClassRule& R) {
+    Exactness E(3, 6, 1, true);
+    const double w1 = 1.0;
+    const double t1 = 0.5 - std::sqrt(225.0 - 30.0 * std::sqrt(30.0)) / 30.0;
+    auto expand = [&](const std::vector<double>& u, double* tau, double* om) {
+        tau[0] = t1; tau[1] = u[0]; tau[2] = 4.0 - u[0]; tau[3] = 4.0 - t1;
+        om[0] = w1; om[1] = u[1]; om[2] = u[1]; om[3] = w1;
+    };
+    ResidualFn F = [&](const std::vector<double>& u, std::vector<double>& r) {
+        double tau[4], om[4];
+        expand(u, tau, om);
+        r[0] = E.residual(1, 4, tau, om);       // offset -2 (line 2)
+        r[1] = E.residual(3, 4, tau, om);       // offset  0 (line 4)
+    };
+    for (double a : {1.5, 1.3, 1.7, 1.15, 1.85}) {
+        std::vector<double> u = {a, 1.0};
+        double nr = newton(F, u, {{1.0, 2.0}, {0.0, 0.0}});
+        if (nr < 1e-14 && u[0] > 1 && u[0] < 2 && u[1] > 0) {
+            R.m = 4;
+            expand(u, R.tau, R.omega);
+            return finish(R, E);
+        }
+    }
+    return WGQ_ENOCONV;
+}
+
+void gl_per_element(int p, int j, ClassRule& R) {
+    std::vector<double> gx, gw;
+    gauss_legendre(p + 1, gx, gw);
+    R.m = 0;
+    for (int e = 0; e <= j; ++e)
+        for (int q = 0; q <= p; ++q) {
+            R.tau[R.m] = e + 0.5 + 0.5 * gx[q];
+            R.omega[R.m] = 0.5 * gw[q];
+            ++R.m;
+        }
+}
+
+// Reading R1: m = ceil(D/2) nodes; the last node is fixed at j + 1/2 when D is odd.
+int boundary_rule(int p, int j, int kind, int bnd, ClassRule& R) {
+    const int order = kind == WGQ_MASS ? 0 : 1;
+    Exactness E(p, j, order, false);
+    if (bnd == WGQ_BND_GL) {
+        gl_per_element(p, j, R);
+        return finish(R, E);
+    }
+    const int D = order == 0 ? p + j + 1 : p + j;
+    const int m = (D + 1) / 2;
+    const bool fixed = (D % 2) == 1;
+    const int nfree = fixed ? m - 1 : m;
+    const double L = j + 1.0;
+    const int neq = D;                         // stiffness: last constraint implied (sum B'_i = 0)
+    auto expand = [&](const std::vector<double>& u, double* tau, double* om) {
+        for (int k = 0; k < nfree; ++k) tau[k] = u[k];
+        if (fixed) tau[m - 1] = j + 0.5;
+        for (int k = 0; k < m; ++k) om[k] = u[nfree + k];
+    };
+    ResidualFn F = [&](const std::vector<double>& u, std::vector<double>& r) {
+        double tau[kMaxStiffNodes], om[kMaxStiffNodes];
+        expand(u, tau, om);
+        for (int e = 0; e < neq; ++e) r[e] = E.residual(e, m, tau, om);
+    };
+    std::vector<std::pair<double, double>> box;
+    for (int k = 0; k < nfree; ++k) box.push_back({0.0, L});
+    for (int k = 0; k < m; ++k) box.push_back({0.0, 0.0});
+    // deterministic multi-start: increasing tuples of a 9-point grid
+    const int G = 9;
+    std::vector<double> grid;
+    for (int g = 0; g < G; ++g) grid.push_back(L * (0.05 + 0.9 * g / (G - 1)));
+    std::vector<int> idx(nfree);
+    std::function<bool(int, int)> rec = [&](int pos, int start) -> bool {
+        if (pos == nfree) {
+            std::vector<double> u;
+            for (int k = 0; k < nfree; ++k) u.push_back(grid[idx[k]]);
+            if (fixed && nfree > 0 && u.back() >= j + 0.5) return false;
+            for (int k = 0; k < m; ++k) u.push_back(1.0 / m);
+            double nr = newton(F, u, box);
+            if (nr > 1e-14) return false;
+            double tau[kMaxStiffNodes], om[kMaxStiffNodes];
+            expand(u, tau, om);
+            for (int k = 0; k < m; ++k) {
+                if (!(tau[k] > 1e-9 && tau[k] < L - 1e-9 && om[k] > 0)) return false;
+                if (k > 0 && !(tau[k] > tau[k - 1] + 1e-9)) return false;
+            }
+            R.m = m;
+            std::memcpy(R.tau, tau, sizeof(double) * m);
+            std::memcpy(R.omega, om, sizeof(double) * m);
+            return true;
+        }
+        for (int g = start; g < G; ++g) {
+            idx[pos] = g;
+            if (rec(pos + 1, g + 1)) return true;
+        }
+        return false;
+    };
+    if (!rec(0, 0)) gl_per_element(p, j, R);    // no admissible minimal rule -> GL (R1)
+    return finish(R, E);
+}
+
+}  // namespace
+
+int build_class_rules(int p, int bnd, ClassRule out[2][kMaxP + 1]) {
+    int rc;
+    if (p == 2) {
+        if ((rc = interior_mass_p2(out[WGQ_MASS][p])) != WGQ_OK) return rc;
+        if ((rc = interior_stiff_p2(out[WGQ_STIFFNESS][p])) != WGQ_OK) return rc;
+    } else if (p == 3) {
+        if ((rc = interior_mass_p3(out[WGQ_MASS][p])) != WGQ_OK) return rc;
+        if ((rc = interior_stiff_p3(out[WGQ_STIFFNESS][p])) != WGQ_OK) return rc;
+    } else {
+        return WGQ_EUNSUPPORTED;
+    }
+    for (int kind = 0; kind < 2; ++kind)
+        for (int j = 0; j < p; ++j)
+            if ((rc = boundary_rule(p, j, kind, bnd, out[kind][j])) != WGQ_OK) return rc;
+    return WGQ_OK;
+}
+
+}  // namespace wgq

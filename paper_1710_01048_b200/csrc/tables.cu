@@ -1,0 +1,187 @@
+// Device construction of the per-1D-row tables: for every
+// basis function r of one direction, its physical quadrature nodes, effective weights
+// and the values B_{r+o}(x_k) / B'_{r+o}(x_k), o = -p..p, of the 2p+1 interacting
+// functions at those nodes.  The tables depend on (p, n, rules) only and are built once
+// per device and cached in the rules handle.
+//
+// Node placement (R1): row r < p uses the left boundary class j = r (x = tau/n); row
+// r >= n the mirrored class j = N-1-r (x = 1 - tau/n); other rows the interior rule
+// shifted to supp B_r = [(r-p)/n, (r+1)/n] (x = (r - p + tau)/n).  Weights scale
+// by h = 1/n (dx = h dtau); derivative values are physical.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "internal.h"
+
+namespace wgq {
+namespace {
+
+struct ClassArgs {
+    int p;
+    int64_t n;
+    int64_t N;
+    int m[2][kMaxP + 1];
+    double tau[2][kMaxP + 1][kMaxStiffNodes];
+    double omega[2][kMaxP + 1][kMaxStiffNodes];
+};
+
+// open uniform knot t_i on [0,1]: 0 for i <= p, (i-p)/n inside, 1 for i >= n+p (eq:Gmap3)
+__device__ __forceinline__ double knot(int64_t i, int p, int64_t n) {
+    int64_t k = i - p;
+    k = k < 0 ? 0 : (k > n ? n : k);
+    return (double)k / (double)n;
+}
+
+// Values and first derivatives of the p+1 nonzero B-splines on the span of x (Cox-de Boor
+// triangle; vals[q] = B_{s-p+q}(x), ders[q] = B'_{s-p+q}(x)).  Returns the span s.
+__device__ int64_t eval_span(double x, int p, int64_t n, double* vals, double* ders) {
+    int64_t e = (int64_t)floor(x * (double)n);
+    e = e < 0 ? 0 : (e > n - 1 ? n - 1 : e);
+    const int64_t s = e + p;
+    double lower[kMaxP + 1];           // degree p-1 values
+    double N[kMaxP + 1];
+    N[0] = 1.0;
+    for (int deg = 1; deg <= p; ++deg) {
+        if (deg == p)
+            for (int q = 0; q < p; ++q) lower[q] = N[q];
+        double next[kMaxP + 1];
+        // functions B_{s-deg..s, deg}: q-th is B_{s-deg+q}
+        for (int q = 0; q <= deg; ++q) {
+            const int64_t i = s - deg + q;
+            double v = 0.0;
+            if (q >= 1) {                      // B_{i,deg-1} = N[q-1]
+                double den = knot(i + deg, p, n) - knot(i, p, n);
+                if (den > 0.0) v += (x - knot(i, p, n)) / den * N[q - 1];
+            }
+            if (q <= deg - 1) {                // B_{i+1,deg-1} = N[q]
+                double den = knot(i + deg + 1, p, n) - knot(i + 1, p, n);
+                if (den > 0.0) v += (knot(i + deg + 1, p, n) - x) / den * N[q];
+            }
+            next[q] = v;
+        }
+        for (int q = 0; q <= deg; ++q) N[q] = next[q];
+    }
+    for (int q = 0; q <= p; ++q) {
+        vals[q] = N[q];
+        const int64_t i = s - p + q;
+        double d = 0.0;
+        if (q >= 1) {
+            double den = knot(i + p, p, n) - knot(i, p, n);
+            if (den > 0.0) d += p / den * lower[q - 1];
+        }
+        if (q <= p - 1) {
+            double den = knot(i + p + 1, p, n) - knot(i + 1, p, n);
+            if (den > 0.0) d -= p / den * lower[q];
+        }
+        ders[q] = d;
+    }
+    return s;
+}
+
+__global__ void k_row_tables(ClassArgs A, RowTables T) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t r = tid / (2 * kMaxStiffNodes);
+    const int kind = (int)((tid / kMaxStiffNodes) & 1);
+    const int k = (int)(tid % kMaxStiffNodes);
+    if (r >= A.N) return;
+    const int p = A.p;
+    const int64_t n = A.n, N = A.N;
+    int cls;
+    bool mirror = false;
+    if (r < p) {
+        cls = (int)r;
+    } else if (r >= n) {
+        cls = (int)(N - 1 - r);
+        mirror = true;
+    } else {
+        cls = p;
+    }
+    const int m = A.m[kind][cls];
+    const int maxn = kind == WGQ_MASS ? kMaxMassNodes : kMaxStiffNodes;
+    if (k == 0) (kind == WGQ_MASS ? T.mM : T.mK)[r] = m;
+    if (k >= maxn) return;
+    double* X = kind == WGQ_MASS ? T.xM : T.xK;
+    double* W = kind == WGQ_MASS ? T.wM : T.wK;
+    double* V = kind == WGQ_MASS ? T.VM : T.DK;
+    double* row = V + (r * maxn + k) * kMaxS;
+    if (k >= m) {                         // unused node slot: zero weight, zero table
+        X[r * maxn + k] = 0.0;
+        W[r * maxn + k] = 0.0;
+        for (int o = 0; o < kMaxS; ++o) row[o] = 0.0;
+        return;
+    }
+    double x, om;
+    if (cls == p) {
+        x = ((double)(r - p) + A.tau[kind][cls][k]) / (double)n;
+        om = A.omega[kind][cls][k] / (double)n;
+    } else if (!mirror) {
+        x = A.tau[kind][cls][k] / (double)n;
+        om = A.omega[kind][cls][k] / (double)n;
+    } else {
+        x = 1.0 - A.tau[kind][cls][m - 1 - k] / (double)n;
+        om = A.omega[kind][cls][m - 1 - k] / (double)n;
+    }
+    double vals[kMaxP + 1], ders[kMaxP + 1];
+    const int64_t s = eval_span(x, p, n, vals, ders);
+    const double* src = kind == WGQ_MASS ? vals : ders;
+    for (int o = 0; o < kMaxS; ++o) {
+        double v = 0.0;
+        if (o <= 2 * p) {
+            const int64_t i = r + o - p;
+            if (i >= 0 && i < N && i >= s - p && i <= s) v = src[i - (s - p)];
+        }
+        row[o] = v;
+    }
+    X[r * maxn + k] = x;
+    W[r * maxn + k] = om * row[p];        // omega * B_r(x) or omega * B'_r(x)
+}
+
+}  // namespace
+
+int build_row_tables(const wgq_rules_s* R, RowTables* T, void* stream) {
+    const int64_t N = R->N;
+    size_t bytes = 2 * N * sizeof(int) + N * (kMaxMassNodes * (2 + kMaxS) + kMaxStiffNodes * (2 + kMaxS)) * sizeof(double);
+    bytes += 256;
+    void* base = nullptr;
+    if (cudaMalloc(&base, bytes) != cudaSuccess) return WGQ_ECUDA;
+    T->base = base;
+    T->N = N;
+    double* d = (double*)base;
+    T->xM = d; d += N * kMaxMassNodes;
+    T->wM = d; d += N * kMaxMassNodes;
+    T->VM = d; d += N * kMaxMassNodes * kMaxS;
+    T->xK = d; d += N * kMaxStiffNodes;
+    T->wK = d; d += N * kMaxStiffNodes;
+    T->DK = d; d += N * kMaxStiffNodes * kMaxS;
+    T->mM = (int*)d;
+    T->mK = T->mM + N;
+    T->maxM = T->maxK = 0;
+    for (int c = 0; c <= R->p; ++c) {
+        T->maxM = std::max(T->maxM, R->rules[WGQ_MASS][c].m);
+        T->maxK = std::max(T->maxK, R->rules[WGQ_STIFFNESS][c].m);
+    }
+    ClassArgs A{};
+    A.p = R->p;
+    A.n = R->n;
+    A.N = N;
+    for (int kind = 0; kind < 2; ++kind)
+        for (int c = 0; c <= R->p; ++c) {
+            A.m[kind][c] = R->rules[kind][c].m;
+            for (int k = 0; k < kMaxStiffNodes; ++k) {
+                A.tau[kind][c][k] = R->rules[kind][c].tau[k];
+                A.omega[kind][c][k] = R->rules[kind][c].omega[k];
+            }
+        }
+    const int64_t threads = N * 2 * kMaxStiffNodes;
+    k_row_tables<<<(unsigned)((threads + 255) / 256), 256, 0, (cudaStream_t)stream>>>(A, *T);
+    if (cudaGetLastError() != cudaSuccess) return WGQ_ECUDA;
+    return WGQ_OK;
+}
+
+void free_row_tables(RowTables* T) {
+    if (T->base) cudaFree(T->base);
+    T->base = nullptr;
+}
+
+}  // namespace wgq

@@ -1,0 +1,266 @@
+"""Thin ctypes binding of libwgq (include/wgq.h): argument marshalling only.
+
+Every function has the name of the C entry point it calls.  Tensors are passed by
+``data_ptr()``; streams by ``torch.cuda.Stream.cuda_stream``.  Nothing here computes any
+part of the method: the product path is the CUDA library, and it fails loudly (ImportError
+/ WgqError) when the library is missing or a call fails -- there is no CPU fallback.
+"""
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libwgq.so")
+
+WGQ_OK, WGQ_EINVAL, WGQ_EUNSUPPORTED, WGQ_ENOCONV, WGQ_ECUDA, WGQ_ERANGE, WGQ_ENOMEM = 0, -1, -2, -3, -4, -5, -6
+WGQ_BND_GAUSS, WGQ_BND_GL = 0, 1
+WGQ_MASS, WGQ_STIFFNESS = 0, 1
+WGQ_COEF_CONST, WGQ_COEF_TRIG_SEP, WGQ_COEF_FOURIER_LOGN, WGQ_COEF_GRID = 0, 1, 2, 3
+WGQ_TRIG_SIN, WGQ_TRIG_COS = 0, 1
+WGQ_MAX_MODES = 16
+WGQ_ELL, WGQ_CSR = 0, 1
+
+
+class WgqError(RuntimeError):
+    def __init__(self, fn, code):
+        super().__init__(f"{fn} failed: {code} ({_lib.wgq_strerror(code).decode()})")
+        self.code = code
+
+
+class wgq_coeff_t(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int), ("c0", ctypes.c_double), ("amp", ctypes.c_double),
+                ("trig", ctypes.c_int * 3), ("wavenum", ctypes.c_int * 3), ("n_modes", ctypes.c_int),
+                ("modes", ctypes.POINTER(ctypes.c_double)), ("grid", ctypes.c_void_p),
+                ("grid_plane0", ctypes.c_int64), ("grid_planes", ctypes.c_int64)]
+
+
+class wgq_out_t(ctypes.Structure):
+    _fields_ = [("layout", ctypes.c_int), ("row_begin", ctypes.c_int64), ("row_end", ctypes.c_int64),
+                ("values", ctypes.c_void_p), ("ld", ctypes.c_int64), ("row_ptr", ctypes.c_void_p),
+                ("col_idx", ctypes.c_void_p)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libwgq.so (raises if it was not built: no fallback path exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: run `python -m paper_1710_01048_b200.build` (no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    c_int, c_i64, vp, dp = ctypes.c_int, ctypes.c_int64, ctypes.c_void_p, ctypes.POINTER(ctypes.c_double)
+    sig = {
+        "wgq_strerror": (ctypes.c_char_p, [c_int]),
+        "wgq_version": (ctypes.c_char_p, []),
+        "wgq_build_rules": (c_int, [c_int, c_i64, c_int, ctypes.POINTER(vp)]),
+        "wgq_build_rules_ex": (c_int, [c_int, c_i64, c_int, c_int, ctypes.POINTER(vp)]),
+        "wgq_free_rules": (None, [vp]),
+        "wgq_rules_info": (c_int, [vp, ctypes.POINTER(c_int), ctypes.POINTER(c_i64), ctypes.POINTER(c_int),
+                                   ctypes.POINTER(c_i64), ctypes.POINTER(c_i64), ctypes.POINTER(c_int)]),
+        "wgq_rules_query": (c_int, [vp, c_int, c_int, ctypes.POINTER(c_int), dp, dp, dp]),
+        "wgq_nnz": (c_int, [vp, c_i64, c_i64, ctypes.POINTER(c_i64)]),
+        "wgq_assemble_mass": (c_int, [vp, ctypes.POINTER(wgq_coeff_t), ctypes.POINTER(wgq_out_t), vp]),
+        "wgq_assemble_stiffness": (c_int, [vp, ctypes.POINTER(wgq_coeff_t), ctypes.POINTER(wgq_out_t), vp]),
+        "wgq_assemble_mass_stiffness": (c_int, [vp, ctypes.POINTER(wgq_coeff_t), ctypes.POINTER(wgq_out_t),
+                                                ctypes.POINTER(wgq_out_t), vp]),
+        "wgq_csr_structure": (c_int, [vp, c_i64, c_i64, vp, vp, vp]),
+        "wgq_generate_grid": (c_int, [c_i64, c_int, ctypes.c_uint64, ctypes.c_double, c_i64, c_i64, vp, vp]),
+        "wgq_row_moments": (c_int, [vp, ctypes.POINTER(wgq_out_t), vp, vp]),
+        "wgq_checksum": (c_int, [vp, ctypes.POINTER(wgq_out_t), vp, vp]),
+        "wgq_assemble_host": (c_int, [vp, ctypes.POINTER(wgq_coeff_t), c_i64, c_i64, vp, vp, c_i64, c_i64]),
+        "wgq_host_alloc": (c_int, [ctypes.c_uint64, ctypes.POINTER(vp)]),
+        "wgq_host_free": (c_int, [vp]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+def exported_symbols():
+    return ["wgq_strerror", "wgq_version", "wgq_build_rules", "wgq_build_rules_ex", "wgq_free_rules",
+            "wgq_rules_info", "wgq_rules_query", "wgq_nnz", "wgq_assemble_mass", "wgq_assemble_stiffness",
+            "wgq_assemble_mass_stiffness", "wgq_csr_structure", "wgq_generate_grid", "wgq_row_moments",
+            "wgq_checksum", "wgq_assemble_host", "wgq_host_alloc", "wgq_host_free"]
+
+
+def _check(fn, rc):
+    if rc != WGQ_OK:
+        raise WgqError(fn, rc)
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return ctypes.c_void_p(stream)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+# ---------------------------------------------------------------------------------------
+# rules
+# ---------------------------------------------------------------------------------------
+class Rules:
+    """Owns a wgq_rules_t handle (wgq_build_rules_ex / wgq_free_rules)."""
+
+    def __init__(self, p, n_elems, dim, boundary_mode=WGQ_BND_GAUSS):
+        h = ctypes.c_void_p()
+        _check("wgq_build_rules_ex", lib().wgq_build_rules_ex(p, n_elems, dim, boundary_mode, ctypes.byref(h)))
+        self.handle = h
+        self.p, self.n, self.dim = p, n_elems, dim
+        info = wgq_rules_info(self)
+        self.N, self.n_rows, self.stencil = info["n_rows_1d"], info["n_rows"], info["stencil"]
+
+    def __del__(self):
+        if getattr(self, "handle", None) and _lib is not None:
+            _lib.wgq_free_rules(self.handle)
+            self.handle = None
+
+
+def wgq_build_rules(p, n_elems, dim, boundary_mode=WGQ_BND_GAUSS):
+    return Rules(p, n_elems, dim, boundary_mode)
+
+
+def wgq_rules_info(rules):
+    p, d, st = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    n, N, nr = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    _check("wgq_rules_info", lib().wgq_rules_info(rules.handle, ctypes.byref(p), ctypes.byref(n), ctypes.byref(d),
+                                                  ctypes.byref(N), ctypes.byref(nr), ctypes.byref(st)))
+    return {"p": p.value, "n_elems": n.value, "dim": d.value, "n_rows_1d": N.value, "n_rows": nr.value,
+            "stencil": st.value}
+
+
+def wgq_rules_query(rules, cls, kind):
+    m = ctypes.c_int()
+    tau = (ctypes.c_double * 12)()
+    om = (ctypes.c_double * 12)()
+    res = ctypes.c_double()
+    _check("wgq_rules_query", lib().wgq_rules_query(rules.handle, cls, kind, ctypes.byref(m), tau, om, ctypes.byref(res)))
+    return np.array(tau[:m.value]), np.array(om[:m.value]), res.value
+
+
+def wgq_nnz(rules, row_begin, row_end):
+    out = ctypes.c_int64()
+    _check("wgq_nnz", lib().wgq_nnz(rules.handle, row_begin, row_end, ctypes.byref(out)))
+    return out.value
+
+
+# ---------------------------------------------------------------------------------------
+# descriptors
+# ---------------------------------------------------------------------------------------
+def make_coeff(desc, grid=None, plane0=0):
+    """wgq_coeff_t from a descriptor dict (inputs/configs.py); grid = device tensor."""
+    c = wgq_coeff_t()
+    kind = desc["kind"]
+    keep = []
+    if kind == "const":
+        c.kind = WGQ_COEF_CONST
+        c.c0 = float(desc["c0"])
+    elif kind == "trig_sep":
+        c.kind = WGQ_COEF_TRIG_SEP
+        c.c0 = float(desc["c0"])
+        c.amp = float(desc["amp"])
+        for a, (tr, k) in enumerate(zip(desc["trig"], desc["wavenum"])):
+            c.trig[a] = WGQ_TRIG_SIN if tr == "sin" else WGQ_TRIG_COS
+            c.wavenum[a] = int(k)
+    elif kind == "fourier_logn":
+        c.kind = WGQ_COEF_FOURIER_LOGN
+        modes = np.ascontiguousarray(desc["modes"], dtype=np.float64)
+        c.n_modes = modes.shape[0]
+        buf = (ctypes.c_double * modes.size)(*modes.reshape(-1))
+        keep.append(buf)
+        c.modes = ctypes.cast(buf, ctypes.POINTER(ctypes.c_double))
+    elif kind == "grid":
+        c.kind = WGQ_COEF_GRID
+        if grid is None:
+            raise ValueError("grid coefficient needs a device grid tensor")
+        c.grid = grid.data_ptr()
+        c.grid_plane0 = int(plane0)
+        c.grid_planes = int(grid.shape[0])
+    else:
+        raise ValueError(kind)
+    c._keep = keep
+    return c
+
+
+def make_out(values, row_begin, row_end, ld=None, layout=WGQ_ELL, row_ptr=None):
+    o = wgq_out_t()
+    o.layout = layout
+    o.row_begin, o.row_end = int(row_begin), int(row_end)
+    o.values = values.data_ptr() if values is not None else None
+    o.ld = int(ld if ld is not None else (values.shape[1] if values is not None and values.dim() == 2 else 0))
+    o.row_ptr = row_ptr.data_ptr() if row_ptr is not None else None
+    o.col_idx = None
+    return o
+
+
+# ---------------------------------------------------------------------------------------
+# assembly / inputs / checks
+# ---------------------------------------------------------------------------------------
+def wgq_assemble_mass(rules, coeff, M, stream=None):
+    _check("wgq_assemble_mass", lib().wgq_assemble_mass(rules.handle, ctypes.byref(coeff), ctypes.byref(M), _stream(stream)))
+
+
+def wgq_assemble_stiffness(rules, coeff, K, stream=None):
+    _check("wgq_assemble_stiffness",
+           lib().wgq_assemble_stiffness(rules.handle, ctypes.byref(coeff), ctypes.byref(K), _stream(stream)))
+
+
+def wgq_assemble_mass_stiffness(rules, coeff, M, K, stream=None):
+    _check("wgq_assemble_mass_stiffness",
+           lib().wgq_assemble_mass_stiffness(rules.handle, ctypes.byref(coeff), ctypes.byref(M), ctypes.byref(K),
+                                             _stream(stream)))
+
+
+def wgq_csr_structure(rules, row_begin, row_end, row_ptr, col_idx, stream=None):
+    _check("wgq_csr_structure", lib().wgq_csr_structure(rules.handle, row_begin, row_end, row_ptr.data_ptr(),
+                                                        col_idx.data_ptr() if col_idx is not None else None,
+                                                        _stream(stream)))
+
+
+def wgq_generate_grid(n_elems, dim, seed, sigma, plane0, planes, grid, stream=None):
+    _check("wgq_generate_grid", lib().wgq_generate_grid(n_elems, dim, seed, sigma, plane0, planes, grid.data_ptr(),
+                                                        _stream(stream)))
+
+
+def wgq_row_moments(rules, A, out, stream=None):
+    _check("wgq_row_moments", lib().wgq_row_moments(rules.handle, ctypes.byref(A), out.data_ptr(), _stream(stream)))
+
+
+def wgq_checksum(rules, A, out, stream=None):
+    _check("wgq_checksum", lib().wgq_checksum(rules.handle, ctypes.byref(A), out.data_ptr(), _stream(stream)))
+
+
+def wgq_assemble_host(rules, coeff, row_begin, row_end, M_host, K_host, ld, chunk_rows=0):
+    """Blocking end-to-end call; M_host / K_host are numpy arrays (or None) [rows][ld]."""
+    ptr = (lambda a: a.ctypes.data if a is not None else None)
+    _check("wgq_assemble_host", lib().wgq_assemble_host(rules.handle, ctypes.byref(coeff), row_begin, row_end,
+                                                        ptr(M_host), ptr(K_host), ld, chunk_rows))
+
+
+class PinnedArray:
+    """numpy view of page-locked host memory from wgq_host_alloc (freed on close/del)."""
+
+    def __init__(self, shape, dtype=np.float64):
+        nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        p = ctypes.c_void_p()
+        _check("wgq_host_alloc", lib().wgq_host_alloc(max(nbytes, 8), ctypes.byref(p)))
+        self._ptr = p
+        buf = (ctypes.c_char * max(nbytes, 8)).from_address(p.value)
+        self.array = np.frombuffer(buf, dtype=dtype, count=int(np.prod(shape))).reshape(shape)
+
+    def close(self):
+        if getattr(self, "_ptr", None) is not None and _lib is not None:
+            self.array = None
+            _lib.wgq_host_free(self._ptr)
+            self._ptr = None
+
+    def __del__(self):
+        self.close()

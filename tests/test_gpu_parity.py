@@ -1,0 +1,159 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle, element by element.
+
+Tolerance (north_star, R12): relative Frobenius <= 1e-12 and max entrywise
+relative <= 1e-10 with denominator max(|o|, 1e-14 * max_row |o|).
+"""
+import numpy as np
+import pytest
+
+import inputs
+from oracle import assemble as oasm
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+REL_F = 1e-12
+REL_E = 1e-10
+
+
+def compare(gpu, ref, what=""):
+    gpu = np.asarray(gpu)
+    ref = np.asarray(ref)
+    assert gpu.shape == ref.shape, (what, gpu.shape, ref.shape)
+    nrm = np.linalg.norm(ref)
+    relf = np.linalg.norm(gpu - ref) / (nrm if nrm > 0 else 1.0)
+    rowmax = np.max(np.abs(ref), axis=1, keepdims=True)
+    den = np.maximum(np.abs(ref), 1e-14 * rowmax)
+    den = np.where(den > 0, den, 1.0)
+    rele = np.max(np.abs(gpu - ref) / den)
+    assert relf <= REL_F, (what, relf)
+    assert rele <= REL_E, (what, rele)
+    return relf, rele
+
+
+def coeff_cases(d, n):
+    out = [("const", {"kind": "const", "c0": 1.0}),
+           ("trig", {"kind": "trig_sep", "c0": 1.0, "amp": 0.5, "trig": ("sin", "cos", "sin")[:d], "wavenum": (1, 1, 2)[:d]}),
+           ("fourier", inputs.coefficient({"kind": "fourier_logn", "seed": inputs.SEED, "n_modes": 8, "amp": 0.3}, d)),
+           ("grid", {"kind": "grid", "seed": 3, "sigma": 0.5})]
+    return out
+
+
+def gpu_assemble(p, n, d, desc, kinds=("mass", "stiffness"), row_begin=0, row_end=None, bnd=0, host_grid=None,
+                 plane0=0, ld=None):
+    from paper_1710_01048_b200 import api, wgq
+    rules = wgq.Rules(p, n, d, bnd)
+    grid_t = None
+    if desc["kind"] == "grid":
+        grid_t = torch.from_numpy(np.ascontiguousarray(host_grid)).cuda()
+    c = api.coefficient(desc, grid_t, plane0)
+    out = api.assemble(rules, c, kinds, row_begin, row_end, ld=ld)
+    torch.cuda.synchronize()
+    return {k: v.cpu().numpy() for k, v in out.items()}, rules
+
+
+SMALL = [(2, 1, 64), (3, 1, 33), (2, 2, 13), (3, 2, 11), (2, 3, 7), (3, 3, 6), (3, 3, 3), (2, 2, 2)]
+
+
+@pytest.mark.parametrize("p,d,n", SMALL)
+def test_all_rows_all_coefficients(p, d, n):
+    N = n + p
+    rows = np.arange(N ** d)
+    for name, desc in coeff_cases(d, n):
+        grid = inputs.lognormal_grid(n, seed=desc.get("seed", 1), dim=d) if name == "grid" else None
+        g, _ = gpu_assemble(p, n, d, desc, host_grid=grid)
+        ref = oasm.assemble_rows(p, n, d, rows, desc, grid=grid)
+        for k in ("mass", "stiffness"):
+            compare(g[k], ref[k], (p, d, n, name, k))
+
+
+@pytest.mark.parametrize("p,d,n", [(2, 2, 9), (3, 3, 4)])
+def test_gl_boundary_mode(p, d, n):
+    N = n + p
+    rows = np.arange(N ** d)
+    desc = {"kind": "trig_sep", "c0": 1.0, "amp": 0.5, "trig": ("sin",) * d, "wavenum": (1,) * d}
+    g, _ = gpu_assemble(p, n, d, desc, bnd=1)
+    ref = oasm.assemble_rows(p, n, d, rows, desc, mode="gl")
+    for k in ("mass", "stiffness"):
+        compare(g[k], ref[k], ("gl", k))
+
+
+def test_constant_coefficient_exact_1d_c1():
+    """C1: 1D p=2 n=64 c=1 mass against the exact Galerkin matrix (closed form via scipy)."""
+    from tests.test_oracle_assembly import exact_1d, to_ell
+    g, _ = gpu_assemble(2, 64, 1, {"kind": "const", "c0": 1.0}, kinds=("mass",))
+    M, _ = exact_1d(2, 64)
+    compare(g["mass"], to_ell(M, 2, 64, 1), "C1")
+
+
+def test_slabs_bitwise_equal_and_padded_ld():
+    p, d, n = 3, 3, 7
+    N = n + p
+    desc = {"kind": "grid", "seed": 9, "sigma": 0.5}
+    grid = inputs.lognormal_grid(n, seed=9)
+    full, _ = gpu_assemble(p, n, d, desc, host_grid=grid)
+    b = [0, 7 * N * N, 8 * N * N + 5, N ** 3]            # uneven, ragged slab boundaries
+    for lo, hi in zip(b[:-1], b[1:]):
+        z0, z1 = lo // (N * N), (hi - 1) // (N * N)
+        pl, ph = max(0, z0 - p), min(n, z1 + 1)
+        part, _ = gpu_assemble(p, n, d, desc, row_begin=lo, row_end=hi, host_grid=grid[pl:ph + 1], plane0=pl, ld=344)
+        for k in ("mass", "stiffness"):
+            assert np.array_equal(part[k][:, :343], full[k][lo:hi]), (lo, hi, k)
+
+
+def test_csr_matches_ell():
+    from paper_1710_01048_b200 import api, wgq
+    p, d, n = 2, 3, 5
+    rules = wgq.Rules(p, n, d)
+    desc = {"kind": "trig_sep", "c0": 1.0, "amp": 0.3, "trig": ("sin",) * 3, "wavenum": (1,) * 3}
+    c = api.coefficient(desc)
+    ell = api.assemble(rules, c)
+    lo, hi = 17, rules.n_rows - 11
+    row_ptr, col_idx, vals = api.assemble_csr(rules, c, row_begin=lo, row_end=hi)
+    torch.cuda.synchronize()
+    rp, ci = row_ptr.cpu().numpy(), col_idx.cpu().numpy()
+    for k in ("mass", "stiffness"):
+        e = ell[k].cpu().numpy()
+        v = vals[k].cpu().numpy()
+        for r in range(lo, hi):
+            cols = oasm.ell_columns(p, n, d, r)
+            ok = cols >= 0
+            seg = slice(rp[r - lo], rp[r - lo + 1])
+            assert np.array_equal(ci[seg], cols[ok])
+            assert np.array_equal(v[seg], e[r][ok])
+    assert rp[-1] == wgq.wgq_nnz(rules, lo, hi)
+
+
+@pytest.mark.parametrize("dim,n,plane0,planes", [(3, 16, 0, 17), (3, 20, 5, 9), (2, 40, 3, 20), (1, 30, 0, 31)])
+def test_device_grid_generator_matches_inputs(dim, n, plane0, planes):
+    from paper_1710_01048_b200 import wgq
+    shape = {1: (n + 1,), 2: (planes, n + 1), 3: (planes, n + 1, n + 1)}[dim]
+    g = torch.empty(shape, dtype=torch.float64, device="cuda")
+    wgq.wgq_generate_grid(n, dim, inputs.SEED, 0.5, plane0, planes, g)
+    torch.cuda.synchronize()
+    ref = inputs.lognormal_grid(n, seed=inputs.SEED, dim=dim, plane0=plane0, planes=planes if dim > 1 else None)
+    assert np.max(np.abs(g.cpu().numpy() - ref) / ref) < 1e-14
+
+
+def test_row_moments_identities():
+    """P9 on the GPU output: (K 1)_i = 0 and (M 1)_i = sum_k W^M_ik for all rows."""
+    from paper_1710_01048_b200 import api, wgq
+    p, d, n = 3, 3, 6
+    N = n + p
+    desc = inputs.coefficient({"kind": "fourier_logn", "seed": 5, "n_modes": 8, "amp": 0.3}, 3)
+    rules = wgq.Rules(p, n, d)
+    out = api.assemble(rules, api.coefficient(desc))
+    mom = {}
+    for k in ("mass", "stiffness"):
+        m = torch.empty((N ** d, 1 + d), dtype=torch.float64, device="cuda")
+        wgq.wgq_row_moments(rules, wgq.make_out(out[k], 0, N ** d), m)
+        mom[k] = m.cpu().numpy()
+    rows = np.arange(N ** d)
+    m1, mx, kx = oasm.row_weight_sums(p, n, d, rows, desc)
+    scaleM = np.abs(out["mass"].cpu().numpy()).max(axis=1)
+    scaleK = np.abs(out["stiffness"].cpu().numpy()).max(axis=1)
+    assert np.max(np.abs(mom["mass"][:, 0] - m1) / scaleM) < 1e-13
+    assert np.max(np.abs(mom["stiffness"][:, 0]) / scaleK) < 1e-13
+    for a in range(d):
+        assert np.max(np.abs(mom["mass"][:, 1 + a] - mx[:, a]) / scaleM) < 1e-13
+        assert np.max(np.abs(mom["stiffness"][:, 1 + a] - kx[:, a]) / scaleK) < 1e-13
