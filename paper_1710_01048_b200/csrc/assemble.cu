@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "coef.cuh"
 #include "internal.h"
@@ -75,9 +76,9 @@ __device__ __forceinline__ void stage_term(const GenericArgs& a, const Dir d1, c
         T1[e] = s;
     }
     __syncwarp();
-    // y-stage
+    // y-stage: T2 is laid out [k1][o3][o2] so that o2 + S2*o3 is the slot's (o2,o3) part
     for (int e = lane; e < n1 * S2 * S3; e += 32) {
-        const int o3 = e % S3, o2 = (e / S3) % S2, k1 = e / (S3 * S2);
+        const int o2 = e % S2, o3 = (e / S2) % S3, k1 = e / (S3 * S2);
         double s = accumulate ? T2[e] : 0.0;
         for (int k2 = 0; k2 < n2; ++k2) s = fma(T1[(k1 * n2 + k2) * S3 + o3], d2.A[k2 * kMaxS + o2], s);
         T2[e] = s;
@@ -248,6 +249,11 @@ CoefDev make_coef(const wgq_coeff_t* c) {
 
 int launch_assemble(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, const wgq_out_t* M,
                     const wgq_out_t* K, void* stream) {
+    static const bool force_generic = [] {
+        const char* e = getenv("WGQ_FORCE_GENERIC");
+        return e && e[0] == '1';
+    }();
+    if (!force_generic && line_kernel_applies(R, c, M, K)) return launch_line(R, T, c, M, K, stream);
     GenericArgs a{};
     a.T = T;
     a.coef = make_coef(c);

@@ -15,6 +15,7 @@ constexpr int kMaxS = 2 * kMaxP + 1;   // stencil width per direction
 constexpr int kMaxNodes = 12;          // per direction: GL(p+1) on up to p elements (R1, WGQ_BND_GL)
 constexpr int kMaxMassNodes = kMaxNodes;
 constexpr int kMaxStiffNodes = kMaxNodes;
+constexpr int kMaxV = kMaxP + 2;       // vertex planes touched by one row's support
 
 // One unit-spacing rule of a direction class (paper convention, P:250 / P:351).
 struct ClassRule {
@@ -37,6 +38,13 @@ struct RowTables {
     double* xK = nullptr;      // [N][kMaxStiffNodes]
     double* wK = nullptr;      // [N][kMaxStiffNodes]  omega*B'_r(x)
     double* DK = nullptr;      // [N][kMaxStiffNodes][kMaxS] B'_{r+o}(x_k)
+    // Vertex-projected tables for a multilinear (GRID) coefficient: with b_r = max(0, r-p),
+    //   PM[r][v][o] = sum_k wM[k] B_{r+o}(x_k) lambda_v(x_k),  PK likewise with wK, B',
+    // lambda_v = the hat function of vertex plane b_r + v (v < p+2), i.e. the node's
+    // interpolation weight on that vertex.  sum_v g_{b+v} PM[v][o] is the 1D rule applied
+    // to c * B_{r+o} when c is the vertex field's linear interpolant (R6).
+    double* PM = nullptr;      // [N][kMaxV][kMaxS]
+    double* PK = nullptr;      // [N][kMaxV][kMaxS]
     void* base = nullptr;      // single allocation
 };
 
@@ -58,6 +66,10 @@ namespace wgq {
 
 // rules.cpp (host)
 int build_class_rules(int p, int bnd, ClassRule out[2][kMaxP + 1]);
+// Unit-spacing vertex-projected tables of the interior (shift-invariant) rule:
+// PM[v][o] = sum_k omega_k B(tau_k) B_o(tau_k) lambda_v(tau_k) (mass), PK with B' (stiffness).
+void interior_vertex_tables(int p, const ClassRule& mass, const ClassRule& stiff, double PM[kMaxV][kMaxS],
+                            double PK[kMaxV][kMaxS]);
 
 // tables.cu
 int build_row_tables(const wgq_rules_s* R, RowTables* T, void* stream);
@@ -70,6 +82,11 @@ int launch_csr_structure(const wgq_rules_s* R, int64_t row_begin, int64_t row_en
                          int64_t* row_ptr, int32_t* col_idx, void* stream);
 int launch_row_moments(const wgq_rules_s* R, const wgq_out_t* A, double* out, void* stream);
 int launch_checksum(const wgq_rules_s* R, const wgq_out_t* A, unsigned long long* out, void* stream);
+
+// assemble_line.cu (GRID coefficient, d = 3, ELL)
+bool line_kernel_applies(const wgq_rules_s* R, const wgq_coeff_t* c, const wgq_out_t* M, const wgq_out_t* K);
+int launch_line(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, const wgq_out_t* M,
+                const wgq_out_t* K, void* stream);
 
 // grid.cu
 int launch_generate_grid(int64_t n, int dim, uint64_t seed, double sigma, int64_t plane0,

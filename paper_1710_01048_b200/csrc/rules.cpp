@@ -419,6 +419,31 @@ int boundary_rule(int p, int j, int kind, int bnd, ClassRule& R) {
 
 }  // namespace
 
+void interior_vertex_tables(int p, const ClassRule& mass, const ClassRule& stiff, double PM[kMaxV][kMaxS],
+                            double PK[kMaxV][kMaxS]) {
+    // reference knots, cardinal weight j = 2p with support [p, 2p+1]; neighbours j+o
+    Knots K = unit_open_knots(p, 4 * p + 2);
+    const int j = 2 * p;
+    for (int v = 0; v < kMaxV; ++v)
+        for (int o = 0; o < kMaxS; ++o) PM[v][o] = PK[v][o] = 0.0;
+    for (int kind = 0; kind < 2; ++kind) {
+        const ClassRule& R = kind == 0 ? mass : stiff;
+        double (*P)[kMaxS] = kind == 0 ? PM : PK;
+        for (int k = 0; k < R.m; ++k) {
+            const double t = R.tau[k];
+            const int e = (int)std::floor(t);                 // element of the node (inside it)
+            const double f = t - e;
+            const double x = p + t;
+            const double w = R.omega[k] * bval(K, j, x, kind);
+            for (int o = -p; o <= p; ++o) {
+                const double a = w * bval(K, j + o, x, kind);
+                P[e][o + p] += (1.0 - f) * a;
+                P[e + 1][o + p] += f * a;
+            }
+        }
+    }
+}
+
 int build_class_rules(int p, int bnd, ClassRule out[2][kMaxP + 1]) {
     int rc;
     if (p == 2) {

@@ -137,11 +137,42 @@ __global__ void k_row_tables(ClassArgs A, RowTables T) {
     W[r * maxn + k] = om * row[p];        // omega * B_r(x) or omega * B'_r(x)
 }
 
+// Vertex-projected tables: one thread per (row, kind, v, o).
+__global__ void k_vertex_tables(int p, int64_t n, RowTables T) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int per_row = 2 * kMaxV * kMaxS;
+    const int64_t r = tid / per_row;
+    if (r >= T.N) return;
+    const int rem = (int)(tid % per_row);
+    const int kind = rem / (kMaxV * kMaxS);
+    const int v = (rem / kMaxS) % kMaxV;
+    const int o = rem % kMaxS;
+    const int m = kind == WGQ_MASS ? T.mM[r] : T.mK[r];
+    const double* X = (kind == WGQ_MASS ? T.xM : T.xK) + r * kMaxNodes;
+    const double* W = (kind == WGQ_MASS ? T.wM : T.wK) + r * kMaxNodes;
+    const double* A = (kind == WGQ_MASS ? T.VM : T.DK) + r * kMaxNodes * kMaxS;
+    const int64_t b = r - p > 0 ? r - p : 0;
+    double acc = 0.0;
+    for (int k = 0; k < m; ++k) {
+        const double s = X[k] * (double)n;
+        int64_t e = (int64_t)floor(s);
+        e = e < 0 ? 0 : (e > n - 1 ? n - 1 : e);
+        const double f = s - (double)e;
+        const int64_t rel = e - b;
+        double lam = 0.0;
+        if (rel == v) lam = 1.0 - f;
+        else if (rel + 1 == v) lam = f;
+        acc = fma(lam * W[k], A[k * kMaxS + o], acc);
+    }
+    (kind == WGQ_MASS ? T.PM : T.PK)[(r * kMaxV + v) * kMaxS + o] = acc;
+}
+
 }  // namespace
 
 int build_row_tables(const wgq_rules_s* R, RowTables* T, void* stream) {
     const int64_t N = R->N;
-    size_t bytes = 2 * N * sizeof(int) + N * (kMaxMassNodes * (2 + kMaxS) + kMaxStiffNodes * (2 + kMaxS)) * sizeof(double);
+    size_t bytes = 2 * N * sizeof(int) +
+                   N * (kMaxMassNodes * (2 + kMaxS) + kMaxStiffNodes * (2 + kMaxS) + 2 * kMaxV * kMaxS) * sizeof(double);
     bytes += 256;
     void* base = nullptr;
     if (cudaMalloc(&base, bytes) != cudaSuccess) return WGQ_ECUDA;
@@ -154,6 +185,8 @@ int build_row_tables(const wgq_rules_s* R, RowTables* T, void* stream) {
     T->xK = d; d += N * kMaxStiffNodes;
     T->wK = d; d += N * kMaxStiffNodes;
     T->DK = d; d += N * kMaxStiffNodes * kMaxS;
+    T->PM = d; d += N * kMaxV * kMaxS;
+    T->PK = d; d += N * kMaxV * kMaxS;
     T->mM = (int*)d;
     T->mK = T->mM + N;
     T->maxM = T->maxK = 0;
@@ -175,6 +208,8 @@ int build_row_tables(const wgq_rules_s* R, RowTables* T, void* stream) {
         }
     const int64_t threads = N * 2 * kMaxStiffNodes;
     k_row_tables<<<(unsigned)((threads + 255) / 256), 256, 0, (cudaStream_t)stream>>>(A, *T);
+    const int64_t vthreads = N * 2 * kMaxV * kMaxS;
+    k_vertex_tables<<<(unsigned)((vthreads + 255) / 256), 256, 0, (cudaStream_t)stream>>>(R->p, R->n, *T);
     if (cudaGetLastError() != cudaSuccess) return WGQ_ECUDA;
     return WGQ_OK;
 }
