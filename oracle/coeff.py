@@ -27,15 +27,20 @@ def evaluate(desc, n, pts, grid=None, plane0=0):
             prod = prod * f(2.0 * math.pi * desc["wavenum"][a] * pts[a])
         return desc["c0"] + desc["amp"] * prod
     if kind == "fourier_logn":
-        s = np.zeros(np.shape(pts[0]))
+        # Evaluated in x87 extended precision (64-bit mantissa) and rounded once: the phase
+        # 2 pi (k . x) reaches ~100, where a double-precision phase would carry ~1e-14
+        # absolute error and make the oracle's own c wrong beyond the parity tolerance.
+        ld = np.longdouble
+        two_pi = ld(2) * ld("3.14159265358979323846264338327950288")
+        s = np.zeros(np.shape(pts[0]), dtype=ld)
         for a_m, kx, ky, kz, th in desc["modes"]:
-            arg = kx * pts[0]
+            arg = ld(kx) * np.asarray(pts[0], dtype=ld)
             if d > 1:
-                arg = arg + ky * pts[1]
+                arg = arg + ld(ky) * np.asarray(pts[1], dtype=ld)
             if d > 2:
-                arg = arg + kz * pts[2]
-            s = s + a_m * np.cos(2.0 * math.pi * arg + th)
-        return np.exp(s)
+                arg = arg + ld(kz) * np.asarray(pts[2], dtype=ld)
+            s = s + ld(a_m) * np.cos(two_pi * arg + ld(th))
+        return np.exp(s).astype(np.float64)
     if kind == "grid":
         return _multilinear(grid, n, pts, plane0)
     raise ValueError(kind)

@@ -80,7 +80,7 @@ def test_gl_boundary_mode(p, d, n):
 
 def test_constant_coefficient_exact_1d_c1():
     """C1: 1D p=2 n=64 c=1 mass against the exact Galerkin matrix (closed form via scipy)."""
-    from tests.test_oracle_assembly import exact_1d, to_ell
+    from wgq_exact import exact_1d, to_ell
     g, _ = gpu_assemble(2, 64, 1, {"kind": "const", "c0": 1.0}, kinds=("mass",))
     M, _ = exact_1d(2, 64)
     compare(g["mass"], to_ell(M, 2, 64, 1), "C1")
