@@ -139,6 +139,56 @@ def _newton(evaluate, param, u0, brackets, iters=40, tol=2e-16):
     return u, nr
 
 
+def _polish(t, p, j, order, rows, param, u, dps=40):
+    """Refine a converged fp64 root of the same system in mpmath (``dps`` digits) and round
+    it once, so that the rule is correctly rounded rather than accurate to the fp64 residual
+    floor times the system's condition number (R14)."""
+    import mpmath as mp
+    with mp.workdps(dps):
+        tk = [mp.mpf(float(v)) for v in t]
+        lo = tk[j]
+        hi = tk[j + p + 1]
+
+        def moment(i):
+            total = mp.mpf(0)
+            for s in range(len(tk) - 1):
+                a, b = tk[s], tk[s + 1]
+                if b > a and a >= lo and b <= hi:
+                    total += mp.quad(lambda x: spline.deriv_scalar(tk, i, p, x, order) *
+                                     spline.deriv_scalar(tk, j, p, x, order), [a, b])
+            return total
+
+        mu = [moment(i) for i in rows]
+        Tm = [[mp.mpf(float(v)) for v in r] for r in param.Tm]
+        Wm = [[mp.mpf(float(v)) for v in r] for r in param.Wm]
+        tb = [mp.mpf(float(v)) for v in param.tb]
+        wb = [mp.mpf(float(v)) for v in param.wb]
+
+        def F(*uu):
+            tau = [sum(Tm[k][q] * uu[q] for q in range(len(uu))) + tb[k] for k in range(len(tb))]
+            om = [sum(Wm[k][q] * uu[q] for q in range(len(uu))) + wb[k] for k in range(len(wb))]
+            res = []
+            for ri, i in enumerate(rows):
+                acc = mp.mpf(0)
+                for k in range(len(tau)):
+                    x = lo + tau[k]
+                    acc += om[k] * spline.deriv_scalar(tk, i, p, x, order) * spline.deriv_scalar(tk, j, p, x, order)
+                res.append(acc - mu[ri])
+            return res
+
+        x0 = [mp.mpf(float(v)) for v in u]
+        sol = mp.findroot(F, x0, solver="mdnewton", tol=mp.mpf(10) ** (-2 * dps + 12), maxsteps=60)
+        sol = [sol] if len(u) == 1 else list(sol)
+        return np.array([float(v) for v in sol])
+
+
+def _polished(t, p, j, order, rows, param, u):
+    v = _polish(t, p, j, order, rows, param, u)
+    if np.max(np.abs(v - u)) > 1e-12:
+        raise RuntimeError("high-precision refinement moved the root: %s -> %s" % (u, v))
+    return v
+
+
 def full_residual(rule, t=None):
     """max_i |sum_k omega_k F_i(tau_k) W(tau_k) - mu_i| over the FULL interacting set."""
     p = rule.p
@@ -168,6 +218,7 @@ def interior_mass_p2():
     param = _Param(Tm=[[1, 0, 0], [0, 0, 0], [-1, 0, 0]], tb=[0, 1.5, 3.0],
                    Wm=[[0, 1, 0], [0, 0, 1], [0, 1, 0]], wb=[0, 0, 0])
     u, nr = _newton(ev, param, [0.5, 1.0, 1.0], {0: (0.0, 1.0)})
+    u = _polished(t, p, j, 0, [j - 2, j - 1, j], param, u)
     rule = Rule("mass", p, "interior", param.tau(u), param.omega(u), 0.0, "eq:WQquadratic")
     rule.residual = full_residual(rule)
     return rule
@@ -190,6 +241,8 @@ def interior_mass_p3(starts=None):
         u, nr = _newton(ev, param, s, {0: (0.0, 1.0), 1: (1.0, 2.0)})
         tau, om = param.tau(u), param.omega(u)
         if nr < 1e-13 and 0 < tau[0] < 1 and 1 < tau[1] < 2 and np.all(om > 0):
+            u = _polished(t, p, j, 0, [j - 3, j - 2, j - 1, j], param, u)
+            tau, om = param.tau(u), param.omega(u)
             rule = Rule("mass", p, "interior", tau, om, 0.0, "eq:WQcubic")
             rule.residual = full_residual(rule)
             return rule
@@ -207,6 +260,7 @@ def interior_stiff_p2(omega2=8.0 / 9.0):
     param = _Param(Tm=[[1, 0], [0, 0], [-1, 0]], tb=[0, 1.5, 3.0],
                    Wm=[[0, 1], [0, 0], [0, 1]], wb=[0, omega2, 0])
     u, nr = _newton(ev, param, [0.5, 1.0], {0: (0.0, 1.0)})
+    u = _polished(t, p, j, 1, [j - 2, j - 1], param, u)
     rule = Rule("stiffness", p, "interior", param.tau(u), param.omega(u), 0.0, "eq:WQquadraticStiff")
     rule.residual = full_residual(rule)
     return rule
@@ -238,6 +292,11 @@ def interior_stiff_p3(omega1=1.0):
         u, nr = _newton(ev, param, [1.5 + a, 1.0], {0: (1.0, 2.0)})
         tau, om = param.tau(u), param.omega(u)
         if nr < 1e-13 and 1 < tau[1] < 2 and np.all(om > 0):
+            # refine tau1 (line 1 = the quartic), tau2, omega2 together (lines 1, 2, 4)
+            pfull = _Param(Tm=[[1, 0, 0], [0, 1, 0], [0, -1, 0], [-1, 0, 0]], tb=[0, 0, 4, 4],
+                           Wm=[[0, 0, 0], [0, 0, 1], [0, 0, 1], [0, 0, 0]], wb=[omega1, 0, 0, omega1])
+            v = _polished(t, p, j, 1, [j - 3, j - 2, j], pfull, np.array([tau1, u[0], u[1]]))
+            tau, om = pfull.tau(v), pfull.omega(v)
             rule = Rule("stiffness", p, "interior", tau, om, 0.0, "eq:WQcubicStiff")
             rule.residual = full_residual(rule)
             return rule
@@ -260,11 +319,18 @@ def gl_rule(kind, p, j):
     """Standard Gauss rule on the support (the paper's alternative): (p+1)-point
     Gauss-Legendre on every element of [0, j+1]; omega are the GL weights (the rule then
     integrates f*W exactly for every polynomial f*W of degree <= 2p+1 per element)."""
+    import mpmath as mp
     tau, om = [], []
+    m = p + 1
     for e in range(j + 1):
-        x, w = quadrature.gauss_legendre(p + 1, float(e), float(e + 1))
-        tau.extend(x)
-        om.extend(w)
+        x, w = quadrature.gauss_legendre(m, float(e), float(e + 1))
+        # refine each node as a root of P_m(2x - 1) in 40 digits; w = 1/((1-s^2) P_m'(s)^2)
+        with mp.workdps(40):
+            for xi in x:
+                s = mp.findroot(lambda z: mp.legendre(m, z), mp.mpf(2 * (float(xi) - e) - 1))
+                dP = mp.diff(lambda z: mp.legendre(m, z), s)
+                tau.append(float(e + (s + 1) / 2))
+                om.append(float(1 / ((1 - s * s) * dP * dP)))
     rule = Rule(kind, p, ("left", j), tau, om, 0.0, "GL(p+1) per element")
     rule.residual = full_residual(rule)
     return rule
@@ -316,6 +382,9 @@ def boundary_gauss(kind, p, j, grid_points=7):
     if not roots:
         return None, 0
     tau, om = roots[0]
+    u = np.concatenate([tau[:nfree], om])
+    u = _polished(t, p, j, order, rows, param, u)
+    tau, om = param.tau(u), param.omega(u)
     rule = Rule(kind, p, ("left", j), tau, om, 0.0, "boundary Gauss (R1)")
     rule.residual = full_residual(rule)
     return rule, len(roots)

@@ -79,3 +79,35 @@ def support(t, i, k):
 def interacting(p, n, j):
     """Indices i with |supp B_i cap supp B_j| > 0: {j-p..j+p} clipped to [0, dim)."""
     return [i for i in range(j - p, j + p + 1) if 0 <= i < dim(p, n)]
+
+
+def basis_scalar(t, i, k, x):
+    """Cox-de Boor for one scalar x of any real type (float or mpmath.mpf); same
+    conventions as ``basis`` (used to refine the rules in high precision)."""
+    if k == 0:
+        lo, hi = t[i], t[i + 1]
+        if hi <= lo:
+            return 0 * x
+        if lo <= x < hi or (x == hi and hi == t[-1]):
+            return 0 * x + 1
+        return 0 * x
+    out = 0 * x
+    if t[i + k] != t[i]:
+        out += (x - t[i]) / (t[i + k] - t[i]) * basis_scalar(t, i, k - 1, x)
+    if t[i + k + 1] != t[i + 1]:
+        out += (t[i + k + 1] - x) / (t[i + k + 1] - t[i + 1]) * basis_scalar(t, i + 1, k - 1, x)
+    return out
+
+
+def deriv_scalar(t, i, k, x, order=1):
+    """order-th derivative of B_{i,k} at a scalar x of any real type."""
+    if order == 0:
+        return basis_scalar(t, i, k, x)
+    if k == 0:
+        return 0 * x
+    out = 0 * x
+    if t[i + k] != t[i]:
+        out += k / (t[i + k] - t[i]) * deriv_scalar(t, i, k - 1, x, order - 1)
+    if t[i + k + 1] != t[i + 1]:
+        out -= k / (t[i + k + 1] - t[i + 1]) * deriv_scalar(t, i + 1, k - 1, x, order - 1)
+    return out

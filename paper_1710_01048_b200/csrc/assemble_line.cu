@@ -14,10 +14,12 @@
 //   HK[v][o2,o3]  = sum_{vy,vz} g[..][..][v] (PKy PMz + PMy PKz)
 // are computed once per line (phase A, ~1 plane per row) and each row finishes with
 //   M[o1,o23] = sum_vx PMx[vx][o1] HM[bx+vx][o23],  K = sum_vx PKx HM + PMx HK     (phase B)
-// Interior x-rows (class I) share one table P^ (scaled by h, 1/h) that lives in __constant__
-// memory, so phase B is FP64 FMAs with constant operands plus two LDS per output group.
-// A CTA owns a line, walks it in tiles of TR rows, stages the tile's M and K rows in shared
-// memory (double-buffered) and writes each tile with one cp.async.bulk per matrix.
+// Interior x-rows (class I) share one table P^ (times h resp. 1/h) that lives in __constant__
+// memory; its zero pattern is structural (a node in element k touches planes k, k+1 and
+// columns k..k+p), so phase B issues only the structurally nonzero FP64 FMAs, with constant
+// operands, plus 2 LDS per output group.  A CTA owns a line, walks it in tiles of TR rows,
+// prefetches the next tile's vertex patch with cp.async, stages the tile's M and K rows in
+// shared memory (double-buffered) and writes each tile with one cp.async.bulk per matrix.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -44,18 +46,20 @@ struct Cfg {
     static constexpr int RING = 16;                    // H ring (>= MAXNEW), power of two
     static constexpr int SR = S3 + 1;                  // staging row stride for padded ld
     static constexpr int STAGE = TR * SR + 2;          // doubles per staging buffer per matrix
-    static constexpr int SMEM = 4 * STAGE + RING * 2 * S2 + 4 * V * S + MAXNEW * V * V + 2 * MAXNEW * V * S;
+    static constexpr int PATCH = MAXNEW * V * V;
+    static constexpr int SMEM = 4 * STAGE + RING * 2 * S2 + 4 * V * S + 2 * PATCH + 2 * MAXNEW * V * S;
+    static_assert(MAXNEW <= RING, "ring too small");
 };
 
 struct LineArgs {
     RowTables T;
     const double* grid;
-    int64_t plane0, planes;
-    int64_t n, N;
-    int64_t row_begin, row_end;
+    int plane0, planes;
+    int n, N;
+    int row_begin, row_end;
     double* M;
     double* K;
-    int64_t ld;
+    long long ld;
     int do_mass, do_stiff;
     double h, inv_h;
 };
@@ -64,6 +68,11 @@ __device__ __forceinline__ void bulk_store(double* gdst, const double* ssrc, uin
     const uint32_t s = (uint32_t)__cvta_generic_to_shared(ssrc);
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(s), "r"(bytes)
                  : "memory");
+}
+
+__device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc, bool valid) {
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(gsrc), "r"(valid ? 8 : 0) : "memory");
 }
 
 template <int P>
@@ -77,6 +86,23 @@ __device__ __forceinline__ double cPK(int v, int o) {
     else return c_PK2[v][o];
 }
 
+// Issue the vertex patch of planes [c0, c0+nnew) of the line (by, bz): patch[j][vz][vy].
+template <int P>
+__device__ __forceinline__ void load_patch(const LineArgs& a, double* patch, int c0, int nnew, int by, int bz,
+                                           int tid) {
+    using C = Cfg<P>;
+    constexpr int V = C::V;
+    const int nv = a.n + 1;
+    for (int e = tid; e < nnew * V * V; e += C::NT) {
+        const int j = e % nnew, vy = (e / nnew) % V, vz = e / (nnew * V);
+        const int x = c0 + j, y = by + vy, z = bz + vz;
+        const bool ok = x <= a.n && y <= a.n && z <= a.n && z - a.plane0 < a.planes;
+        const double* src = ok ? a.grid + ((size_t)(z - a.plane0) * nv + y) * nv + x : a.grid;
+        cp_async8(patch + (j * V + vz) * V + vy, src, ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
 template <int P>
 __global__ void __launch_bounds__(Cfg<P>::NT, 2) k_line_grid3(const LineArgs a) {
     using C = Cfg<P>;
@@ -86,8 +112,8 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 2) k_line_grid3(const LineArgs a) 
     double* Hm = stage + 4 * C::STAGE;                    // [RING][S2]
     double* Hk = Hm + RING * S2;                          // [RING][S2]
     double* Q = Hk + RING * S2;                           // QyM, QyK, QzM, QzK: [V][S] each
-    double* patch = Q + 4 * V * S;                        // [MAXNEW][V(z)][V(y)]
-    double* TM = patch + C::MAXNEW * V * V;               // [MAXNEW][V(z)][S(o2)]
+    double* patches = Q + 4 * V * S;                      // [2][MAXNEW][V(z)][V(y)]
+    double* TM = patches + 2 * C::PATCH;                  // [MAXNEW][V(z)][S(o2)]
     double* TK = TM + C::MAXNEW * V * S;
     const double* QyM = Q;
     const double* QyK = Q + V * S;
@@ -95,103 +121,103 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 2) k_line_grid3(const LineArgs a) 
     const double* QzK = Q + 3 * V * S;
 
     const int tid = threadIdx.x;
-    const int64_t n = a.n, N = a.N, nv = n + 1;
+    const int n = a.n, N = a.N;
     const bool padded = a.ld != S3;
     const int SRr = padded ? C::SR : S3;
-    const int64_t first_line = a.row_begin / N, last_line = (a.row_end - 1) / N;
-    int tiles = 0;
+    const int first_line = a.row_begin / N, last_line = (a.row_end - 1) / N;
+    int tiles = 0, pbuf = 0;
 
-    for (int64_t line = first_line + blockIdx.x; line <= last_line; line += gridDim.x) {
-        const int64_t i2 = line % N, i3 = line / N;
-        const int64_t x0 = max(a.row_begin, line * N) - line * N;
-        const int64_t x1 = min(a.row_end, line * N + N) - line * N;
-        const int64_t by = i2 - P > 0 ? i2 - P : 0, bz = i3 - P > 0 ? i3 - P : 0;
-        __syncthreads();                                   // previous line done with Q / H
+    for (int line = first_line + blockIdx.x; line <= last_line; line += gridDim.x) {
+        const int i2 = line % N, i3 = line / N;
+        const int x0 = max(a.row_begin, line * N) - line * N;
+        const int x1 = min(a.row_end, line * N + N) - line * N;
+        const int by = max(0, i2 - P), bz = max(0, i3 - P);
+        __syncthreads();                                   // previous line done with Q / H / patches
         for (int e = tid; e < 4 * V * S; e += C::NT) {
             const int which = e / (V * S), v = (e / S) % V, o = e % S;
-            const int64_t r = which < 2 ? i2 : i3;
+            const int r = which < 2 ? i2 : i3;
             const double* src = (which & 1) ? a.T.PK : a.T.PM;
-            Q[e] = src[(r * kMaxV + v) * kMaxS + o];
+            Q[e] = src[((size_t)r * kMaxV + v) * kMaxS + o];
         }
-        int64_t hcomp = -1;                                // vertex planes computed: (hcomp-RING, hcomp]
-        for (int64_t t0 = x0; t0 < x1; t0 += TR) {
-            const int tr = (int)min((int64_t)TR, x1 - t0);
-            const int64_t lo_need = t0 - P > 0 ? t0 - P : 0;
-            const int64_t last = t0 + tr - 1;
-            const int64_t hi_need = (last - P > 0 ? last - P : 0) + V - 1;
-            if (hcomp < lo_need - 1) hcomp = lo_need - 1;
-            if (hcomp < hi_need) {
-                // ---- phase A: new vertex planes c0..hi_need -> HM, HK --------------------
-                const int64_t c0 = hcomp + 1;
-                const int nnew = (int)(hi_need - hcomp);
-                __syncthreads();                           // Q visible; ring slots free
-                for (int e = tid; e < nnew * V * V; e += C::NT) {
-                    const int j = e % nnew, vy = (e / nnew) % V, vz = e / (nnew * V);
-                    const int64_t x = c0 + j, y = by + vy, z = bz + vz;
-                    double g = 0.0;
-                    if (x <= n && y <= n && z <= n && z - a.plane0 < a.planes)
-                        g = __ldg(a.grid + ((z - a.plane0) * nv + y) * nv + x);
-                    patch[(j * V + vz) * V + vy] = g;
-                }
-                __syncthreads();
-                for (int e = tid; e < nnew * V * S; e += C::NT) {
-                    const int o2 = e % S, vz = (e / S) % V, j = e / (S * V);
-                    const double* pr = patch + (j * V + vz) * V;
-                    double sm_ = 0.0, sk = 0.0;
+        int hcomp = max(0, x0 - P) - 1;                     // vertex planes computed: (hcomp-RING, hcomp]
+        // first tile's patch (later tiles are prefetched one tile ahead)
+        {
+            const int last = min(x0 + TR, x1) - 1;
+            const int hi = max(0, last - P) + V - 1;
+            load_patch<P>(a, patches + pbuf * C::PATCH, hcomp + 1, hi - hcomp, by, bz, tid);
+        }
+        for (int t0 = x0; t0 < x1; t0 += TR) {
+            const int tr = min(TR, x1 - t0);
+            const int hi_need = max(0, t0 + tr - 1 - P) + V - 1;
+            const int c0 = hcomp + 1;
+            const int nnew = hi_need - hcomp;              // >= 1: the window moves every tile
+            const double* patch = patches + pbuf * C::PATCH;
+            // ---- phase A: new vertex planes c0..hi_need -> HM, HK --------------------------
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            __syncthreads();                               // patch + Q visible; ring slots free
+            for (int e = tid; e < nnew * V * S; e += C::NT) {
+                const int o2 = e % S, vz = (e / S) % V, j = e / (S * V);
+                const double* pr = patch + (j * V + vz) * V;
+                double sm_ = 0.0, sk = 0.0;
 #pragma unroll
-                    for (int vy = 0; vy < V; ++vy) {
-                        sm_ = fma(pr[vy], QyM[vy * S + o2], sm_);
-                        sk = fma(pr[vy], QyK[vy * S + o2], sk);
-                    }
-                    TM[(j * V + vz) * S + o2] = sm_;
-                    TK[(j * V + vz) * S + o2] = sk;
+                for (int vy = 0; vy < V; ++vy) {
+                    sm_ = fma(pr[vy], QyM[vy * S + o2], sm_);
+                    sk = fma(pr[vy], QyK[vy * S + o2], sk);
                 }
-                __syncthreads();
-                for (int e = tid; e < nnew * S2; e += C::NT) {
-                    const int o23 = e % S2, j = e / S2, o2 = o23 % S, o3 = o23 / S;
-                    const double* tm = TM + j * V * S + o2;
-                    const double* tk = TK + j * V * S + o2;
-                    double hm = 0.0, hk = 0.0;
-#pragma unroll
-                    for (int vz = 0; vz < V; ++vz) {
-                        hm = fma(tm[vz * S], QzM[vz * S + o3], hm);
-                        hk = fma(tk[vz * S], QzM[vz * S + o3], hk);
-                        hk = fma(tm[vz * S], QzK[vz * S + o3], hk);
-                    }
-                    const int slot = (int)((c0 + j) & (RING - 1));
-                    Hm[slot * S2 + o23] = hm;
-                    Hk[slot * S2 + o23] = hk;
-                }
-                hcomp = hi_need;
+                TM[(j * V + vz) * S + o2] = sm_;
+                TK[(j * V + vz) * S + o2] = sk;
             }
-            // ---- phase B: rows of the tile -> staging ------------------------------------
+            if (t0 + TR < x1) {                            // prefetch the next tile's patch
+                const int nlast = min(t0 + 2 * TR, x1) - 1;
+                const int nhi = max(0, nlast - P) + V - 1;
+                load_patch<P>(a, patches + (pbuf ^ 1) * C::PATCH, hi_need + 1, nhi - hi_need, by, bz, tid);
+            }
+            __syncthreads();
+            for (int e = tid; e < nnew * S2; e += C::NT) {
+                const int o23 = e % S2, j = e / S2, o2 = o23 % S, o3 = o23 / S;
+                const double* tm = TM + j * V * S + o2;
+                const double* tk = TK + j * V * S + o2;
+                double hm = 0.0, hk = 0.0;
+#pragma unroll
+                for (int vz = 0; vz < V; ++vz) {
+                    hm = fma(tm[vz * S], QzM[vz * S + o3], hm);
+                    hk = fma(tk[vz * S], QzM[vz * S + o3], hk);
+                    hk = fma(tm[vz * S], QzK[vz * S + o3], hk);
+                }
+                const int slot = (c0 + j) & (RING - 1);
+                Hm[slot * S2 + o23] = hm;
+                Hk[slot * S2 + o23] = hk;
+            }
+            hcomp = hi_need;
+            pbuf ^= 1;
+            // ---- phase B: rows of the tile -> staging --------------------------------------
             const int buf = tiles & 1;
             if (tiles >= 2 && tid == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
             __syncthreads();                               // H ready; staging buffer free
-            const int64_t orow0 = line * N + t0 - a.row_begin;     // output row of the tile
-            const int64_t g0 = orow0 * a.ld;                       // first element (doubles)
+            const long long orow0 = (long long)line * N + t0 - a.row_begin;   // output row of the tile
+            const long long g0 = orow0 * a.ld;                                // first element
             const int pad = padded ? 0 : (int)(g0 & 1);
             double* stM = stage + (buf * 2 + 0) * C::STAGE + pad;
             double* stK = stage + (buf * 2 + 1) * C::STAGE + pad;
-            for (int it = tid; it < tr * S2; it += C::NT) {
-                const int j = it / S2, o23 = it % S2;
-                const int64_t r = t0 + j;
-                const int64_t bx = r - P > 0 ? r - P : 0;
+            if (tid < tr * S2) {
+                const int j = tid / S2, o23 = tid % S2;
+                const int r = t0 + j;
+                const int bx = max(0, r - P);
                 double hm[V], hk[V];
 #pragma unroll
                 for (int v = 0; v < V; ++v) {
-                    const int slot = (int)((bx + v) & (RING - 1));
+                    const int slot = (bx + v) & (RING - 1);
                     hm[v] = Hm[slot * S2 + o23];
                     hk[v] = Hk[slot * S2 + o23];
                 }
                 double* dM = stM + j * SRr + S * o23;
                 double* dK = stK + j * SRr + S * o23;
-                if (r >= 2 * P && r <= n - 1 - P) {       // class I: constant tables
+                if (r >= 2 * P && r <= n - 1 - P) {       // class I: constant tables, structural zeros skipped
 #pragma unroll
                     for (int o1 = 0; o1 < S; ++o1) {
                         double s = 0.0, s1 = 0.0, s2 = 0.0;
 #pragma unroll
-                        for (int v = 0; v < V; ++v) {
+                        for (int v = (o1 - P > 0 ? o1 - P : 0); v <= (o1 + 1 < P + 1 ? o1 + 1 : P + 1); ++v) {
                             s = fma(cPM<P>(v, o1), hm[v], s);
                             s1 = fma(cPK<P>(v, o1), hm[v], s1);
                             s2 = fma(cPM<P>(v, o1), hk[v], s2);
@@ -200,8 +226,8 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 2) k_line_grid3(const LineArgs a) 
                         if (a.do_stiff) dK[o1] = fma(a.h, s2, s1 * a.inv_h) + 0.0;
                     }
                 } else {                                   // boundary-affected x-row: its own tables
-                    const double* pm = a.T.PM + r * kMaxV * kMaxS;
-                    const double* pk = a.T.PK + r * kMaxV * kMaxS;
+                    const double* pm = a.T.PM + (size_t)r * kMaxV * kMaxS;
+                    const double* pk = a.T.PK + (size_t)r * kMaxV * kMaxS;
 #pragma unroll
                     for (int o1 = 0; o1 < S; ++o1) {
                         double s = 0.0, s1 = 0.0;
@@ -219,34 +245,37 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 2) k_line_grid3(const LineArgs a) 
             }
             __syncthreads();
             // ---- store the tile: bulk copies of the 16-byte aligned interior, peeled ends ----
-            for (int mat = 0; mat < 2; ++mat) {
-                if (mat == 0 ? !a.do_mass : !a.do_stiff) continue;
-                double* out = mat == 0 ? a.M : a.K;
-                const double* st = mat == 0 ? stM : stK;
-                if (!padded) {
-                    const int total = tr * S3;
-                    const int head = (int)(g0 & 1);
-                    const int tail = (int)((g0 + total) & 1);
-                    if (tid == 0) {
-                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                        bulk_store(out + g0 + head, st + head, (uint32_t)(total - head - tail) * 8u);
-                    } else if (tid == 32 && head) {
-                        out[g0] = st[0];
-                    } else if (tid == 64 && tail) {
-                        out[g0 + total - 1] = st[total - 1];
+            if (!padded) {
+                const int total = tr * S3;
+                const int head = (int)(g0 & 1);
+                const int tail = (int)((g0 + total) & 1);
+                if (tid == 0) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    if (a.do_mass) bulk_store(a.M + g0 + head, stM + head, (uint32_t)(total - head - tail) * 8u);
+                    if (a.do_stiff) bulk_store(a.K + g0 + head, stK + head, (uint32_t)(total - head - tail) * 8u);
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                } else if (tid == 32 && head) {
+                    if (a.do_mass) a.M[g0] = stM[0];
+                    if (a.do_stiff) a.K[g0] = stK[0];
+                } else if (tid == 64 && tail) {
+                    if (a.do_mass) a.M[g0 + total - 1] = stM[total - 1];
+                    if (a.do_stiff) a.K[g0 + total - 1] = stK[total - 1];
+                }
+            } else {                                       // even ld: rows start 16B-aligned
+                if (tid == 0) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    for (int j = 0; j < tr; ++j) {
+                        if (a.do_mass) bulk_store(a.M + (orow0 + j) * a.ld, stM + j * SRr, (uint32_t)(S3 - 1) * 8u);
+                        if (a.do_stiff) bulk_store(a.K + (orow0 + j) * a.ld, stK + j * SRr, (uint32_t)(S3 - 1) * 8u);
                     }
-                } else {                                   // even ld: rows start 16B-aligned
-                    if (tid == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    if (tid == 0)
-                        for (int j = 0; j < tr; ++j)
-                            bulk_store(out + (orow0 + j) * a.ld, st + j * SRr, (uint32_t)(S3 - 1) * 8u);
-                    if (tid >= 32 && tid < 32 + tr) {
-                        const int j = tid - 32;
-                        out[(orow0 + j) * a.ld + S3 - 1] = st[j * SRr + S3 - 1];
-                    }
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
+                if (tid >= 32 && tid < 32 + tr) {
+                    const int j = tid - 32;
+                    if (a.do_mass) a.M[(orow0 + j) * a.ld + S3 - 1] = stM[j * SRr + S3 - 1];
+                    if (a.do_stiff) a.K[(orow0 + j) * a.ld + S3 - 1] = stK[j * SRr + S3 - 1];
                 }
             }
-            if (tid == 0) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             ++tiles;
         }
     }
@@ -329,12 +358,12 @@ int launch_line(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, 
     LineArgs a{};
     a.T = T;
     a.grid = c->grid;
-    a.plane0 = c->grid_plane0;
-    a.planes = c->grid_planes;
-    a.n = R->n;
-    a.N = R->N;
-    a.row_begin = o->row_begin;
-    a.row_end = o->row_end;
+    a.plane0 = (int)c->grid_plane0;
+    a.planes = (int)c->grid_planes;
+    a.n = (int)R->n;
+    a.N = (int)R->N;
+    a.row_begin = (int)o->row_begin;
+    a.row_end = (int)o->row_end;
     a.M = M ? M->values : nullptr;
     a.K = K ? K->values : nullptr;
     a.ld = o->ld;

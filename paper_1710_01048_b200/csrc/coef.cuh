@@ -27,7 +27,7 @@ __device__ __forceinline__ double grid_eval(const CoefDev& c, int64_t n, const d
     double f[3];
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-        double s = x[a] * (double)n;
+        double s = __dmul_rn(x[a], (double)n);
         int64_t k = (int64_t)floor(s);
         k = k < 0 ? 0 : (k > n - 1 ? n - 1 : k);
         e[a] = k;

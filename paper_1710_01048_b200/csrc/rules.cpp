@@ -16,6 +16,9 @@
 //                      eq:CubicQuadratureStiff (true signs R3).
 //  boundary j < p    : reading R1 (remark P:438-440).
 // Each rule is checked against exact moments over the full interacting set (< 1e-13).
+// All of the setup arithmetic runs in x87 extended precision (long double, 64-bit mantissa)
+// and each node/weight is rounded to double once, so the tables are correctly rounded
+// (R14) instead of carrying the fp64 residual floor times the condition number.
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -27,15 +30,17 @@
 namespace wgq {
 namespace {
 
+using real = long double;
+
 // ---------------------------------------------------------------------------------------
 // B-splines on an explicit knot vector: all nonzero functions of a span and their
 // derivatives (triangular de Boor table, Piegl & Tiller's algorithm A2.3).
 // ---------------------------------------------------------------------------------------
 struct Knots {
-    std::vector<double> t;
+    std::vector<real> t;
     int p;
     int nfun() const { return (int)t.size() - p - 1; }
-    int span(double x) const {
+    int span(real x) const {
         int hi = nfun();                       // last valid span index is nfun()-1
         if (x >= t[hi]) return hi - 1;
         int s = p;
@@ -47,25 +52,25 @@ struct Knots {
 Knots unit_open_knots(int p, int n) {
     Knots k;
     k.p = p;
-    for (int i = 0; i <= p; ++i) k.t.push_back(0.0);
-    for (int i = 1; i < n; ++i) k.t.push_back((double)i);
-    for (int i = 0; i <= p; ++i) k.t.push_back((double)n);
+    for (int i = 0; i <= p; ++i) k.t.push_back(0.0L);
+    for (int i = 1; i < n; ++i) k.t.push_back((real)i);
+    for (int i = 0; i <= p; ++i) k.t.push_back((real)n);
     return k;
 }
 
 // ders[d][r] = d-th derivative of N_{s-p+r}(x), r = 0..p, d = 0..nd (nd <= 2)
-void span_ders(const Knots& K, int s, double x, int nd, double ders[3][kMaxP + 1]) {
+void span_ders(const Knots& K, int s, real x, int nd, real ders[3][kMaxP + 1]) {
     const int p = K.p;
-    const double* t = K.t.data();
-    double ndu[kMaxP + 1][kMaxP + 1], left[kMaxP + 1], right[kMaxP + 1];
-    ndu[0][0] = 1.0;
+    const real* t = K.t.data();
+    real ndu[kMaxP + 1][kMaxP + 1], left[kMaxP + 1], right[kMaxP + 1];
+    ndu[0][0] = 1.0L;
     for (int j = 1; j <= p; ++j) {
         left[j] = x - t[s + 1 - j];
         right[j] = t[s + j] - x;
-        double saved = 0.0;
+        real saved = 0.0L;
         for (int r = 0; r < j; ++r) {
             ndu[j][r] = right[r + 1] + left[j - r];
-            double tmp = ndu[r][j - 1] / ndu[j][r];
+            real tmp = ndu[r][j - 1] / ndu[j][r];
             ndu[r][j] = saved + right[r + 1] * tmp;
             saved = left[j - r] * tmp;
         }
@@ -73,11 +78,11 @@ void span_ders(const Knots& K, int s, double x, int nd, double ders[3][kMaxP + 1
     }
     for (int r = 0; r <= p; ++r) ders[0][r] = ndu[r][p];
     for (int r = 0; r <= p; ++r) {
-        double a[2][kMaxP + 1];
+        real a[2][kMaxP + 1];
         int s1 = 0, s2 = 1;
-        a[0][0] = 1.0;
+        a[0][0] = 1.0L;
         for (int k = 1; k <= nd; ++k) {
-            double d = 0.0;
+            real d = 0.0L;
             int rk = r - k, pk = p - k;
             if (r >= k) {
                 a[s2][0] = a[s1][0] / ndu[pk + 1][rk];
@@ -97,7 +102,7 @@ void span_ders(const Knots& K, int s, double x, int nd, double ders[3][kMaxP + 1
             std::swap(s1, s2);
         }
     }
-    double f = p;
+    real f = p;
     for (int k = 1; k <= nd; ++k) {
         for (int r = 0; r <= p; ++r) ders[k][r] *= f;
         f *= (p - k);
@@ -105,10 +110,10 @@ void span_ders(const Knots& K, int s, double x, int nd, double ders[3][kMaxP + 1
 }
 
 // value of the order-th derivative of B_i at x
-double bval(const Knots& K, int i, double x, int order) {
+real bval(const Knots& K, int i, real x, int order) {
     int s = K.span(x);
-    if (i < s - K.p || i > s) return 0.0;
-    double ders[3][kMaxP + 1];
+    if (i < s - K.p || i > s) return 0.0L;
+    real ders[3][kMaxP + 1];
     span_ders(K, s, x, order, ders);
     return ders[order][i - (s - K.p)];
 }
@@ -116,40 +121,41 @@ double bval(const Knots& K, int i, double x, int order) {
 // ---------------------------------------------------------------------------------------
 // Gauss-Legendre by Newton on the three-term recurrence.
 // ---------------------------------------------------------------------------------------
-void gauss_legendre(int m, std::vector<double>& x, std::vector<double>& w) {
-    x.assign(m, 0.0);
-    w.assign(m, 0.0);
+void gauss_legendre(int m, std::vector<real>& x, std::vector<real>& w) {
+    x.assign(m, 0.0L);
+    w.assign(m, 0.0L);
+    const real pi = 3.14159265358979323846264338327950288L;
     for (int i = 0; i < m; ++i) {
-        double z = std::cos(M_PI * (i + 0.75) / (m + 0.5));
-        double dp = 0.0;
+        real z = std::cos(pi * (i + 0.75L) / (m + 0.5L));
+        real dp = 0.0L;
         for (int it = 0; it < 100; ++it) {
-            double p0 = 1.0, p1 = 0.0;
+            real p0 = 1.0L, p1 = 0.0L;
             for (int k = 1; k <= m; ++k) {
-                double p2 = p1;
+                real p2 = p1;
                 p1 = p0;
-                p0 = ((2.0 * k - 1.0) * z * p1 - (k - 1.0) * p2) / k;
+                p0 = ((2.0L * k - 1.0L) * z * p1 - (k - 1.0L) * p2) / k;
             }
-            dp = m * (z * p0 - p1) / (z * z - 1.0);
-            double dz = p0 / dp;
+            dp = m * (z * p0 - p1) / (z * z - 1.0L);
+            real dz = p0 / dp;
             z -= dz;
-            if (std::fabs(dz) < 1e-17) break;
+            if (std::fabs(dz) < 1e-21L) break;
         }
         x[m - 1 - i] = z;                       // ascending
-        w[m - 1 - i] = 2.0 / ((1.0 - z * z) * dp * dp);
+        w[m - 1 - i] = 2.0L / ((1.0L - z * z) * dp * dp);
     }
 }
 
 // int_{lo}^{hi} B_i^{(o)} B_j^{(o)} dx, exact by (p+2)-point GL on every knot span
-double product_moment(const Knots& K, int i, int j, int order, double lo, double hi) {
-    std::vector<double> gx, gw;
+real product_moment(const Knots& K, int i, int j, int order, real lo, real hi) {
+    std::vector<real> gx, gw;
     gauss_legendre(K.p + 2, gx, gw);
-    double sum = 0.0;
+    real sum = 0.0L;
     for (size_t s = 0; s + 1 < K.t.size(); ++s) {
-        double a = K.t[s], b = K.t[s + 1];
+        real a = K.t[s], b = K.t[s + 1];
         if (b <= a || a < lo || b > hi) continue;
         for (size_t q = 0; q < gx.size(); ++q) {
-            double x = 0.5 * (a + b) + 0.5 * (b - a) * gx[q];
-            sum += 0.5 * (b - a) * gw[q] * bval(K, i, x, order) * bval(K, j, x, order);
+            real x = 0.5L * (a + b) + 0.5L * (b - a) * gx[q];
+            sum += 0.5L * (b - a) * gw[q] * bval(K, i, x, order) * bval(K, j, x, order);
         }
     }
     return sum;
@@ -159,9 +165,9 @@ double product_moment(const Knots& K, int i, int j, int order, double lo, double
 struct Exactness {
     Knots K;
     int j, order;
-    double lo, hi;
+    real lo, hi;
     std::vector<int> rows;
-    std::vector<double> mu;
+    std::vector<real> mu;
     Exactness(int p, int j_, int order_, bool interior) : K(unit_open_knots(p, 4 * p + 2)), j(j_), order(order_) {
         lo = K.t[j];
         hi = K.t[j + p + 1];
@@ -170,95 +176,96 @@ struct Exactness {
         (void)interior;
         for (int i : rows) mu.push_back(product_moment(K, i, j, order, lo, hi));
     }
-    double residual(int row_index, int m, const double* tau, const double* om) const {
-        double q = 0.0;
+    template <typename T>
+    real residual(int row_index, int m, const T* tau, const T* om) const {
+        real q = 0.0L;
         for (int k = 0; k < m; ++k) {
-            double x = lo + tau[k];
-            q += om[k] * bval(K, rows[row_index], x, order) * bval(K, j, x, order);
+            real x = lo + (real)tau[k];
+            q += (real)om[k] * bval(K, rows[row_index], x, order) * bval(K, j, x, order);
         }
         return q - mu[row_index];
     }
     double max_residual(int m, const double* tau, const double* om) const {
-        double worst = 0.0;
+        real worst = 0.0L;
         for (size_t r = 0; r < rows.size(); ++r) worst = std::max(worst, std::fabs(residual((int)r, m, tau, om)));
-        return worst;
+        return (double)worst;
     }
 };
 
 // ---------------------------------------------------------------------------------------
 // Damped Newton with finite-difference Jacobian, step halving and bracket projection.
 // ---------------------------------------------------------------------------------------
-using ResidualFn = std::function<void(const std::vector<double>& u, std::vector<double>& r)>;
+using ResidualFn = std::function<void(const std::vector<real>& u, std::vector<real>& r)>;
 
-bool solve_linear(std::vector<double> A, std::vector<double> b, int n, std::vector<double>& x) {
+bool solve_linear(std::vector<real> A, std::vector<real> b, int n, std::vector<real>& x) {
     for (int c = 0; c < n; ++c) {
         int piv = c;
         for (int r = c + 1; r < n; ++r)
             if (std::fabs(A[r * n + c]) > std::fabs(A[piv * n + c])) piv = r;
-        if (std::fabs(A[piv * n + c]) < 1e-300) return false;
+        if (std::fabs(A[piv * n + c]) < 1e-300L) return false;
         if (piv != c) {
             for (int k = 0; k < n; ++k) std::swap(A[c * n + k], A[piv * n + k]);
             std::swap(b[c], b[piv]);
         }
         for (int r = c + 1; r < n; ++r) {
-            double f = A[r * n + c] / A[c * n + c];
+            real f = A[r * n + c] / A[c * n + c];
             for (int k = c; k < n; ++k) A[r * n + k] -= f * A[c * n + k];
             b[r] -= f * b[c];
         }
     }
-    x.assign(n, 0.0);
+    x.assign(n, 0.0L);
     for (int r = n - 1; r >= 0; --r) {
-        double s = b[r];
+        real s = b[r];
         for (int k = r + 1; k < n; ++k) s -= A[r * n + k] * x[k];
         x[r] = s / A[r * n + r];
     }
     return true;
 }
 
-double newton(const ResidualFn& F, std::vector<double>& u, const std::vector<std::pair<double, double>>& box) {
+real newton(const ResidualFn& F, std::vector<real>& u, const std::vector<std::pair<real, real>>& box) {
     const int n = (int)u.size();
-    auto project = [&](std::vector<double>& v) {
+    auto project = [&](std::vector<real>& v) {
         for (int i = 0; i < n; ++i) {
-            double a = box[i].first, b = box[i].second;
-            if (a < b) v[i] = std::min(std::max(v[i], a + 1e-12 * (b - a)), b - 1e-12 * (b - a));
+            real a = box[i].first, b = box[i].second;
+            if (a < b) v[i] = std::min(std::max(v[i], a + 1e-12L * (b - a)), b - 1e-12L * (b - a));
         }
     };
-    auto norm = [](const std::vector<double>& r) {
-        double m = 0.0;
-        for (double v : r) m = std::max(m, std::fabs(v));
+    auto norm = [](const std::vector<real>& r) {
+        real m = 0.0L;
+        for (real v : r) m = std::max(m, std::fabs(v));
         return m;
     };
     project(u);
-    std::vector<double> r(n), rp(n), rm(n), J(n * n), du, v;
+    std::vector<real> r(n), rp(n), rm(n), J(n * n), du, v;
     F(u, r);
-    double nr = norm(r);
-    for (int it = 0; it < 60 && nr > 4e-17; ++it) {
+    real nr = norm(r);
+    for (int it = 0; it < 80 && nr > 1e-21L; ++it) {
         for (int c = 0; c < n; ++c) {
-            double h = 1e-7 * std::max(1.0, std::fabs(u[c]));
-            std::vector<double> up = u, um = u;
+            real h = 1e-9L * std::max((real)1.0L, std::fabs(u[c]));
+            std::vector<real> up = u, um = u;
             up[c] += h;
             um[c] -= h;
             F(up, rp);
             F(um, rm);
-            for (int rr = 0; rr < n; ++rr) J[rr * n + c] = (rp[rr] - rm[rr]) / (2.0 * h);
+            for (int rr = 0; rr < n; ++rr) J[rr * n + c] = (rp[rr] - rm[rr]) / (2.0L * h);
         }
         if (!solve_linear(J, r, n, du)) break;
-        double lam = 1.0;
+        real lam = 1.0L;
         bool ok = false;
-        while (lam > 1e-6) {
+        while (lam > 1e-6L) {
             v = u;
             for (int i = 0; i < n; ++i) v[i] -= lam * du[i];
             project(v);
             F(v, rp);
-            double nv = norm(rp);
-            if (std::isfinite(nv) && nv < nr) {
+            real nv = norm(rp);
+            if (std::isfinite((double)nv) && nv < nr) {
                 u = v;
                 r = rp;
                 nr = nv;
                 ok = true;
                 break;
             }
-            lam *= 0.5;
+            lam *= 0.5L;
         }
         if (!ok) break;
     }
@@ -273,37 +280,45 @@ int finish(ClassRule& R, const Exactness& E) {
     return R.residual < 1e-13 ? WGQ_OK : WGQ_ENOCONV;
 }
 
+// round an extended-precision rule to the stored doubles
+void store(ClassRule& R, int m, const real* tau, const real* om) {
+    R.m = m;
+    for (int k = 0; k < m; ++k) {
+        R.tau[k] = (double)tau[k];
+        R.omega[k] = (double)om[k];
+    }
+}
+
 int interior_mass_p2(ClassRule& R) {
     Exactness E(2, 4, 0, true);
-    double t1 = (24.0 - std::sqrt(30.0)) / 26.0;          // root in (0,1) of 26t^2 - 48t + 21
-    double w1 = 1.0 / (30.0 * t1 * t1 * (1.0 - t1) * (1.0 - t1));
-    double w2 = (16.0 / 9.0) * (11.0 / 20.0 - 0.5 * w1 * t1 * t1 * t1 * t1);
-    R.m = 3;
-    double tau[3] = {t1, 1.5, 3.0 - t1}, om[3] = {w1, w2, w1};
-    std::memcpy(R.tau, tau, sizeof tau);
-    std::memcpy(R.omega, om, sizeof om);
+    const real t1 = (24.0L - std::sqrt(30.0L)) / 26.0L;   // root in (0,1) of 26t^2 - 48t + 21
+    const real w1 = 1.0L / (30.0L * t1 * t1 * (1.0L - t1) * (1.0L - t1));
+    const real w2 = (16.0L / 9.0L) * (11.0L / 20.0L - 0.5L * w1 * t1 * t1 * t1 * t1);
+    const real tau[3] = {t1, 1.5L, 3.0L - t1}, om[3] = {w1, w2, w1};
+    store(R, 3, tau, om);
     return finish(R, E);
 }
 
 int interior_mass_p3(ClassRule& R) {
     Exactness E(3, 6, 0, true);
-    auto expand = [](const std::vector<double>& u, double* tau, double* om) {
-        tau[0] = u[0]; tau[1] = u[1]; tau[2] = 4.0 - u[1]; tau[3] = 4.0 - u[0];
+    auto expand = [](const std::vector<real>& u, real* tau, real* om) {
+        tau[0] = u[0]; tau[1] = u[1]; tau[2] = 4.0L - u[1]; tau[3] = 4.0L - u[0];
         om[0] = u[2]; om[1] = u[3]; om[2] = u[3]; om[3] = u[2];
     };
-    ResidualFn F = [&](const std::vector<double>& u, std::vector<double>& r) {
-        double tau[4], om[4];
+    ResidualFn F = [&](const std::vector<real>& u, std::vector<real>& r) {
+        real tau[4], om[4];
         expand(u, tau, om);
         for (int k = 0; k < 4; ++k) r[k] = E.residual(k, 4, tau, om);   // offsets -3..0
     };
-    const double s1[] = {0.5, 0.3, 0.7, 0.15, 0.85}, s2[] = {1.5, 1.3, 1.7, 1.15, 1.85};
-    for (double a : s1)
-        for (double b : s2) {
-            std::vector<double> u = {a, b, 1.0, 1.0};
-            double nr = newton(F, u, {{0.0, 1.0}, {1.0, 2.0}, {0.0, 0.0}, {0.0, 0.0}});
-            if (nr < 1e-14 && u[0] > 0 && u[0] < 1 && u[1] > 1 && u[1] < 2 && u[2] > 0 && u[3] > 0) {
-                R.m = 4;
-                expand(u, R.tau, R.omega);
+    const real s1[] = {0.5L, 0.3L, 0.7L, 0.15L, 0.85L}, s2[] = {1.5L, 1.3L, 1.7L, 1.15L, 1.85L};
+    for (real a : s1)
+        for (real b : s2) {
+            std::vector<real> u = {a, b, 1.0L, 1.0L};
+            real nr = newton(F, u, {{0.0L, 1.0L}, {1.0L, 2.0L}, {0.0L, 0.0L}, {0.0L, 0.0L}});
+            if (nr < 1e-17L && u[0] > 0 && u[0] < 1 && u[1] > 1 && u[1] < 2 && u[2] > 0 && u[3] > 0) {
+                real tau[4], om[4];
+                expand(u, tau, om);
+                store(R, 4, tau, om);
                 return finish(R, E);
             }
         }
@@ -312,32 +327,33 @@ int interior_mass_p3(ClassRule& R) {
 
 int interior_stiff_p2(ClassRule& R) {
     Exactness E(2, 4, 1, true);
-    R.m = 2;                                   // the middle node tau = 3/2 has B'_j = 0 (R2)
-    R.tau[0] = 0.75; R.tau[1] = 2.25;
-    R.omega[0] = R.omega[1] = 8.0 / 9.0;
+    // the middle node tau = 3/2 has B'_j = 0 (R2): dropped
+    const real tau[2] = {0.75L, 2.25L}, om[2] = {8.0L / 9.0L, 8.0L / 9.0L};
+    store(R, 2, tau, om);
     return finish(R, E);
 }
 
 int interior_stiff_p3(ClassRule& R) {
     Exactness E(3, 6, 1, true);
-    const double w1 = 1.0;
-    const double t1 = 0.5 - std::sqrt(225.0 - 30.0 * std::sqrt(30.0)) / 30.0;
-    auto expand = [&](const std::vector<double>& u, double* tau, double* om) {
-        tau[0] = t1; tau[1] = u[0]; tau[2] = 4.0 - u[0]; tau[3] = 4.0 - t1;
+    const real w1 = 1.0L;
+    const real t1 = 0.5L - std::sqrt(225.0L - 30.0L * std::sqrt(30.0L)) / 30.0L;
+    auto expand = [&](const std::vector<real>& u, real* tau, real* om) {
+        tau[0] = t1; tau[1] = u[0]; tau[2] = 4.0L - u[0]; tau[3] = 4.0L - t1;
         om[0] = w1; om[1] = u[1]; om[2] = u[1]; om[3] = w1;
     };
-    ResidualFn F = [&](const std::vector<double>& u, std::vector<double>& r) {
-        double tau[4], om[4];
+    ResidualFn F = [&](const std::vector<real>& u, std::vector<real>& r) {
+        real tau[4], om[4];
         expand(u, tau, om);
         r[0] = E.residual(1, 4, tau, om);       // offset -2 (line 2)
         r[1] = E.residual(3, 4, tau, om);       // offset  0 (line 4)
     };
-    for (double a : {1.5, 1.3, 1.7, 1.15, 1.85}) {
-        std::vector<double> u = {a, 1.0};
-        double nr = newton(F, u, {{1.0, 2.0}, {0.0, 0.0}});
-        if (nr < 1e-14 && u[0] > 1 && u[0] < 2 && u[1] > 0) {
-            R.m = 4;
-            expand(u, R.tau, R.omega);
+    for (real a : {1.5L, 1.3L, 1.7L, 1.15L, 1.85L}) {
+        std::vector<real> u = {a, 1.0L};
+        real nr = newton(F, u, {{1.0L, 2.0L}, {0.0L, 0.0L}});
+        if (nr < 1e-17L && u[0] > 1 && u[0] < 2 && u[1] > 0) {
+            real tau[4], om[4];
+            expand(u, tau, om);
+            store(R, 4, tau, om);
             return finish(R, E);
         }
     }
@@ -345,15 +361,17 @@ int interior_stiff_p3(ClassRule& R) {
 }
 
 void gl_per_element(int p, int j, ClassRule& R) {
-    std::vector<double> gx, gw;
+    std::vector<real> gx, gw;
     gauss_legendre(p + 1, gx, gw);
-    R.m = 0;
+    real tau[kMaxNodes], om[kMaxNodes];
+    int m = 0;
     for (int e = 0; e <= j; ++e)
         for (int q = 0; q <= p; ++q) {
-            R.tau[R.m] = e + 0.5 + 0.5 * gx[q];
-            R.omega[R.m] = 0.5 * gw[q];
-            ++R.m;
+            tau[m] = e + 0.5L + 0.5L * gx[q];
+            om[m] = 0.5L * gw[q];
+            ++m;
         }
+    store(R, m, tau, om);
 }
 
 // Reading R1: m = ceil(D/2) nodes; the last node is fixed at j + 1/2 when D is odd.
@@ -368,43 +386,41 @@ int boundary_rule(int p, int j, int kind, int bnd, ClassRule& R) {
     const int m = (D + 1) / 2;
     const bool fixed = (D % 2) == 1;
     const int nfree = fixed ? m - 1 : m;
-    const double L = j + 1.0;
+    const real L = j + 1.0L;
     const int neq = D;                         // stiffness: last constraint implied (sum B'_i = 0)
-    auto expand = [&](const std::vector<double>& u, double* tau, double* om) {
+    auto expand = [&](const std::vector<real>& u, real* tau, real* om) {
         for (int k = 0; k < nfree; ++k) tau[k] = u[k];
-        if (fixed) tau[m - 1] = j + 0.5;
+        if (fixed) tau[m - 1] = j + 0.5L;
         for (int k = 0; k < m; ++k) om[k] = u[nfree + k];
     };
-    ResidualFn F = [&](const std::vector<double>& u, std::vector<double>& r) {
-        double tau[kMaxStiffNodes], om[kMaxStiffNodes];
+    ResidualFn F = [&](const std::vector<real>& u, std::vector<real>& r) {
+        real tau[kMaxNodes], om[kMaxNodes];
         expand(u, tau, om);
         for (int e = 0; e < neq; ++e) r[e] = E.residual(e, m, tau, om);
     };
-    std::vector<std::pair<double, double>> box;
-    for (int k = 0; k < nfree; ++k) box.push_back({0.0, L});
-    for (int k = 0; k < m; ++k) box.push_back({0.0, 0.0});
+    std::vector<std::pair<real, real>> box;
+    for (int k = 0; k < nfree; ++k) box.push_back({0.0L, L});
+    for (int k = 0; k < m; ++k) box.push_back({0.0L, 0.0L});
     // deterministic multi-start: increasing tuples of a 9-point grid
     const int G = 9;
-    std::vector<double> grid;
-    for (int g = 0; g < G; ++g) grid.push_back(L * (0.05 + 0.9 * g / (G - 1)));
+    std::vector<real> grid;
+    for (int g = 0; g < G; ++g) grid.push_back(L * (0.05L + 0.9L * g / (G - 1)));
     std::vector<int> idx(nfree);
     std::function<bool(int, int)> rec = [&](int pos, int start) -> bool {
         if (pos == nfree) {
-            std::vector<double> u;
+            std::vector<real> u;
             for (int k = 0; k < nfree; ++k) u.push_back(grid[idx[k]]);
-            if (fixed && nfree > 0 && u.back() >= j + 0.5) return false;
-            for (int k = 0; k < m; ++k) u.push_back(1.0 / m);
-            double nr = newton(F, u, box);
-            if (nr > 1e-14) return false;
-            double tau[kMaxStiffNodes], om[kMaxStiffNodes];
+            if (fixed && nfree > 0 && u.back() >= j + 0.5L) return false;
+            for (int k = 0; k < m; ++k) u.push_back(1.0L / m);
+            real nr = newton(F, u, box);
+            if (nr > 1e-17L) return false;
+            real tau[kMaxNodes], om[kMaxNodes];
             expand(u, tau, om);
             for (int k = 0; k < m; ++k) {
-                if (!(tau[k] > 1e-9 && tau[k] < L - 1e-9 && om[k] > 0)) return false;
-                if (k > 0 && !(tau[k] > tau[k - 1] + 1e-9)) return false;
+                if (!(tau[k] > 1e-9L && tau[k] < L - 1e-9L && om[k] > 0)) return false;
+                if (k > 0 && !(tau[k] > tau[k - 1] + 1e-9L)) return false;
             }
-            R.m = m;
-            std::memcpy(R.tau, tau, sizeof(double) * m);
-            std::memcpy(R.omega, om, sizeof(double) * m);
+            store(R, m, tau, om);
             return true;
         }
         for (int g = start; g < G; ++g) {
@@ -424,24 +440,27 @@ void interior_vertex_tables(int p, const ClassRule& mass, const ClassRule& stiff
     // reference knots, cardinal weight j = 2p with support [p, 2p+1]; neighbours j+o
     Knots K = unit_open_knots(p, 4 * p + 2);
     const int j = 2 * p;
-    for (int v = 0; v < kMaxV; ++v)
-        for (int o = 0; o < kMaxS; ++o) PM[v][o] = PK[v][o] = 0.0;
+    real acc[2][kMaxV][kMaxS] = {};
     for (int kind = 0; kind < 2; ++kind) {
         const ClassRule& R = kind == 0 ? mass : stiff;
-        double (*P)[kMaxS] = kind == 0 ? PM : PK;
         for (int k = 0; k < R.m; ++k) {
-            const double t = R.tau[k];
+            const real t = R.tau[k];
             const int e = (int)std::floor(t);                 // element of the node (inside it)
-            const double f = t - e;
-            const double x = p + t;
-            const double w = R.omega[k] * bval(K, j, x, kind);
+            const real f = t - e;
+            const real x = p + t;
+            const real w = (real)R.omega[k] * bval(K, j, x, kind);
             for (int o = -p; o <= p; ++o) {
-                const double a = w * bval(K, j + o, x, kind);
-                P[e][o + p] += (1.0 - f) * a;
-                P[e + 1][o + p] += f * a;
+                const real a = w * bval(K, j + o, x, kind);
+                acc[kind][e][o + p] += (1.0L - f) * a;
+                acc[kind][e + 1][o + p] += f * a;
             }
         }
     }
+    for (int v = 0; v < kMaxV; ++v)
+        for (int o = 0; o < kMaxS; ++o) {
+            PM[v][o] = (double)acc[0][v][o];
+            PK[v][o] = (double)acc[1][v][o];
+        }
 }
 
 int build_class_rules(int p, int bnd, ClassRule out[2][kMaxP + 1]) {

@@ -4,10 +4,10 @@
 // functions at those nodes.  The tables depend on (p, n, rules) only and are built once
 // per device and cached in the rules handle.
 //
-// Node placement (R1): row r < p uses the left boundary class j = r (x = tau/n); row
-// r >= n the mirrored class j = N-1-r (x = 1 - tau/n); other rows the interior rule
-// shifted to supp B_r = [(r-p)/n, (r+1)/n] (x = (r - p + tau)/n).  Weights scale
-// by h = 1/n (dx = h dtau); derivative values are physical.
+// Node placement (R1): row r < p uses the left boundary class j = r (x = h tau); row
+// r >= n the mirrored class j = N-1-r (x = 1 - h tau); other rows the interior rule
+// shifted to supp B_r = [(r-p)h, (r+1)h] (x = h (r - p + tau)), h = 1/n.  Weights
+// scale by h (dx = h dtau); derivative values are physical.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -111,16 +111,19 @@ __global__ void k_row_tables(ClassArgs A, RowTables T) {
         for (int o = 0; o < kMaxS; ++o) row[o] = 0.0;
         return;
     }
+    // x = h*(e0 + tau), omega_h = h*omega with h = 1/n, rounded exactly as written (no FMA
+    // contraction) so that node coordinates are reproducible bit for bit (R14).
+    const double h = 1.0 / (double)n;
     double x, om;
     if (cls == p) {
-        x = ((double)(r - p) + A.tau[kind][cls][k]) / (double)n;
-        om = A.omega[kind][cls][k] / (double)n;
+        x = __dmul_rn(h, __dadd_rn((double)(r - p), A.tau[kind][cls][k]));
+        om = __dmul_rn(h, A.omega[kind][cls][k]);
     } else if (!mirror) {
-        x = A.tau[kind][cls][k] / (double)n;
-        om = A.omega[kind][cls][k] / (double)n;
+        x = __dmul_rn(h, A.tau[kind][cls][k]);
+        om = __dmul_rn(h, A.omega[kind][cls][k]);
     } else {
-        x = 1.0 - A.tau[kind][cls][m - 1 - k] / (double)n;
-        om = A.omega[kind][cls][m - 1 - k] / (double)n;
+        x = __dsub_rn(1.0, __dmul_rn(h, A.tau[kind][cls][m - 1 - k]));
+        om = __dmul_rn(h, A.omega[kind][cls][m - 1 - k]);
     }
     double vals[kMaxP + 1], ders[kMaxP + 1];
     const int64_t s = eval_span(x, p, n, vals, ders);
@@ -154,7 +157,7 @@ __global__ void k_vertex_tables(int p, int64_t n, RowTables T) {
     const int64_t b = r - p > 0 ? r - p : 0;
     double acc = 0.0;
     for (int k = 0; k < m; ++k) {
-        const double s = X[k] * (double)n;
+        const double s = __dmul_rn(X[k], (double)n);
         int64_t e = (int64_t)floor(s);
         e = e < 0 ? 0 : (e > n - 1 ? n - 1 : e);
         const double f = s - (double)e;
