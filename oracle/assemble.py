@@ -62,14 +62,17 @@ def decode(row, N, d):
     return idx
 
 
-def _term(dirs, desc, n, grid, plane0):
-    """One tensor term: sum_k [prod w] c(x_k) prod_a T_a[k_a, o_a] as an ELL row."""
+def _term(dirs, desc, n, grid, plane0, absolute=False):
+    """One tensor term: sum_k [prod w] c(x_k) prod_a T_a[k_a, o_a] as an ELL row
+    (absolute=True: the same sum over |terms|, the rounding scale of each entry)."""
     d = len(dirs)
     xs = [x for x, _, _ in dirs]
-    ws = [w for _, w, _ in dirs]
-    Ts = [T for _, _, T in dirs]
+    ws = [np.abs(w) if absolute else w for _, w, _ in dirs]
+    Ts = [np.abs(T) if absolute else T for _, _, T in dirs]
     X = np.meshgrid(*xs, indexing="ij")
     c = coeff.evaluate(desc, n, X, grid, plane0)
+    if absolute:
+        c = np.abs(c)
     Wt = c.copy()
     for a in range(d):
         shape = [1] * d
@@ -86,8 +89,11 @@ def _term(dirs, desc, n, grid, plane0):
     return Wt.reshape(nk) @ Phi.reshape(nk, -1)
 
 
-def assemble_rows(p, n, d, rows, desc, kinds=("mass", "stiffness"), grid=None, plane0=0, mode="gauss"):
-    """ELL values of the requested global rows: {'mass': [R, s^d], 'stiffness': [R, s^d]}."""
+def assemble_rows(p, n, d, rows, desc, kinds=("mass", "stiffness"), grid=None, plane0=0, mode="gauss",
+                  absolute=False):
+    """ELL values of the requested global rows: {'mass': [R, s^d], 'stiffness': [R, s^d]}.
+    absolute=True returns sum_k |term_k| per entry instead (the scale of FP64 rounding in
+    that entry, used by the parity tests' conditioning-aware tolerance, R12)."""
     tab = tables_1d(p, n, mode)
     N = n + p
     s = 2 * p + 1
@@ -96,12 +102,12 @@ def assemble_rows(p, n, d, rows, desc, kinds=("mass", "stiffness"), grid=None, p
         idx = decode(int(row), N, d)
         R = [tab[i] for i in idx]
         if "mass" in kinds:
-            out["mass"][ri] = _term([(r.xM, r.wM, r.VM) for r in R], desc, n, grid, plane0)
+            out["mass"][ri] = _term([(r.xM, r.wM, r.VM) for r in R], desc, n, grid, plane0, absolute)
         if "stiffness" in kinds:
             acc = np.zeros(s ** d)
             for a in range(d):
                 dirs = [(R[b].xK, R[b].wK, R[b].DK) if b == a else (R[b].xM, R[b].wM, R[b].VM) for b in range(d)]
-                acc = acc + _term(dirs, desc, n, grid, plane0)
+                acc = acc + _term(dirs, desc, n, grid, plane0, absolute)
             out["stiffness"][ri] = acc
     return out
 
