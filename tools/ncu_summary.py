@@ -8,6 +8,7 @@ rep = sys.argv[1]
 out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr = rows[0]
+units = dict(zip(hdr, rows[1]))
 for vals in rows[2:]:
     d = dict(zip(hdr, vals))
     print("kernel:", d.get("Kernel Name", "")[:90])
@@ -17,7 +18,7 @@ for vals in rows[2:]:
               "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__issue_active.avg.pct_of_peak_sustained_active",
               "launch__registers_per_thread", "launch__occupancy_limit_shared_mem", "smsp__inst_executed.sum",
               "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "sm__cycles_elapsed.avg"]:
-        print("  ", k, d.get(k))
+        print("  ", k, d.get(k), units.get(k, ""))
     st = []
     for h, v in d.items():
         if h.startswith("smsp__pcsamp_warps_issue_stalled") and not h.endswith("not_issued"):
