@@ -1,0 +1,85 @@
+"""Multi-GPU plumbing (one process per GPU, torch.distributed): row slabs, the coefficient
+halo, and the final reductions.
+
+Rows are independent: rank r owns the contiguous z-planes (3D; y-lines in 2D) of
+``api.slab_rows`` and assembles them with no data-path collective.  The only exchanges are
+* ``exchange_halo`` -- for a user-supplied (not seeded) vertex field distributed by owned
+  planes, the p planes below and the 1 plane above a rank's rows (NCCL P2P over NVLink;
+  a seeded field is instead regenerated per rank by ``wgq_generate_grid``), and
+* ``reduce_checks`` / ``max_time`` -- checksum, norms and the max-over-ranks step time.
+Everything here is host logic; the arithmetic of the method stays in libwgq.
+"""
+import torch
+import torch.distributed as dist
+
+from . import api
+
+
+def owned_vertex_planes(n, N, dim, rank, world):
+    """Vertex planes [v0, v1) of the slowest axis a rank owns when a user field is
+    distributed alongside the row slabs (row planes [z0, z1) clipped to [0, n+1))."""
+    plane_rows = N ** (dim - 1)
+    b, e = api.slab_rows(N, dim, rank, world)
+    z0, z1 = b // plane_rows, e // plane_rows
+    return min(z0, n + 1), min(z1, n + 1)
+
+
+def needed_vertex_planes(p, n, N, dim, rank, world):
+    """Vertex planes [lo, hi] touched by the rank's rows: [max(0, z0-p), min(n, z1)]."""
+    plane_rows = N ** (dim - 1)
+    b, e = api.slab_rows(N, dim, rank, world)
+    if e <= b:
+        return 0, -1
+    z0, z1 = b // plane_rows, (e - 1) // plane_rows
+    return max(0, z0 - p), min(n, z1 + 1)
+
+
+def exchange_halo(owned, p, n, N, dim, group=None):
+    """Given this rank's owned vertex planes ``owned`` ([v1-v0, ...] tensor), return the
+    planes [lo, hi] its rows need (owned planes plus halo from the neighbours) and lo.
+    Point-to-point sends of whole planes; works with NCCL (device tensors) and gloo."""
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    own = [owned_vertex_planes(n, N, dim, r, world) for r in range(world)]
+    need = [needed_vertex_planes(p, n, N, dim, r, world) for r in range(world)]
+    lo, hi = need[rank]
+    plane_shape = owned.shape[1:]
+    out = torch.empty((max(hi - lo + 1, 0),) + tuple(plane_shape), dtype=owned.dtype, device=owned.device)
+    reqs = []
+    # receive: planes of [lo, hi] owned by other ranks
+    for src in range(world):
+        a, b = max(lo, own[src][0]), min(hi + 1, own[src][1])
+        if a >= b:
+            continue
+        if src == rank:
+            out[a - lo:b - lo] = owned[a - own[rank][0]:b - own[rank][0]]
+        else:
+            reqs.append(dist.irecv(out[a - lo:b - lo], src=src, group=group))
+    # send: my owned planes other ranks need
+    for dst in range(world):
+        if dst == rank:
+            continue
+        dlo, dhi = need[dst]
+        a, b = max(dlo, own[rank][0]), min(dhi + 1, own[rank][1])
+        if a >= b:
+            continue
+        reqs.append(dist.isend(owned[a - own[rank][0]:b - own[rank][0]].contiguous(), dst=dst, group=group))
+    for r in reqs:
+        r.wait()
+    return out, lo
+
+
+def reduce_checks(local, group=None):
+    """Sum per-rank (hash, sum, sum of squares) checks: the uint64 hash as a wrapping int64
+    sum (== sum mod 2^64), the FP64 sums as doubles."""
+    h = local[0:1].view(torch.int64).clone()
+    s = local[1:3].view(torch.float64).clone()
+    dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+    dist.all_reduce(s, op=dist.ReduceOp.SUM, group=group)
+    return int(h.item()) & (2 ** 64 - 1), float(s[0].item()), float(s[1].item())
+
+
+def max_time(ms, device, group=None):
+    t = torch.tensor([float(ms)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())

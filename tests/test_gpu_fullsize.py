@@ -1,0 +1,117 @@
+"""Full-size parity at BASELINE.json's sizes, in the launch configuration bench.py times.
+
+Each config is assembled on the GPU exactly as bench.py does (api.assemble over the whole
+mesh, device-generated GRID field for C5); the oracle recomputes a sample of rows one by one
+(every boundary / near-boundary row class plus random interior rows) and the GPU rows must
+match them (R12).  Properties that hold at any size are checked on ALL rows on the device:
+(K 1)_i = 0 (P9) and the 8-slab z-partition of C5 reproduces the one-GPU checksum exactly.
+"""
+import numpy as np
+import pytest
+
+import inputs
+from oracle import assemble as oasm
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+REL_F, REL_E = 1e-12, 1e-10
+FLOOR = 64 * np.finfo(np.float64).eps / REL_E
+
+
+def sample_rows(p, n, d, count, seed):
+    """Row sample covering every class combination: per direction the indices 0..2p+1,
+    N-2p-2..N-1 and random interior ones."""
+    N = n + p
+    rng = np.random.default_rng(seed)
+    edge = sorted(set(list(range(0, 2 * p + 2)) + list(range(N - 2 * p - 2, N))))
+    rows = set()
+    while len(rows) < count:
+        idx = []
+        for _ in range(d):
+            idx.append(int(rng.choice(edge)) if rng.random() < 0.5 else int(rng.integers(0, N)))
+        rows.add(sum(idx[a] * N ** a for a in range(d)))
+    return np.array(sorted(rows))
+
+
+def check_rows(gpu_rows, ref, sc, what):
+    nrm = np.linalg.norm(ref)
+    relf = np.linalg.norm(gpu_rows - ref) / nrm
+    den = np.maximum.reduce([np.abs(ref), 1e-14 * np.abs(ref).max(axis=1, keepdims=True), FLOOR * sc])
+    den = np.where(den > 0, den, 1.0)
+    rele = np.max(np.abs(gpu_rows - ref) / den)
+    assert relf <= REL_F and rele <= REL_E, (what, relf, rele)
+
+
+def assemble_config(name):
+    from paper_1710_01048_b200 import api, wgq
+    cfg = inputs.config(name)
+    p, n, d = cfg["p"], cfg["n"], cfg["dim"]
+    rules = wgq.Rules(p, n, d)
+    desc = inputs.coefficient(cfg["coeff"], d)
+    grid, plane0 = (None, 0)
+    if desc["kind"] == "grid":
+        grid, plane0 = api.make_grid(rules, desc["seed"], desc["sigma"], 0, rules.n_rows)
+    out = api.assemble(rules, api.coefficient(desc, grid, plane0), cfg["kinds"])
+    torch.cuda.synchronize()
+    return cfg, rules, desc, out
+
+
+@pytest.mark.parametrize("name,count", [("C2", 600), ("C3", 400), ("C4", 500), ("C5", 700)])
+def test_full_size_sampled_rows(name, count):
+    from paper_1710_01048_b200 import wgq
+    cfg, rules, desc, out = assemble_config(name)
+    p, n, d = cfg["p"], cfg["n"], cfg["dim"]
+    rows = sample_rows(p, n, d, count, seed=sum(map(ord, name)))
+    host_grid = None
+    if desc["kind"] == "grid":
+        host_grid = inputs.lognormal_grid(n, seed=desc["seed"], sigma=desc["sigma"])
+    ref = oasm.assemble_rows(p, n, d, rows, desc, cfg["kinds"], grid=host_grid)
+    sc = oasm.assemble_rows(p, n, d, rows, desc, cfg["kinds"], grid=host_grid, absolute=True)
+    idx = torch.from_numpy(rows).cuda()
+    for k in cfg["kinds"]:
+        check_rows(out[k].index_select(0, idx).cpu().numpy(), ref[k], sc[k], (name, k))
+    # every row: (K 1)_i = 0 relative to the row's scale (P9)
+    if "stiffness" in cfg["kinds"]:
+        K = out["stiffness"]
+        mom = torch.empty((rules.n_rows, 1 + d), dtype=torch.float64, device="cuda")
+        wgq.wgq_row_moments(rules, wgq.make_out(K, 0, rules.n_rows), mom)
+        rowmax = K.abs().amax(dim=1)
+        assert float((mom[:, 0].abs() / rowmax).max()) < 1e-12
+    if "mass" in cfg["kinds"]:
+        M = out["mass"]
+        mom = torch.empty((rules.n_rows, 1 + d), dtype=torch.float64, device="cuda")
+        wgq.wgq_row_moments(rules, wgq.make_out(M, 0, rules.n_rows), mom)
+        assert bool((mom[:, 0] > 0).all())
+    del out
+    torch.cuda.empty_cache()
+
+
+def test_c5_slabs_reproduce_one_gpu_checksum():
+    """8 z-slabs, each with its own device-generated coefficient slab (as 8 ranks would),
+    give exactly the one-GPU checksum (order-independent uint64 hash)."""
+    from paper_1710_01048_b200 import api, wgq
+    cfg, rules, desc, out = assemble_config("C5")
+    N = rules.N
+    full = {}
+    for k in cfg["kinds"]:
+        h = torch.zeros(3, dtype=torch.int64, device="cuda")
+        wgq.wgq_checksum(rules, wgq.make_out(out[k], 0, rules.n_rows), h)
+        full[k] = int(h[0].item()) & (2 ** 64 - 1)
+    del out
+    torch.cuda.empty_cache()
+    acc = {k: 0 for k in cfg["kinds"]}
+    buf = None
+    for r in range(8):
+        b, e = api.slab_rows(N, 3, r, 8)
+        grid, plane0 = api.make_grid(rules, desc["seed"], desc["sigma"], b, e)
+        if buf is None:
+            buf = {k: api.alloc_ell(rules, 0, e - b + N * N) for k in cfg["kinds"]}
+        o = {k: buf[k][:e - b] for k in cfg["kinds"]}
+        api.assemble(rules, api.coefficient(desc, grid, plane0), cfg["kinds"], b, e, out=o)
+        for k in cfg["kinds"]:
+            h = torch.zeros(3, dtype=torch.int64, device="cuda")
+            wgq.wgq_checksum(rules, wgq.make_out(o[k], b, e), h)
+            acc[k] = (acc[k] + int(h[0].item())) % 2 ** 64
+    for k in cfg["kinds"]:
+        assert acc[k] == full[k], k
