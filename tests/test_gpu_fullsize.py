@@ -37,7 +37,7 @@ def sample_rows(p, n, d, count, seed):
 def check_rows(gpu_rows, ref, sc, what):
     nrm = np.linalg.norm(ref)
     relf = np.linalg.norm(gpu_rows - ref) / nrm
-    den = np.maximum.reduce([np.abs(ref), 1e-14 * np.abs(ref).max(axis=1, keepdims=True), FLOOR * sc])
+    den = np.maximum(np.maximum(np.abs(ref), 1e-14 * np.abs(ref).max(axis=1, keepdims=True)), FLOOR * sc)
     den = np.where(den > 0, den, 1.0)
     rele = np.max(np.abs(gpu_rows - ref) / den)
     assert relf <= REL_F and rele <= REL_E, (what, relf, rele)
@@ -69,22 +69,25 @@ def test_full_size_sampled_rows(name, count):
     ref = oasm.assemble_rows(p, n, d, rows, desc, cfg["kinds"], grid=host_grid)
     sc = oasm.assemble_rows(p, n, d, rows, desc, cfg["kinds"], grid=host_grid, absolute=True)
     idx = torch.from_numpy(rows).cuda()
-    for k in cfg["kinds"]:
-        check_rows(out[k].index_select(0, idx).cpu().numpy(), ref[k], sc[k], (name, k))
-    # every row: (K 1)_i = 0 relative to the row's scale (P9)
-    if "stiffness" in cfg["kinds"]:
-        K = out["stiffness"]
+    try:
+        for k in cfg["kinds"]:
+            check_rows(out[k].index_select(0, idx).cpu().numpy(), ref[k], sc[k], (name, k))
+        # every row: (K 1)_i = 0 relative to the row's scale (P9); (M 1)_i > 0
         mom = torch.empty((rules.n_rows, 1 + d), dtype=torch.float64, device="cuda")
-        wgq.wgq_row_moments(rules, wgq.make_out(K, 0, rules.n_rows), mom)
-        rowmax = K.abs().amax(dim=1)
-        assert float((mom[:, 0].abs() / rowmax).max()) < 1e-12
-    if "mass" in cfg["kinds"]:
-        M = out["mass"]
-        mom = torch.empty((rules.n_rows, 1 + d), dtype=torch.float64, device="cuda")
-        wgq.wgq_row_moments(rules, wgq.make_out(M, 0, rules.n_rows), mom)
-        assert bool((mom[:, 0] > 0).all())
-    del out
-    torch.cuda.empty_cache()
+        if "stiffness" in cfg["kinds"]:
+            wgq.wgq_row_moments(rules, wgq.make_out(out["stiffness"], 0, rules.n_rows), mom)
+            worst = 0.0
+            for lo in range(0, rules.n_rows, 1 << 22):      # chunked: no 95 GB temporaries
+                rowmax = out["stiffness"][lo:lo + (1 << 22)].abs().amax(dim=1)
+                worst = max(worst, float((mom[lo:lo + (1 << 22), 0].abs() / rowmax).max()))
+            assert worst < 1e-12, worst
+        if "mass" in cfg["kinds"]:
+            wgq.wgq_row_moments(rules, wgq.make_out(out["mass"], 0, rules.n_rows), mom)
+            assert bool((mom[:, 0] > 0).all())
+        del mom
+    finally:
+        out.clear()
+        torch.cuda.empty_cache()
 
 
 def test_c5_slabs_reproduce_one_gpu_checksum():
@@ -98,7 +101,7 @@ def test_c5_slabs_reproduce_one_gpu_checksum():
         h = torch.zeros(3, dtype=torch.int64, device="cuda")
         wgq.wgq_checksum(rules, wgq.make_out(out[k], 0, rules.n_rows), h)
         full[k] = int(h[0].item()) & (2 ** 64 - 1)
-    del out
+    out.clear()
     torch.cuda.empty_cache()
     acc = {k: 0 for k in cfg["kinds"]}
     buf = None
