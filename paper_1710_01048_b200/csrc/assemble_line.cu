@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "internal.h"
@@ -32,8 +33,6 @@
 namespace wgq {
 namespace {
 
-__constant__ double c_PM3[5][7], c_PK3[5][7];
-__constant__ double c_PM2[4][5], c_PK2[4][5];
 
 template <int P>
 struct Cfg {
@@ -63,8 +62,11 @@ struct LineArgs {
     double* M;
     double* K;
     long long ld;
-    int do_mass, do_stiff;
     double h, inv_h;
+    // interior (class I) x-row vertex tables P^ in physical units: PMh = h * PM, PKi = PK / h
+    // (kernel parameters: constant-bank operands, no global state shared between handles)
+    double PMh[kMaxV][kMaxS], PKi[kMaxV][kMaxS];
+    int dbg;   // profiling only (WGQ_LINE_DBG): 1 = skip compute, 2 = skip stores
 };
 
 __device__ __forceinline__ void bulk_store(double* gdst, const double* ssrc, uint32_t bytes) {
@@ -78,17 +80,6 @@ __device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc, bool
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(gsrc), "r"(valid ? 8 : 0) : "memory");
 }
 
-template <int P>
-__device__ __forceinline__ double cPM(int v, int o) {
-    if constexpr (P == 3) return c_PM3[v][o];
-    else return c_PM2[v][o];
-}
-template <int P>
-__device__ __forceinline__ double cPK(int v, int o) {
-    if constexpr (P == 3) return c_PK3[v][o];
-    else return c_PK2[v][o];
-}
-
 // Issue the vertex patch of planes [c0, c0+nnew) of the line (by, bz): patch[j][vz][vy].
 template <int P>
 __device__ __forceinline__ void load_patch(const LineArgs& a, double* patch, int c0, int nnew, int by, int bz,
@@ -96,8 +87,9 @@ __device__ __forceinline__ void load_patch(const LineArgs& a, double* patch, int
     using C = Cfg<P>;
     constexpr int V = C::V;
     const int nv = a.n + 1;
-    for (int e = tid; e < nnew * V * V; e += C::NT) {
-        const int j = e % nnew, vy = (e / nnew) % V, vz = e / (nnew * V);
+    for (int e = tid; e < C::W * V * V; e += C::NT) {      // constant divisors; j >= nnew idle
+        const int j = e % C::W, vy = (e / C::W) % V, vz = e / (C::W * V);
+        if (j >= nnew) continue;
         const int x = c0 + j, y = by + vy, z = bz + vz;
         const bool ok = x <= a.n && y <= a.n && z <= a.n && z - a.plane0 < a.planes;
         const double* src = ok ? a.grid + ((size_t)(z - a.plane0) * nv + y) * nv + x : a.grid;
@@ -106,27 +98,66 @@ __device__ __forceinline__ void load_patch(const LineArgs& a, double* patch, int
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
-// one interior (class I) row from its window hm/hk[OFF..OFF+V): structural nonzeros only
-template <int P, int OFF>
+// two consecutive interior (class I) rows r, r+1 from the shared window hm/hk[0..V]: row r
+// uses planes 0..V-1, row r+1 planes 1..V.  Only the structural nonzeros of P^ are issued
+// (a node in element k touches planes k, k+1 and columns k..k+p), each constant-bank
+// coefficient feeds both rows, and h / 1/h are folded into the tables.
+template <int P, int MODE>
+__device__ __forceinline__ void finish_pair_interior(const double* hm, const double* hk, double* dM, double* dK,
+                                                     int SRr, bool second, const LineArgs& a) {
+    constexpr int S = 2 * P + 1;
+#pragma unroll
+    for (int o1 = 0; o1 < S; ++o1) {
+        double m0 = 0.0, k0 = 0.0, m1 = 0.0, k1 = 0.0;
+#pragma unroll
+        for (int v = (o1 - P > 0 ? o1 - P : 0); v <= (o1 + 1 < P + 1 ? o1 + 1 : P + 1); ++v) {
+            const double pm = a.PMh[v][o1];
+            if (MODE & 1) {
+                m0 = fma(pm, hm[v], m0);
+                m1 = fma(pm, hm[v + 1], m1);
+            }
+            if (MODE & 2) {
+                const double pk = a.PKi[v][o1];
+                k0 = fma(pk, hm[v], k0);
+                k1 = fma(pk, hm[v + 1], k1);
+                k0 = fma(pm, hk[v], k0);
+                k1 = fma(pm, hk[v + 1], k1);
+            }
+        }
+        if (MODE & 1) {
+            dM[o1] = m0;
+            if (second) dM[SRr + o1] = m1;
+        }
+        if (MODE & 2) {
+            dK[o1] = k0;
+            if (second) dK[SRr + o1] = k1;
+        }
+    }
+}
+
+// one interior row (P^ tables) from its window hm/hk[0..V)
+template <int P, int MODE>
 __device__ __forceinline__ void finish_interior(const double* hm, const double* hk, double* dM, double* dK,
                                                 const LineArgs& a) {
     constexpr int S = 2 * P + 1;
 #pragma unroll
     for (int o1 = 0; o1 < S; ++o1) {
-        double s = 0.0, s1 = 0.0, s2 = 0.0;
+        double m = 0.0, k = 0.0;
 #pragma unroll
         for (int v = (o1 - P > 0 ? o1 - P : 0); v <= (o1 + 1 < P + 1 ? o1 + 1 : P + 1); ++v) {
-            s = fma(cPM<P>(v, o1), hm[v + OFF], s);
-            s1 = fma(cPK<P>(v, o1), hm[v + OFF], s1);
-            s2 = fma(cPM<P>(v, o1), hk[v + OFF], s2);
+            if (MODE & 1) m = fma(a.PMh[v][o1], hm[v], m);
+            if (MODE & 2) {
+                k = fma(a.PKi[v][o1], hm[v], k);
+                k = fma(a.PMh[v][o1], hk[v], k);
+            }
         }
-        if (a.do_mass) dM[o1] = a.h * s + 0.0;
-        if (a.do_stiff) dK[o1] = fma(a.h, s2, s1 * a.inv_h) + 0.0;
+        if (MODE & 1) dM[o1] = m;
+        if (MODE & 2) dK[o1] = k;
     }
 }
 
 // a boundary-affected row: its own vertex tables from global memory
-template <int P>
+template <int P, int MODE>
 __device__ __forceinline__ void finish_general(int r, const double* hm, const double* hk, double* dM, double* dK,
                                                const LineArgs& a) {
     constexpr int S = 2 * P + 1, V = P + 2;
@@ -142,13 +173,13 @@ __device__ __forceinline__ void finish_general(int r, const double* hm, const do
             s1 = fma(__ldg(pk + v * kMaxS + o1), hm[v], s1);
             s1 = fma(m, hk[v], s1);
         }
-        if (a.do_mass) dM[o1] = s + 0.0;
-        if (a.do_stiff) dK[o1] = s1 + 0.0;
+        if (MODE & 1) dM[o1] = s + 0.0;
+        if (MODE & 2) dK[o1] = s1 + 0.0;
     }
 }
 
-template <int P>
-__global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const LineArgs a) {
+template <int P, int MODE>
+__global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const __grid_constant__ LineArgs a) {
     using C = Cfg<P>;
     constexpr int S = C::S, S2 = C::S2, S3 = C::S3, V = C::V, TR = C::TR, RING = C::RING;
     extern __shared__ __align__(128) double sm[];
@@ -200,7 +231,7 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const LineArgs a) 
             // ---- phase A: new vertex planes c0..hi_need -> HM, HK --------------------------
             asm volatile("cp.async.wait_group 0;" ::: "memory");
             __syncthreads();                               // patch + Q visible; ring slots free
-            for (int e = tid; e < nnew * V * S; e += C::NT) {
+            for (int e = tid; e < (a.dbg == 1 ? 0 : nnew * V * S); e += C::NT) {
                 const int o2 = e % S, vz = (e / S) % V, j = e / (S * V);
                 const double* pr = patch + (j * V + vz) * V;
                 double sm_ = 0.0, sk = 0.0;
@@ -218,7 +249,7 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const LineArgs a) 
                 load_patch<P>(a, patches + (pbuf ^ 1) * C::PATCH, hi_need + 1, nhi - hi_need, by, bz, tid);
             }
             __syncthreads();
-            for (int jj = q; jj < nnew; jj += C::NT / S2) {
+            for (int jj = q; jj < (a.dbg == 1 ? 0 : nnew); jj += C::NT / S2) {
                 if (tid >= (C::NT / S2) * S2) break;
                 const double* tm = TM + jj * V * S + o2b;
                 const double* tk = TK + jj * V * S + o2b;
@@ -244,7 +275,7 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const LineArgs a) 
             const int pad = padded ? 0 : (int)(g0 & 1);
             double* stM = stage + pad;
             double* stK = stage + C::STAGE + pad;
-            if (tid < C::ITEMS && 2 * q < tr) {
+            if (tid < C::ITEMS && 2 * q < tr && a.dbg != 1) {
                 const int j = 2 * q, r = t0 + j;
                 const int b0 = max(0, r - P);
                 double hm[V + 1], hk[V + 1];
@@ -259,11 +290,10 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const LineArgs a) 
                 double* dM = stM + j * SRr + S * o23;
                 double* dK = stK + j * SRr + S * o23;
                 if (r >= 2 * P && r + 1 <= n - 1 - P) {   // both rows class I (the common case)
-                    finish_interior<P, 0>(hm, hk, dM, dK, a);
-                    if (second) finish_interior<P, 1>(hm, hk, dM + SRr, dK + SRr, a);
+                    finish_pair_interior<P, MODE>(hm, hk, dM, dK, SRr, second, a);
                 } else {
-                    if (r >= 2 * P && r <= n - 1 - P) finish_interior<P, 0>(hm, hk, dM, dK, a);
-                    else finish_general<P>(r, hm, hk, dM, dK, a);
+                    if (r >= 2 * P && r <= n - 1 - P) finish_interior<P, MODE>(hm, hk, dM, dK, a);
+                    else finish_general<P, MODE>(r, hm, hk, dM, dK, a);
                     if (second) {
                         double hm1[V], hk1[V];
 #pragma unroll
@@ -271,42 +301,43 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const LineArgs a) 
                             hm1[v] = shift ? hm[v + 1] : hm[v];
                             hk1[v] = shift ? hk[v + 1] : hk[v];
                         }
-                        if (r + 1 >= 2 * P && r + 1 <= n - 1 - P) finish_interior<P, 0>(hm1, hk1, dM + SRr, dK + SRr, a);
-                        else finish_general<P>(r + 1, hm1, hk1, dM + SRr, dK + SRr, a);
+                        if (r + 1 >= 2 * P && r + 1 <= n - 1 - P) finish_interior<P, MODE>(hm1, hk1, dM + SRr, dK + SRr, a);
+                        else finish_general<P, MODE>(r + 1, hm1, hk1, dM + SRr, dK + SRr, a);
                     }
                 }
             }
             __syncthreads();
             // ---- store the tile: bulk copies of the 16-byte aligned interior, peeled ends ----
-            if (!padded) {
+            if (a.dbg == 2) {
+            } else if (!padded) {
                 const int total = tr * S3;
                 const int head = (int)(g0 & 1);
                 const int tail = (int)((g0 + total) & 1);
                 if (tid == 0) {
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    if (a.do_mass) bulk_store(a.M + g0 + head, stM + head, (uint32_t)(total - head - tail) * 8u);
-                    if (a.do_stiff) bulk_store(a.K + g0 + head, stK + head, (uint32_t)(total - head - tail) * 8u);
+                    if ((MODE & 1)) bulk_store(a.M + g0 + head, stM + head, (uint32_t)(total - head - tail) * 8u);
+                    if ((MODE & 2)) bulk_store(a.K + g0 + head, stK + head, (uint32_t)(total - head - tail) * 8u);
                     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 } else if (tid == 32 && head) {
-                    if (a.do_mass) a.M[g0] = stM[0];
-                    if (a.do_stiff) a.K[g0] = stK[0];
+                    if ((MODE & 1)) a.M[g0] = stM[0];
+                    if ((MODE & 2)) a.K[g0] = stK[0];
                 } else if (tid == 64 && tail) {
-                    if (a.do_mass) a.M[g0 + total - 1] = stM[total - 1];
-                    if (a.do_stiff) a.K[g0 + total - 1] = stK[total - 1];
+                    if ((MODE & 1)) a.M[g0 + total - 1] = stM[total - 1];
+                    if ((MODE & 2)) a.K[g0 + total - 1] = stK[total - 1];
                 }
             } else {                                       // even ld: rows start 16B-aligned
                 if (tid == 0) {
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     for (int j = 0; j < tr; ++j) {
-                        if (a.do_mass) bulk_store(a.M + (orow0 + j) * a.ld, stM + j * SRr, (uint32_t)(S3 - 1) * 8u);
-                        if (a.do_stiff) bulk_store(a.K + (orow0 + j) * a.ld, stK + j * SRr, (uint32_t)(S3 - 1) * 8u);
+                        if ((MODE & 1)) bulk_store(a.M + (orow0 + j) * a.ld, stM + j * SRr, (uint32_t)(S3 - 1) * 8u);
+                        if ((MODE & 2)) bulk_store(a.K + (orow0 + j) * a.ld, stK + j * SRr, (uint32_t)(S3 - 1) * 8u);
                     }
                     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 }
                 if (tid >= 32 && tid < 32 + tr) {
                     const int j = tid - 32;
-                    if (a.do_mass) a.M[(orow0 + j) * a.ld + S3 - 1] = stM[j * SRr + S3 - 1];
-                    if (a.do_stiff) a.K[(orow0 + j) * a.ld + S3 - 1] = stK[j * SRr + S3 - 1];
+                    if ((MODE & 1)) a.M[(orow0 + j) * a.ld + S3 - 1] = stM[j * SRr + S3 - 1];
+                    if ((MODE & 2)) a.K[(orow0 + j) * a.ld + S3 - 1] = stK[j * SRr + S3 - 1];
                 }
             }
             ++tiles;
@@ -315,56 +346,29 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const LineArgs a) 
     if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-template <int P>
+template <int P, int MODE>
 int launch_line_p(const LineArgs& a, cudaStream_t st) {
     using C = Cfg<P>;
     const size_t smem = (size_t)C::SMEM * sizeof(double);
-    if (cudaFuncSetAttribute(k_line_grid3<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    auto kern = k_line_grid3<P, MODE>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return WGQ_ECUDA;
-    cudaFuncSetAttribute(k_line_grid3<P>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_line_grid3<P>, C::NT, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::NT, smem);
     const int64_t lines = (a.row_end - 1) / a.N - a.row_begin / a.N + 1;
     int64_t blocks = std::min<int64_t>(lines, (int64_t)sms * std::max(per_sm, 1));
-    k_line_grid3<P><<<(unsigned)std::max<int64_t>(blocks, 1), C::NT, smem, st>>>(a);
+    kern<<<(unsigned)std::max<int64_t>(blocks, 1), C::NT, smem, st>>>(a);
     return cudaGetLastError() == cudaSuccess ? WGQ_OK : WGQ_ECUDA;
 }
 
-std::mutex g_const_mu;
-bool g_const_ready[64][4] = {};
-
-int upload_constants(const wgq_rules_s* R) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    std::lock_guard<std::mutex> lock(g_const_mu);
-    if (dev < 64 && g_const_ready[dev][R->p]) return WGQ_OK;
-    double PM[kMaxV][kMaxS], PK[kMaxV][kMaxS];
-    interior_vertex_tables(R->p, R->rules[WGQ_MASS][R->p], R->rules[WGQ_STIFFNESS][R->p], PM, PK);
-    cudaError_t e1, e2;
-    if (R->p == 3) {
-        double m[5][7], k[5][7];
-        for (int v = 0; v < 5; ++v)
-            for (int o = 0; o < 7; ++o) {
-                m[v][o] = PM[v][o];
-                k[v][o] = PK[v][o];
-            }
-        e1 = cudaMemcpyToSymbol(c_PM3, m, sizeof m);
-        e2 = cudaMemcpyToSymbol(c_PK3, k, sizeof k);
-    } else {
-        double m[4][5], k[4][5];
-        for (int v = 0; v < 4; ++v)
-            for (int o = 0; o < 5; ++o) {
-                m[v][o] = PM[v][o];
-                k[v][o] = PK[v][o];
-            }
-        e1 = cudaMemcpyToSymbol(c_PM2, m, sizeof m);
-        e2 = cudaMemcpyToSymbol(c_PK2, k, sizeof k);
-    }
-    if (e1 != cudaSuccess || e2 != cudaSuccess) return WGQ_ECUDA;
-    if (dev < 64) g_const_ready[dev][R->p] = true;
-    return WGQ_OK;
+template <int P>
+int launch_line_mode(const LineArgs& a, int mode, cudaStream_t st) {
+    if (mode == 3) return launch_line_p<P, 3>(a, st);
+    if (mode == 1) return launch_line_p<P, 1>(a, st);
+    return launch_line_p<P, 2>(a, st);
 }
 
 }  // namespace
@@ -385,8 +389,6 @@ bool line_kernel_applies(const wgq_rules_s* R, const wgq_coeff_t* c, const wgq_o
 
 int launch_line(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, const wgq_out_t* M,
                 const wgq_out_t* K, void* stream) {
-    int rc = upload_constants(R);
-    if (rc != WGQ_OK) return rc;
     const wgq_out_t* o = M ? M : K;
     LineArgs a{};
     a.T = T;
@@ -400,13 +402,22 @@ int launch_line(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, 
     a.M = M ? M->values : nullptr;
     a.K = K ? K->values : nullptr;
     a.ld = o->ld;
-    a.do_mass = M != nullptr;
-    a.do_stiff = K != nullptr;
+    const int mode = (M ? 1 : 0) | (K ? 2 : 0);
     a.h = 1.0 / (double)R->n;
     a.inv_h = (double)R->n;
+    {
+        double PM[kMaxV][kMaxS], PK[kMaxV][kMaxS];
+        interior_vertex_tables(R->p, R->rules[WGQ_MASS][R->p], R->rules[WGQ_STIFFNESS][R->p], PM, PK);
+        for (int v = 0; v < kMaxV; ++v)
+            for (int o1 = 0; o1 < kMaxS; ++o1) {
+                a.PMh[v][o1] = PM[v][o1] * a.h;
+                a.PKi[v][o1] = PK[v][o1] * a.inv_h;
+            }
+    }
+    if (const char* e = getenv("WGQ_LINE_DBG")) a.dbg = atoi(e);
     if (a.row_end <= a.row_begin) return WGQ_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    return R->p == 3 ? launch_line_p<3>(a, st) : launch_line_p<2>(a, st);
+    return R->p == 3 ? launch_line_mode<3>(a, mode, st) : launch_line_mode<2>(a, mode, st);
 }
 
 }  // namespace wgq

@@ -1,0 +1,53 @@
+"""Device-time a config's assembly (kernel experiments; not the bench contract).
+
+    python tools/time_case.py --config C5 [--n 256] [--reps 5] [--dbg 0,1,2]
+
+Prints ms per launch (CUDA events, best and median of reps, L2 flushed between reps) and
+the achieved algorithmic GB/s, for each WGQ_LINE_DBG mode listed (profiling switches of the
+line kernel: 1 = skip compute, 2 = skip stores).
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import inputs  # noqa: E402
+from paper_1710_01048_b200 import api, wgq  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="C5")
+ap.add_argument("--n", type=int, default=None)
+ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--dbg", default="0")
+ap.add_argument("--ld", type=int, default=None)
+a = ap.parse_args()
+cfg = inputs.config(a.config, a.n)
+rules = wgq.Rules(cfg["p"], cfg["n"], cfg["dim"])
+grid, plane0 = (None, 0)
+if cfg["coeff"]["kind"] == "grid":
+    grid, plane0 = api.make_grid(rules, cfg["coeff"]["seed"], cfg["coeff"]["sigma"], 0, rules.n_rows)
+coef = api.coefficient(inputs.coefficient(cfg["coeff"], cfg["dim"]), grid, plane0)
+out = {k: api.alloc_ell(rules, 0, rules.n_rows, a.ld) for k in cfg["kinds"]}
+flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+alg = rules.n_rows * rules.stencil * 8 * len(cfg["kinds"])
+res = {}
+for mode in a.dbg.split(","):
+    os.environ["WGQ_LINE_DBG"] = mode
+    api.assemble(rules, coef, cfg["kinds"], out=out)
+    ts = []
+    for _ in range(a.reps):
+        flush.fill_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        api.assemble(rules, coef, cfg["kinds"], out=out)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ts.sort()
+    res[mode] = {"best_ms": round(ts[0], 4), "median_ms": round(ts[len(ts) // 2], 4),
+                 "GBs": round(alg / ts[0] / 1e6, 1)}
+print(json.dumps({"config": cfg["name"], "n": cfg["n"], "rows": rules.n_rows, "modes": res}))
