@@ -49,7 +49,7 @@ struct Cfg {
     static constexpr int SR = S3 + 1;                  // staging row stride for padded ld
     static constexpr int STAGE = TR * SR + 2;          // doubles per staging buffer per matrix
     static constexpr int PATCH = W * V * V;
-    static constexpr int SMEM = 2 * STAGE + RING * 2 * S2 + 4 * V * S + 2 * PATCH + 2 * W * V * S;
+    static constexpr int SMEM = 2 * STAGE + RING * 2 * S2 + 3 * 4 * V * S + 3 * PATCH + 2 * W * V * S;
     static_assert(W <= RING, "ring too small");
 };
 
@@ -178,6 +178,75 @@ __device__ __forceinline__ void finish_general(int r, const double* hm, const do
     }
 }
 
+// Iterator over a CTA's tiles: lines first_line + blockIdx.x + m * gridDim.x, TR rows per
+// tile.  Per-line quantities are refreshed only when the line changes, so the per-tile cost
+// (paid by every thread of the CTA) is a few adds and compares.
+struct TileIt {
+    int line, i2, i3, x0, x1, t0;
+    int qs;      // Q buffer of the line: line ordinal % 3
+    int ps;      // patch buffer of the tile: tile ordinal % 3
+    int lo, hi;  // vertex planes the tile adds to the line's H ring
+};
+
+template <int P>
+__device__ __forceinline__ void it_planes(TileIt& t) {
+    constexpr int V = P + 2;
+    t.lo = t.t0 == t.x0 ? max(0, t.x0 - P) : max(0, t.t0 - 1 - P) + V;
+    t.hi = max(0, min(t.t0 + Cfg<P>::TR, t.x1) - 1 - P) + V - 1;
+}
+
+template <int P>
+__device__ __forceinline__ void it_line(const LineArgs& a, TileIt& t) {
+    t.i2 = t.line % a.N;
+    t.i3 = t.line / a.N;
+    t.x0 = max(a.row_begin, t.line * a.N) - t.line * a.N;
+    t.x1 = min(a.row_end, t.line * a.N + a.N) - t.line * a.N;
+    t.t0 = t.x0;
+}
+
+template <int P>
+__device__ __forceinline__ void it_init(const LineArgs& a, TileIt& t) {
+    t.line = a.row_begin / a.N + blockIdx.x;
+    t.qs = 0;
+    t.ps = 0;
+    it_line<P>(a, t);
+    it_planes<P>(t);
+}
+
+template <int P>
+__device__ __forceinline__ void it_next(const LineArgs& a, TileIt& t) {
+    t.t0 += Cfg<P>::TR;
+    t.ps = t.ps == 2 ? 0 : t.ps + 1;
+    if (t.t0 >= t.x1) {
+        t.line += gridDim.x;
+        t.qs = t.qs == 2 ? 0 : t.qs + 1;
+        it_line<P>(a, t);
+    }
+    it_planes<P>(t);
+}
+
+// Issue (cp.async, one commit group) everything tile t reads from global memory: its new
+// vertex planes into patch buffer t.ps and, for a line's first tile, the line's y/z vertex
+// tables into Q buffer t.qs.  An exhausted iterator commits an empty group.
+template <int P>
+__device__ __forceinline__ void tile_issue(const LineArgs& a, double* patches, double* qbufs, const TileIt& t,
+                                           int last_line, int tid) {
+    using C = Cfg<P>;
+    constexpr int V = C::V, S = C::S;
+    if (t.line <= last_line) {
+        load_patch<P>(a, patches + t.ps * C::PATCH, t.lo, t.hi - t.lo + 1, max(0, t.i2 - P), max(0, t.i3 - P), tid);
+        if (t.t0 == t.x0) {
+            double* Q = qbufs + t.qs * (4 * V * S);
+            for (int e = tid; e < 4 * V * S; e += C::NT) {
+                const int which = e / (V * S), v = (e / S) % V, o = e % S;
+                const int r = which < 2 ? t.i2 : t.i3;
+                cp_async8(Q + e, ((which & 1) ? a.T.PK : a.T.PM) + ((size_t)r * kMaxV + v) * kMaxS + o, true);
+            }
+        }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
 template <int P, int MODE>
 __global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const __grid_constant__ LineArgs a) {
     using C = Cfg<P>;
@@ -186,163 +255,149 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const __grid_const
     double* stage = sm;                                   // [2 mat][STAGE] (single buffer)
     double* Hm = stage + 2 * C::STAGE;                    // [RING][S2]
     double* Hk = Hm + RING * S2;                          // [RING][S2]
-    double* Q = Hk + RING * S2;                           // QyM, QyK, QzM, QzK: [V][S] each
-    double* patches = Q + 4 * V * S;                      // [2][W][V(z)][V(y)]
-    double* TM = patches + 2 * C::PATCH;                  // [W][V(z)][S(o2)]
+    double* qbufs = Hk + RING * S2;                       // [3][QyM, QyK, QzM, QzK: [V][S] each]
+    double* patches = qbufs + 3 * 4 * V * S;              // [3][W][V(z)][V(y)]
+    double* TM = patches + 3 * C::PATCH;                  // [W][V(z)][S(o2)]
     double* TK = TM + C::W * V * S;
-    const double* QyM = Q;
-    const double* QyK = Q + V * S;
-    const double* QzM = Q + 2 * V * S;
-    const double* QzK = Q + 3 * V * S;
 
     const int tid = threadIdx.x;
     const int n = a.n, N = a.N;
     const bool padded = a.ld != S3;
     const int SRr = padded ? C::SR : S3;
     const int first_line = a.row_begin / N, last_line = (a.row_end - 1) / N;
-    // fixed per-thread roles: phase B / A3 item (row pair q, o23); A2 item (plane, vz, o2)
+    // fixed per-thread roles: phase B / A2 item (row pair q, o23)
     const int q = tid / S2, o23 = tid % S2, o2b = o23 % S, o3b = o23 / S;
-    int tiles = 0, pbuf = 0;
 
-    for (int line = first_line + blockIdx.x; line <= last_line; line += gridDim.x) {
-        const int i2 = line % N, i3 = line / N;
-        const int x0 = max(a.row_begin, line * N) - line * N;
-        const int x1 = min(a.row_end, line * N + N) - line * N;
-        const int by = max(0, i2 - P), bz = max(0, i3 - P);
-        __syncthreads();                                   // previous line done with Q / H / patches
-        for (int e = tid; e < 4 * V * S; e += C::NT) {
-            const int which = e / (V * S), v = (e / S) % V, o = e % S;
-            const int r = which < 2 ? i2 : i3;
-            const double* src = (which & 1) ? a.T.PK : a.T.PM;
-            Q[e] = src[((size_t)r * kMaxV + v) * kMaxS + o];
-        }
-        int hcomp = max(0, x0 - P) - 1;                     // vertex planes computed: (hcomp-RING, hcomp]
-        {
-            const int last = min(x0 + TR, x1) - 1;
-            const int hi = max(0, last - P) + V - 1;
-            load_patch<P>(a, patches + pbuf * C::PATCH, hcomp + 1, hi - hcomp, by, bz, tid);
-        }
-        for (int t0 = x0; t0 < x1; t0 += TR) {
-            const int tr = min(TR, x1 - t0);
-            const int hi_need = max(0, t0 + tr - 1 - P) + V - 1;
-            const int c0 = hcomp + 1;
-            const int nnew = hi_need - hcomp;              // >= 1: the window moves every tile
-            const double* patch = patches + pbuf * C::PATCH;
-            // ---- phase A: new vertex planes c0..hi_need -> HM, HK --------------------------
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
-            __syncthreads();                               // patch + Q visible; ring slots free
-            for (int e = tid; e < (a.dbg == 1 ? 0 : nnew * V * S); e += C::NT) {
-                const int o2 = e % S, vz = (e / S) % V, j = e / (S * V);
-                const double* pr = patch + (j * V + vz) * V;
-                double sm_ = 0.0, sk = 0.0;
-#pragma unroll
-                for (int vy = 0; vy < V; ++vy) {
-                    sm_ = fma(pr[vy], QyM[vy * S + o2], sm_);
-                    sk = fma(pr[vy], QyK[vy * S + o2], sk);
-                }
-                TM[(j * V + vz) * S + o2] = sm_;
-                TK[(j * V + vz) * S + o2] = sk;
-            }
-            if (t0 + TR < x1) {                            // prefetch the next tile's patch
-                const int nlast = min(t0 + 2 * TR, x1) - 1;
-                const int nhi = max(0, nlast - P) + V - 1;
-                load_patch<P>(a, patches + (pbuf ^ 1) * C::PATCH, hi_need + 1, nhi - hi_need, by, bz, tid);
-            }
-            __syncthreads();
-            for (int jj = q; jj < (a.dbg == 1 ? 0 : nnew); jj += C::NT / S2) {
-                if (tid >= (C::NT / S2) * S2) break;
-                const double* tm = TM + jj * V * S + o2b;
-                const double* tk = TK + jj * V * S + o2b;
-                double hm = 0.0, hk = 0.0, hk2 = 0.0;
-#pragma unroll
-                for (int vz = 0; vz < V; ++vz) {
-                    hm = fma(tm[vz * S], QzM[vz * S + o3b], hm);
-                    hk = fma(tk[vz * S], QzM[vz * S + o3b], hk);
-                    hk2 = fma(tm[vz * S], QzK[vz * S + o3b], hk2);
-                }
-                const int slot = (c0 + jj) & (RING - 1);
-                Hm[slot * S2 + o23] = hm;
-                Hk[slot * S2 + o23] = hk + hk2;
-            }
-            hcomp = hi_need;
-            pbuf ^= 1;
-            // ---- phase B: row pairs of the tile -> staging ---------------------------------
-            // the single staging buffer was read by the previous tile's bulk copy during phase A
-            if (tiles >= 1 && tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-            __syncthreads();                               // H ready; staging buffer free
-            const long long orow0 = (long long)line * N + t0 - a.row_begin;   // output row of the tile
-            const long long g0 = orow0 * a.ld;                                // first element
-            const int pad = padded ? 0 : (int)(g0 & 1);
-            double* stM = stage + pad;
-            double* stK = stage + C::STAGE + pad;
-            if (tid < C::ITEMS && 2 * q < tr && a.dbg != 1) {
-                const int j = 2 * q, r = t0 + j;
-                const int b0 = max(0, r - P);
-                double hm[V + 1], hk[V + 1];
-#pragma unroll
-                for (int v = 0; v <= V; ++v) {             // planes b0 .. b0+V (the pair's union)
-                    const int slot = (b0 + v) & (RING - 1);
-                    hm[v] = Hm[slot * S2 + o23];
-                    hk[v] = Hk[slot * S2 + o23];
-                }
-                const bool second = j + 1 < tr;
-                const bool shift = r + 1 - P > 0;          // row r+1's window starts one plane later
-                double* dM = stM + j * SRr + S * o23;
-                double* dK = stK + j * SRr + S * o23;
-                if (r >= 2 * P && r + 1 <= n - 1 - P) {   // both rows class I (the common case)
-                    finish_pair_interior<P, MODE>(hm, hk, dM, dK, SRr, second, a);
-                } else {
-                    if (r >= 2 * P && r <= n - 1 - P) finish_interior<P, MODE>(hm, hk, dM, dK, a);
-                    else finish_general<P, MODE>(r, hm, hk, dM, dK, a);
-                    if (second) {
-                        double hm1[V], hk1[V];
-#pragma unroll
-                        for (int v = 0; v < V; ++v) {
-                            hm1[v] = shift ? hm[v + 1] : hm[v];
-                            hk1[v] = shift ? hk[v + 1] : hk[v];
-                        }
-                        if (r + 1 >= 2 * P && r + 1 <= n - 1 - P) finish_interior<P, MODE>(hm1, hk1, dM + SRr, dK + SRr, a);
-                        else finish_general<P, MODE>(r + 1, hm1, hk1, dM + SRr, dK + SRr, a);
-                    }
-                }
-            }
-            __syncthreads();
-            // ---- store the tile: bulk copies of the 16-byte aligned interior, peeled ends ----
-            if (a.dbg == 2) {
-            } else if (!padded) {
-                const int total = tr * S3;
-                const int head = (int)(g0 & 1);
-                const int tail = (int)((g0 + total) & 1);
-                if (tid == 0) {
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    if ((MODE & 1)) bulk_store(a.M + g0 + head, stM + head, (uint32_t)(total - head - tail) * 8u);
-                    if ((MODE & 2)) bulk_store(a.K + g0 + head, stK + head, (uint32_t)(total - head - tail) * 8u);
-                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                } else if (tid == 32 && head) {
-                    if ((MODE & 1)) a.M[g0] = stM[0];
-                    if ((MODE & 2)) a.K[g0] = stK[0];
-                } else if (tid == 64 && tail) {
-                    if ((MODE & 1)) a.M[g0 + total - 1] = stM[total - 1];
-                    if ((MODE & 2)) a.K[g0 + total - 1] = stK[total - 1];
-                }
-            } else {                                       // even ld: rows start 16B-aligned
-                if (tid == 0) {
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    for (int j = 0; j < tr; ++j) {
-                        if ((MODE & 1)) bulk_store(a.M + (orow0 + j) * a.ld, stM + j * SRr, (uint32_t)(S3 - 1) * 8u);
-                        if ((MODE & 2)) bulk_store(a.K + (orow0 + j) * a.ld, stK + j * SRr, (uint32_t)(S3 - 1) * 8u);
-                    }
-                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                }
-                if (tid >= 32 && tid < 32 + tr) {
-                    const int j = tid - 32;
-                    if ((MODE & 1)) a.M[(orow0 + j) * a.ld + S3 - 1] = stM[j * SRr + S3 - 1];
-                    if ((MODE & 2)) a.K[(orow0 + j) * a.ld + S3 - 1] = stK[j * SRr + S3 - 1];
-                }
-            }
-            ++tiles;
-        }
+    (void)first_line;
+    TileIt it, pf;                                     // current tile, prefetch (two ahead)
+    it_init<P>(a, it);
+    pf = it;
+    for (int k = 0; k < 2; ++k) {
+        tile_issue<P>(a, patches, qbufs, pf, last_line, tid);
+        if (pf.line <= last_line) it_next<P>(a, pf);
     }
+    for (int k = 0; it.line <= last_line; ++k) {
+        const int line = it.line, t0 = it.t0;
+        const int tr = min(TR, it.x1 - t0);
+        const int c0 = it.lo, hi_need = it.hi;
+        const int nnew = hi_need - c0 + 1;
+        const double* patch = patches + it.ps * C::PATCH;
+        const double* Q = qbufs + it.qs * (4 * V * S);
+        const double* QyM = Q;
+        const double* QyK = Q + V * S;
+        const double* QzM = Q + 2 * V * S;
+        const double* QzK = Q + 3 * V * S;
+        // ---- phase A: new vertex planes c0..hi_need -> HM, HK --------------------------
+        asm volatile("cp.async.wait_group 1;" ::: "memory");   // tile k landed (k+1 may be pending)
+        __syncthreads();                               // patch + Q visible; ring slots / T free
+        for (int e = tid; e < (a.dbg == 1 ? 0 : nnew * V * S); e += C::NT) {
+            const int o2 = e % S, vz = (e / S) % V, j = e / (S * V);
+            const double* pr = patch + (j * V + vz) * V;
+            double sm_ = 0.0, sk = 0.0;
+#pragma unroll
+            for (int vy = 0; vy < V; ++vy) {
+                sm_ = fma(pr[vy], QyM[vy * S + o2], sm_);
+                sk = fma(pr[vy], QyK[vy * S + o2], sk);
+            }
+            TM[(j * V + vz) * S + o2] = sm_;
+            TK[(j * V + vz) * S + o2] = sk;
+        }
+        // prefetch tile k+2 into patch buffer (k+2) % 3 (last read by tile k-1's phase A)
+        tile_issue<P>(a, patches, qbufs, pf, last_line, tid);
+        if (pf.line <= last_line) it_next<P>(a, pf);
+        __syncthreads();
+        for (int jj = q; jj < (a.dbg == 1 ? 0 : nnew); jj += C::NT / S2) {
+            if (tid >= (C::NT / S2) * S2) break;
+            const double* tm = TM + jj * V * S + o2b;
+            const double* tk = TK + jj * V * S + o2b;
+            double hm = 0.0, hk = 0.0, hk2 = 0.0;
+#pragma unroll
+            for (int vz = 0; vz < V; ++vz) {
+                hm = fma(tm[vz * S], QzM[vz * S + o3b], hm);
+                hk = fma(tk[vz * S], QzM[vz * S + o3b], hk);
+                hk2 = fma(tm[vz * S], QzK[vz * S + o3b], hk2);
+            }
+            const int slot = (c0 + jj) & (RING - 1);
+            Hm[slot * S2 + o23] = hm;
+            Hk[slot * S2 + o23] = hk + hk2;
+        }
+        // ---- phase B: row pairs of the tile -> staging ---------------------------------
+        // the single staging buffer was read by the previous tile's bulk copy during phase A
+        if (k >= 1 && tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncthreads();                               // H ready; staging buffer free
+        const long long orow0 = (long long)line * N + t0 - a.row_begin;   // output row of the tile
+        const long long g0 = orow0 * a.ld;                                // first element
+        const int pad = padded ? 0 : (int)(g0 & 1);
+        double* stM = stage + pad;
+        double* stK = stage + C::STAGE + pad;
+        if (tid < C::ITEMS && 2 * q < tr && a.dbg != 1) {
+            const int j = 2 * q, r = t0 + j;
+            const int b0 = max(0, r - P);
+            double hm[V + 1], hk[V + 1];
+#pragma unroll
+            for (int v = 0; v <= V; ++v) {             // planes b0 .. b0+V (the pair's union)
+                const int slot = (b0 + v) & (RING - 1);
+                hm[v] = Hm[slot * S2 + o23];
+                hk[v] = Hk[slot * S2 + o23];
+            }
+            const bool second = j + 1 < tr;
+            const bool shift = r + 1 - P > 0;          // row r+1's window starts one plane later
+            double* dM = stM + j * SRr + S * o23;
+            double* dK = stK + j * SRr + S * o23;
+            if (r >= 2 * P && r + 1 <= n - 1 - P) {   // both rows class I (the common case)
+                finish_pair_interior<P, MODE>(hm, hk, dM, dK, SRr, second, a);
+            } else {
+                if (r >= 2 * P && r <= n - 1 - P) finish_interior<P, MODE>(hm, hk, dM, dK, a);
+                else finish_general<P, MODE>(r, hm, hk, dM, dK, a);
+                if (second) {
+                    double hm1[V], hk1[V];
+#pragma unroll
+                    for (int v = 0; v < V; ++v) {
+                        hm1[v] = shift ? hm[v + 1] : hm[v];
+                        hk1[v] = shift ? hk[v + 1] : hk[v];
+                    }
+                    if (r + 1 >= 2 * P && r + 1 <= n - 1 - P) finish_interior<P, MODE>(hm1, hk1, dM + SRr, dK + SRr, a);
+                    else finish_general<P, MODE>(r + 1, hm1, hk1, dM + SRr, dK + SRr, a);
+                }
+            }
+        }
+        __syncthreads();
+        // ---- store the tile: bulk copies of the 16-byte aligned interior, peeled ends ----
+        if (a.dbg == 2) {
+        } else if (!padded) {
+            const int total = tr * S3;
+            const int head = (int)(g0 & 1);
+            const int tail = (int)((g0 + total) & 1);
+            if (tid == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                if (MODE & 1) bulk_store(a.M + g0 + head, stM + head, (uint32_t)(total - head - tail) * 8u);
+                if (MODE & 2) bulk_store(a.K + g0 + head, stK + head, (uint32_t)(total - head - tail) * 8u);
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            } else if (tid == 32 && head) {
+                if (MODE & 1) a.M[g0] = stM[0];
+                if (MODE & 2) a.K[g0] = stK[0];
+            } else if (tid == 64 && tail) {
+                if (MODE & 1) a.M[g0 + total - 1] = stM[total - 1];
+                if (MODE & 2) a.K[g0 + total - 1] = stK[total - 1];
+            }
+        } else {                                       // even ld: rows start 16B-aligned
+            if (tid == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                for (int j = 0; j < tr; ++j) {
+                    if (MODE & 1) bulk_store(a.M + (orow0 + j) * a.ld, stM + j * SRr, (uint32_t)(S3 - 1) * 8u);
+                    if (MODE & 2) bulk_store(a.K + (orow0 + j) * a.ld, stK + j * SRr, (uint32_t)(S3 - 1) * 8u);
+                }
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+            if (tid >= 32 && tid < 32 + tr) {
+                const int j = tid - 32;
+                if (MODE & 1) a.M[(orow0 + j) * a.ld + S3 - 1] = stM[j * SRr + S3 - 1];
+                if (MODE & 2) a.K[(orow0 + j) * a.ld + S3 - 1] = stK[j * SRr + S3 - 1];
+            }
+        }
+        it_next<P>(a, it);
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
     if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
