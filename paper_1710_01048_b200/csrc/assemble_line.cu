@@ -49,7 +49,7 @@ struct Cfg {
     static constexpr int SR = S3 + 1;                  // staging row stride for padded ld
     static constexpr int STAGE = TR * SR + 2;          // doubles per staging buffer per matrix
     static constexpr int PATCH = W * V * V;
-    static constexpr int SMEM = 2 * STAGE + RING * 2 * S2 + 3 * 4 * V * S + 3 * PATCH + 2 * W * V * S;
+    static constexpr int SMEM = 2 * STAGE + RING * 2 * S2 + 3 * 4 * V * S + 3 * PATCH;
     static_assert(W <= RING, "ring too small");
 };
 
@@ -247,6 +247,79 @@ __device__ __forceinline__ void tile_issue(const LineArgs& a, double* patches, d
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+// Phase A of tile t on the FP64 tensor cores (DMMA m8n8k4), one warp per new vertex plane c:
+//   A1:  TT_X[o2][vz] = sum_vy Qy_X[vy][o2] g[bz+vz][by+vy][c]      (X = M, K)
+//   A2:  HM[o2][o3]  = sum_vz TT_M[o2][vz] Qz_M[vz][o3]
+//        HK[o2][o3]  = sum_vz TT_K[o2][vz] Qz_M[vz][o3] + TT_M[o2][vz] Qz_K[vz][o3]
+// Fragments (lane = 4 g + t): A[g][t], B[t][g], C[g][2t+i].  The A1 output columns are
+// permuted, column 2t+i <-> vz = t + 4i, so each lane ends A1 holding exactly its A2 A-fragment
+// (TT[g][t], TT[g][t+4]): no shuffle or shared-memory round trip between the two products.
+// Padding rows / columns (o2, o3 >= S, vy, vz >= V) carry zero coefficients.
+template <int P>
+__device__ __forceinline__ void phase_a(const LineArgs& a, const TileIt& t, const double* patches,
+                                        const double* qbufs, double* Hm, double* Hk, int tid) {
+    using C = Cfg<P>;
+    constexpr int V = C::V, S = C::S, S2 = C::S2, RING = C::RING;
+    constexpr int KS = (V + 3) / 4;                    // k-steps of 4 (p=3: 2, p=2: 1)
+    constexpr int NW = C::NT / 32;
+    const int lane = tid & 31, warp = tid >> 5, g = lane >> 2, tq = lane & 3;
+    const double* Q = qbufs + t.qs * (4 * V * S);
+    double aYM[KS], aYK[KS], bZM[KS], bZK[KS];
+#pragma unroll
+    for (int s = 0; s < KS; ++s) {
+        const int v = tq + 4 * s;
+        const bool ok = g < S && v < V;
+        const int e = ok ? v * S + g : 0;
+        aYM[s] = ok ? Q[e] : 0.0;
+        aYK[s] = ok ? Q[V * S + e] : 0.0;
+        bZM[s] = ok ? Q[2 * V * S + e] : 0.0;
+        bZK[s] = ok ? Q[3 * V * S + e] : 0.0;
+    }
+    const double* patch = patches + t.ps * C::PATCH;
+    const int nnew = t.hi - t.lo + 1;
+    const int vzp = (g >> 1) + 4 * (g & 1);            // B column g of A1 <-> vz = pi(g)
+    for (int j = NW - 1 - warp; j < (a.dbg == 1 ? 0 : nnew); j += NW) {
+        double tM0 = 0.0, tM1 = 0.0, tK0 = 0.0, tK1 = 0.0;
+#pragma unroll
+        for (int s = 0; s < KS; ++s) {
+            const int vy = tq + 4 * s;
+            const double b = (vzp < V && vy < V) ? patch[(j * V + vzp) * V + vy] : 0.0;
+            dmma(tM0, tM1, aYM[s], b);
+            dmma(tK0, tK1, aYK[s], b);
+        }
+        // lane holds TT_X[o2 = g][vz = tq] (x0) and TT_X[g][tq + 4] (x1)
+        double hM0 = 0.0, hM1 = 0.0, hK0 = 0.0, hK1 = 0.0;
+        dmma(hM0, hM1, tM0, bZM[0]);
+        dmma(hK0, hK1, tK0, bZM[0]);
+        dmma(hK0, hK1, tM0, bZK[0]);
+        if (KS > 1) {
+            dmma(hM0, hM1, tM1, bZM[KS - 1]);
+            dmma(hK0, hK1, tK1, bZM[KS - 1]);
+            dmma(hK0, hK1, tM1, bZK[KS - 1]);
+        }
+        const int slot = (t.lo + j) & (RING - 1);
+        const int o3 = 2 * tq;
+        if (g < S) {
+            double* hm = Hm + slot * S2 + g;
+            double* hk = Hk + slot * S2 + g;
+            if (o3 < S) {
+                hm[S * o3] = hM0;
+                hk[S * o3] = hK0;
+            }
+            if (o3 + 1 < S) {
+                hm[S * (o3 + 1)] = hM1;
+                hk[S * (o3 + 1)] = hK1;
+            }
+        }
+    }
+}
+
 template <int P, int MODE>
 __global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const __grid_constant__ LineArgs a) {
     using C = Cfg<P>;
@@ -257,79 +330,49 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const __grid_const
     double* Hk = Hm + RING * S2;                          // [RING][S2]
     double* qbufs = Hk + RING * S2;                       // [3][QyM, QyK, QzM, QzK: [V][S] each]
     double* patches = qbufs + 3 * 4 * V * S;              // [3][W][V(z)][V(y)]
-    double* TM = patches + 3 * C::PATCH;                  // [W][V(z)][S(o2)]
-    double* TK = TM + C::W * V * S;
 
     const int tid = threadIdx.x;
     const int n = a.n, N = a.N;
     const bool padded = a.ld != S3;
     const int SRr = padded ? C::SR : S3;
     const int first_line = a.row_begin / N, last_line = (a.row_end - 1) / N;
-    // fixed per-thread roles: phase B / A2 item (row pair q, o23)
-    const int q = tid / S2, o23 = tid % S2, o2b = o23 % S, o3b = o23 / S;
+    // fixed per-thread role in phase B: item (row pair q, o23)
+    const int q = tid / S2, o23 = tid % S2;
 
     (void)first_line;
-    TileIt it, pf;                                     // current tile, prefetch (two ahead)
-    it_init<P>(a, it);
-    pf = it;
+    // Software pipeline, two barriers per tile:
+    //   S1(k): phase B of tile k (H -> staging)
+    //   S2(k): bulk store of tile k  +  phase A of tile k+1 (patch -> H ring)  +  prefetch k+3
+    // The H ring holds a tile's window (W planes) and the next tile's new planes are written
+    // only after that tile's phase B (S2 follows S1), so RING >= W suffices.
+    TileIt itB, itA, itP;                               // tile k, tile k+1, prefetch tile k+3
+    it_init<P>(a, itB);
+    itP = itB;
     for (int k = 0; k < 2; ++k) {
-        tile_issue<P>(a, patches, qbufs, pf, last_line, tid);
-        if (pf.line <= last_line) it_next<P>(a, pf);
+        tile_issue<P>(a, patches, qbufs, itP, last_line, tid);
+        if (itP.line <= last_line) it_next<P>(a, itP);
     }
-    for (int k = 0; it.line <= last_line; ++k) {
-        const int line = it.line, t0 = it.t0;
-        const int tr = min(TR, it.x1 - t0);
-        const int c0 = it.lo, hi_need = it.hi;
-        const int nnew = hi_need - c0 + 1;
-        const double* patch = patches + it.ps * C::PATCH;
-        const double* Q = qbufs + it.qs * (4 * V * S);
-        const double* QyM = Q;
-        const double* QyK = Q + V * S;
-        const double* QzM = Q + 2 * V * S;
-        const double* QzK = Q + 3 * V * S;
-        // ---- phase A: new vertex planes c0..hi_need -> HM, HK --------------------------
-        asm volatile("cp.async.wait_group 1;" ::: "memory");   // tile k landed (k+1 may be pending)
-        __syncthreads();                               // patch + Q visible; ring slots / T free
-        for (int e = tid; e < (a.dbg == 1 ? 0 : nnew * V * S); e += C::NT) {
-            const int o2 = e % S, vz = (e / S) % V, j = e / (S * V);
-            const double* pr = patch + (j * V + vz) * V;
-            double sm_ = 0.0, sk = 0.0;
-#pragma unroll
-            for (int vy = 0; vy < V; ++vy) {
-                sm_ = fma(pr[vy], QyM[vy * S + o2], sm_);
-                sk = fma(pr[vy], QyK[vy * S + o2], sk);
-            }
-            TM[(j * V + vz) * S + o2] = sm_;
-            TK[(j * V + vz) * S + o2] = sk;
-        }
-        // prefetch tile k+2 into patch buffer (k+2) % 3 (last read by tile k-1's phase A)
-        tile_issue<P>(a, patches, qbufs, pf, last_line, tid);
-        if (pf.line <= last_line) it_next<P>(a, pf);
-        __syncthreads();
-        for (int jj = q; jj < (a.dbg == 1 ? 0 : nnew); jj += C::NT / S2) {
-            if (tid >= (C::NT / S2) * S2) break;
-            const double* tm = TM + jj * V * S + o2b;
-            const double* tk = TK + jj * V * S + o2b;
-            double hm = 0.0, hk = 0.0, hk2 = 0.0;
-#pragma unroll
-            for (int vz = 0; vz < V; ++vz) {
-                hm = fma(tm[vz * S], QzM[vz * S + o3b], hm);
-                hk = fma(tk[vz * S], QzM[vz * S + o3b], hk);
-                hk2 = fma(tm[vz * S], QzK[vz * S + o3b], hk2);
-            }
-            const int slot = (c0 + jj) & (RING - 1);
-            Hm[slot * S2 + o23] = hm;
-            Hk[slot * S2 + o23] = hk + hk2;
-        }
-        // ---- phase B: row pairs of the tile -> staging ---------------------------------
-        // the single staging buffer was read by the previous tile's bulk copy during phase A
-        if (k >= 1 && tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        __syncthreads();                               // H ready; staging buffer free
-        const long long orow0 = (long long)line * N + t0 - a.row_begin;   // output row of the tile
-        const long long g0 = orow0 * a.ld;                                // first element
+    // prologue: phases A1, A2 of tile 0
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncthreads();
+    if (itB.line <= last_line) phase_a<P>(a, itB, patches, qbufs, Hm, Hk, tid);
+    tile_issue<P>(a, patches, qbufs, itP, last_line, tid);   // tile 2
+    if (itP.line <= last_line) it_next<P>(a, itP);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");   // tile 1 landed
+    __syncthreads();
+    itA = itB;
+    if (itA.line <= last_line) it_next<P>(a, itA);
+
+    for (int k = 0; itB.line <= last_line; ++k) {
+        const bool haveA = itA.line <= last_line;
+        const int t0 = itB.t0;
+        const int tr = min(TR, itB.x1 - t0);
+        const long long orow0 = (long long)itB.line * N + t0 - a.row_begin;   // output row of the tile
+        const long long g0 = orow0 * a.ld;                                    // first element
         const int pad = padded ? 0 : (int)(g0 & 1);
         double* stM = stage + pad;
         double* stK = stage + C::STAGE + pad;
+        // ---- S1: phase B of tile k ---------------------------------------------------------
         if (tid < C::ITEMS && 2 * q < tr && a.dbg != 1) {
             const int j = 2 * q, r = t0 + j;
             const int b0 = max(0, r - P);
@@ -362,7 +405,7 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const __grid_const
             }
         }
         __syncthreads();
-        // ---- store the tile: bulk copies of the 16-byte aligned interior, peeled ends ----
+        // ---- S2: store tile k, phase A of tile k+1, prefetch tile k+3 --------------------
         if (a.dbg == 2) {
         } else if (!padded) {
             const int total = tr * S3;
@@ -395,7 +438,14 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const __grid_const
                 if (MODE & 2) a.K[(orow0 + j) * a.ld + S3 - 1] = stK[j * SRr + S3 - 1];
             }
         }
-        it_next<P>(a, it);
+        if (haveA) phase_a<P>(a, itA, patches, qbufs, Hm, Hk, tid);
+        tile_issue<P>(a, patches, qbufs, itP, last_line, tid);    // tile k+3
+        if (itP.line <= last_line) it_next<P>(a, itP);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");      // tile k+2 landed
+        if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // staging free
+        __syncthreads();
+        itB = itA;
+        if (haveA) it_next<P>(a, itA);
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
