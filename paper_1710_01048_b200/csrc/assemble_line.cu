@@ -49,7 +49,11 @@ struct Cfg {
     static constexpr int SR = S3 + 1;                  // staging row stride for padded ld
     static constexpr int STAGE = TR * SR + 2;          // doubles per staging buffer per matrix
     static constexpr int PATCH = W * V * V;
-    static constexpr int SMEM = 2 * STAGE + RING * 2 * S2 + 3 * 4 * V * S + 3 * PATCH;
+#ifndef WGQ_LINE_PFD
+#define WGQ_LINE_PFD 4
+#endif
+    static constexpr int PFD = WGQ_LINE_PFD;           // prefetch distance (tiles) = patch / Q buffers
+    static constexpr int SMEM = 2 * STAGE + RING * 2 * S2 + PFD * 4 * V * S + PFD * PATCH;
     static_assert(W <= RING, "ring too small");
 };
 
@@ -66,36 +70,83 @@ struct LineArgs {
     // interior (class I) x-row vertex tables P^ in physical units: PMh = h * PM, PKi = PK / h
     // (kernel parameters: constant-bank operands, no global state shared between handles)
     double PMh[kMaxV][kMaxS], PKi[kMaxV][kMaxS];
-    int dbg;   // profiling only (WGQ_LINE_DBG): 1 = skip compute, 2 = skip stores
+    int dbg;   // profiling only (WGQ_LINE_DBG bits): 1 = skip compute, 2 = skip stores, 4 = skip loads
 };
+
+// L2 policies: the assembled matrices stream through L2 once (evict_first), the vertex grid
+// and row tables are re-read by neighbouring lines (evict_last), so the write stream does not
+// evict the small read working set (each DRAM read inside the write stream costs bus
+// turnarounds).
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
 
 __device__ __forceinline__ void bulk_store(double* gdst, const double* ssrc, uint32_t bytes) {
     const uint32_t s = (uint32_t)__cvta_generic_to_shared(ssrc);
+#ifdef WGQ_NO_L2_HINTS
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(s), "r"(bytes)
                  : "memory");
+#else
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gdst), "r"(s),
+                 "r"(bytes), "l"(policy_evict_first())
+                 : "memory");
+#endif
 }
 
 __device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc, bool valid) {
     const uint32_t s = (uint32_t)__cvta_generic_to_shared(sdst);
+#ifdef WGQ_NO_L2_HINTS
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(gsrc), "r"(valid ? 8 : 0) : "memory");
+#else
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2, %3;" ::"r"(s), "l"(gsrc),
+                 "r"(valid ? 8 : 0), "l"(policy_evict_last())
+                 : "memory");
+#endif
 }
 
-// Issue the vertex patch of planes [c0, c0+nnew) of the line (by, bz): patch[j][vz][vy].
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Patch loading: thread tid owns vertex row (vz, vy) = divmod(tid / 8, V) of the patch and
+// x-offsets j = tid % 8 (+ 8); the row's base pointer is refreshed only when the prefetched
+// tile starts a new line, so issuing a tile costs each thread one or two cp.async.
+struct PatchRow {
+    const double* base;   // &g[z][y][0] of the thread's vertex row, or nullptr (outside grid/slab)
+};
+
 template <int P>
-__device__ __forceinline__ void load_patch(const LineArgs& a, double* patch, int c0, int nnew, int by, int bz,
-                                           int tid) {
-    using C = Cfg<P>;
-    constexpr int V = C::V;
+__device__ __forceinline__ void patch_row_init(const LineArgs& a, PatchRow& pr, int i2, int i3, int tid) {
+    constexpr int V = P + 2;
+    const int r = tid >> 3, vy = r % V, vz = r / V;
+    const int y = max(0, i2 - P) + vy, z = max(0, i3 - P) + vz;
     const int nv = a.n + 1;
-    for (int e = tid; e < C::W * V * V; e += C::NT) {      // constant divisors; j >= nnew idle
-        const int j = e % C::W, vy = (e / C::W) % V, vz = e / (C::W * V);
-        if (j >= nnew) continue;
-        const int x = c0 + j, y = by + vy, z = bz + vz;
-        const bool ok = x <= a.n && y <= a.n && z <= a.n && z - a.plane0 < a.planes;
-        const double* src = ok ? a.grid + ((size_t)(z - a.plane0) * nv + y) * nv + x : a.grid;
-        cp_async8(patch + (j * V + vz) * V + vy, src, ok);
+    const bool ok = r < V * V && y <= a.n && z <= a.n && z - a.plane0 < a.planes;
+    pr.base = ok ? a.grid + ((size_t)(z - a.plane0) * nv + y) * nv : nullptr;
+}
+
+// Issue the vertex patch of planes [c0, c0+nnew): patch[j][vz][vy]; out-of-range vertices
+// are zero-filled (cp.async with source size 0).
+template <int P>
+__device__ __forceinline__ void load_patch(const LineArgs& a, const PatchRow& pr, double* patch, int c0, int nnew,
+                                           int tid) {
+    constexpr int V = P + 2;
+    const int r = tid >> 3;
+    if (r >= V * V) return;
+    const int vy = r % V, vz = r / V;
+    for (int j = tid & 7; j < nnew; j += 8) {
+        const int x = c0 + j;
+        const bool ok = pr.base != nullptr && x <= a.n;
+        cp_async8(patch + (j * V + vz) * V + vy, ok ? pr.base + x : a.grid, ok);
     }
-    asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
 // two consecutive interior (class I) rows r, r+1 from the shared window hm/hk[0..V]: row r
@@ -183,8 +234,8 @@ __device__ __forceinline__ void finish_general(int r, const double* hm, const do
 // (paid by every thread of the CTA) is a few adds and compares.
 struct TileIt {
     int line, i2, i3, x0, x1, t0;
-    int qs;      // Q buffer of the line: line ordinal % 3
-    int ps;      // patch buffer of the tile: tile ordinal % 3
+    int qs;      // Q buffer of the line: line ordinal % PFD
+    int ps;      // patch buffer of the tile: tile ordinal % PFD
     int lo, hi;  // vertex planes the tile adds to the line's H ring
 };
 
@@ -216,10 +267,10 @@ __device__ __forceinline__ void it_init(const LineArgs& a, TileIt& t) {
 template <int P>
 __device__ __forceinline__ void it_next(const LineArgs& a, TileIt& t) {
     t.t0 += Cfg<P>::TR;
-    t.ps = t.ps == 2 ? 0 : t.ps + 1;
+    t.ps = t.ps == Cfg<P>::PFD - 1 ? 0 : t.ps + 1;
     if (t.t0 >= t.x1) {
         t.line += gridDim.x;
-        t.qs = t.qs == 2 ? 0 : t.qs + 1;
+        t.qs = t.qs == Cfg<P>::PFD - 1 ? 0 : t.qs + 1;
         it_line<P>(a, t);
     }
     it_planes<P>(t);
@@ -227,15 +278,16 @@ __device__ __forceinline__ void it_next(const LineArgs& a, TileIt& t) {
 
 // Issue (cp.async, one commit group) everything tile t reads from global memory: its new
 // vertex planes into patch buffer t.ps and, for a line's first tile, the line's y/z vertex
-// tables into Q buffer t.qs.  An exhausted iterator commits an empty group.
+// tables into Q buffer t.qs (and the thread's patch row).  An exhausted iterator commits an
+// empty group.
 template <int P>
 __device__ __forceinline__ void tile_issue(const LineArgs& a, double* patches, double* qbufs, const TileIt& t,
-                                           int last_line, int tid) {
+                                           PatchRow& pr, int last_line, int tid) {
     using C = Cfg<P>;
     constexpr int V = C::V, S = C::S;
     if (t.line <= last_line) {
-        load_patch<P>(a, patches + t.ps * C::PATCH, t.lo, t.hi - t.lo + 1, max(0, t.i2 - P), max(0, t.i3 - P), tid);
         if (t.t0 == t.x0) {
+            patch_row_init<P>(a, pr, t.i2, t.i3, tid);
             double* Q = qbufs + t.qs * (4 * V * S);
             for (int e = tid; e < 4 * V * S; e += C::NT) {
                 const int which = e / (V * S), v = (e / S) % V, o = e % S;
@@ -243,8 +295,34 @@ __device__ __forceinline__ void tile_issue(const LineArgs& a, double* patches, d
                 cp_async8(Q + e, ((which & 1) ? a.T.PK : a.T.PM) + ((size_t)r * kMaxV + v) * kMaxS + o, true);
             }
         }
+        load_patch<P>(a, pr, patches + t.ps * C::PATCH, t.lo, t.hi - t.lo + 1, tid);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+// What every warp needs to know about a tile; written by thread 0 when the tile is prefetched.
+struct TileDesc {
+    int line;          // -1: past the CTA's last tile
+    int t0, tr;        // first x-row, rows in the tile
+    int lo, nnew;      // new vertex planes [lo, lo + nnew) for phase A
+    int ps, qs;        // patch / Q buffers
+    int pad;           // staging offset aligning the tile's first element
+    long long orow0;   // output row of the tile's first row
+};
+
+template <int P>
+__device__ __forceinline__ TileDesc make_desc(const LineArgs& a, const TileIt& t, int last_line, bool padded) {
+    TileDesc d;
+    d.line = t.line <= last_line ? t.line : -1;
+    d.t0 = t.t0;
+    d.tr = min(Cfg<P>::TR, t.x1 - t.t0);
+    d.lo = t.lo;
+    d.nnew = t.hi - t.lo + 1;
+    d.ps = t.ps;
+    d.qs = t.qs;
+    d.orow0 = (long long)t.line * a.N + t.t0 - a.row_begin;
+    d.pad = padded ? 0 : (int)((d.orow0 * a.ld) & 1);
+    return d;
 }
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
@@ -262,7 +340,7 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // (TT[g][t], TT[g][t+4]): no shuffle or shared-memory round trip between the two products.
 // Padding rows / columns (o2, o3 >= S, vy, vz >= V) carry zero coefficients.
 template <int P>
-__device__ __forceinline__ void phase_a(const LineArgs& a, const TileIt& t, const double* patches,
+__device__ __forceinline__ void phase_a(const LineArgs& a, const TileDesc& t, const double* patches,
                                         const double* qbufs, double* Hm, double* Hk, int tid) {
     using C = Cfg<P>;
     constexpr int V = C::V, S = C::S, S2 = C::S2, RING = C::RING;
@@ -282,9 +360,9 @@ __device__ __forceinline__ void phase_a(const LineArgs& a, const TileIt& t, cons
         bZK[s] = ok ? Q[3 * V * S + e] : 0.0;
     }
     const double* patch = patches + t.ps * C::PATCH;
-    const int nnew = t.hi - t.lo + 1;
+    const int nnew = t.nnew;
     const int vzp = (g >> 1) + 4 * (g & 1);            // B column g of A1 <-> vz = pi(g)
-    for (int j = NW - 1 - warp; j < (a.dbg == 1 ? 0 : nnew); j += NW) {
+    for (int j = NW - 1 - warp; j < ((a.dbg & 1) ? 0 : nnew); j += NW) {
         double tM0 = 0.0, tM1 = 0.0, tK0 = 0.0, tK1 = 0.0;
 #pragma unroll
         for (int s = 0; s < KS; ++s) {
@@ -320,61 +398,94 @@ __device__ __forceinline__ void phase_a(const LineArgs& a, const TileIt& t, cons
     }
 }
 
+// Bulk store of one matrix of the staged tile (tr rows from output row orow0), without the
+// commit: the 16-byte aligned interior in one cp.async.bulk (tid 0) plus peeled odd end
+// elements; padded even ld: one bulk copy per row plus its odd last element.
+template <int P>
+__device__ __forceinline__ void store_mat(const LineArgs& a, double* out, const double* st, long long orow0, int tr,
+                                          int SRr, bool padded, int tid) {
+    constexpr int S3 = Cfg<P>::S3;
+    const long long g0 = orow0 * a.ld;
+    if (!padded) {
+        const int total = tr * S3;
+        const int head = (int)(g0 & 1);
+        const int tail = (int)((g0 + total) & 1);
+        if (tid == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            bulk_store(out + g0 + head, st + head, (uint32_t)(total - head - tail) * 8u);
+        } else if (tid == 32 && head) {
+            out[g0] = st[0];
+        } else if (tid == 64 && tail) {
+            out[g0 + total - 1] = st[total - 1];
+        }
+    } else {
+        if (tid == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            for (int j = 0; j < tr; ++j) bulk_store(out + (orow0 + j) * a.ld, st + j * SRr, (uint32_t)(S3 - 1) * 8u);
+        }
+        if (tid >= 32 && tid < 32 + tr) {
+            const int j = tid - 32;
+            out[(orow0 + j) * a.ld + S3 - 1] = st[j * SRr + S3 - 1];
+        }
+    }
+}
+
 template <int P, int MODE>
 __global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const __grid_constant__ LineArgs a) {
     using C = Cfg<P>;
-    constexpr int S = C::S, S2 = C::S2, S3 = C::S3, V = C::V, TR = C::TR, RING = C::RING;
+    constexpr int S = C::S, S2 = C::S2, S3 = C::S3, V = C::V, RING = C::RING;
     extern __shared__ __align__(128) double sm[];
     double* stage = sm;                                   // [2 mat][STAGE] (single buffer)
     double* Hm = stage + 2 * C::STAGE;                    // [RING][S2]
     double* Hk = Hm + RING * S2;                          // [RING][S2]
-    double* qbufs = Hk + RING * S2;                       // [3][QyM, QyK, QzM, QzK: [V][S] each]
-    double* patches = qbufs + 3 * 4 * V * S;              // [3][W][V(z)][V(y)]
+    double* qbufs = Hk + RING * S2;                       // [PFD][QyM, QyK, QzM, QzK: [V][S] each]
+    double* patches = qbufs + C::PFD * 4 * V * S;         // [PFD][W][V(z)][V(y)]
 
+    __shared__ TileDesc desc[8];                          // tiles k .. k+PFD (ring)
+    constexpr int PFD = C::PFD;
     const int tid = threadIdx.x;
-    const int n = a.n, N = a.N;
+    const int n = a.n;
     const bool padded = a.ld != S3;
     const int SRr = padded ? C::SR : S3;
-    const int first_line = a.row_begin / N, last_line = (a.row_end - 1) / N;
+    const int last_line = (a.row_end - 1) / a.N;
     // fixed per-thread role in phase B: item (row pair q, o23)
     const int q = tid / S2, o23 = tid % S2;
 
-    (void)first_line;
     // Software pipeline, two barriers per tile:
     //   S1(k): phase B of tile k (H -> staging)
-    //   S2(k): bulk store of tile k  +  phase A of tile k+1 (patch -> H ring)  +  prefetch k+3
+    //   S2(k): bulk store of tile k  +  phase A of tile k+1 (patch -> H ring)  +  prefetch k+PFD
     // The H ring holds a tile's window (W planes) and the next tile's new planes are written
-    // only after that tile's phase B (S2 follows S1), so RING >= W suffices.
-    TileIt itB, itA, itP;                               // tile k, tile k+1, prefetch tile k+3
-    it_init<P>(a, itB);
-    itP = itB;
-    for (int k = 0; k < 2; ++k) {
-        tile_issue<P>(a, patches, qbufs, itP, last_line, tid);
+    // only after that tile's phase B (S2 follows S1), so RING >= W suffices.  Global loads are
+    // issued PFD tiles ahead: under saturated HBM writes their latency is several microseconds.
+    // One tile iterator (the prefetch one) runs in every thread; thread 0 publishes each
+    // prefetched tile's descriptor for phases A and B.
+    TileIt itP;
+    PatchRow prow;
+    prow.base = nullptr;
+    it_init<P>(a, itP);
+    for (int k = 0; k < PFD; ++k) {
+        tile_issue<P>(a, patches, qbufs, itP, prow, last_line, tid);
+        if (tid == 0) desc[k] = make_desc<P>(a, itP, last_line, padded);
         if (itP.line <= last_line) it_next<P>(a, itP);
     }
-    // prologue: phases A1, A2 of tile 0
-    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    cp_async_wait<PFD - 1>();                             // tile 0 landed
     __syncthreads();
-    if (itB.line <= last_line) phase_a<P>(a, itB, patches, qbufs, Hm, Hk, tid);
-    tile_issue<P>(a, patches, qbufs, itP, last_line, tid);   // tile 2
-    if (itP.line <= last_line) it_next<P>(a, itP);
-    asm volatile("cp.async.wait_group 1;" ::: "memory");   // tile 1 landed
+    {
+        const TileDesc d0 = desc[0];
+        if (d0.line >= 0) phase_a<P>(a, d0, patches, qbufs, Hm, Hk, tid);
+    }
+    cp_async_wait<PFD - 2>();                             // tile 1 landed
     __syncthreads();
-    itA = itB;
-    if (itA.line <= last_line) it_next<P>(a, itA);
 
-    for (int k = 0; itB.line <= last_line; ++k) {
-        const bool haveA = itA.line <= last_line;
-        const int t0 = itB.t0;
-        const int tr = min(TR, itB.x1 - t0);
-        const long long orow0 = (long long)itB.line * N + t0 - a.row_begin;   // output row of the tile
-        const long long g0 = orow0 * a.ld;                                    // first element
-        const int pad = padded ? 0 : (int)(g0 & 1);
-        double* stM = stage + pad;
-        double* stK = stage + C::STAGE + pad;
+    for (int k = 0;; ++k) {
+        const TileDesc d = desc[k & 7];
+        if (d.line < 0) break;
+        const TileDesc dA = desc[(k + 1) & 7];
+        double* stM = stage + d.pad;
+        double* stK = stage + C::STAGE + d.pad;
         // ---- S1: phase B of tile k ---------------------------------------------------------
-        if (tid < C::ITEMS && 2 * q < tr && a.dbg != 1) {
-            const int j = 2 * q, r = t0 + j;
+        if (tid < C::ITEMS && 2 * q < d.tr && !(a.dbg & 1)) {
+            const int j = 2 * q, r = d.t0 + j;
             const int b0 = max(0, r - P);
             double hm[V + 1], hk[V + 1];
 #pragma unroll
@@ -383,7 +494,7 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const __grid_const
                 hm[v] = Hm[slot * S2 + o23];
                 hk[v] = Hk[slot * S2 + o23];
             }
-            const bool second = j + 1 < tr;
+            const bool second = j + 1 < d.tr;
             const bool shift = r + 1 - P > 0;          // row r+1's window starts one plane later
             double* dM = stM + j * SRr + S * o23;
             double* dK = stK + j * SRr + S * o23;
@@ -406,46 +517,19 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const __grid_const
         }
         __syncthreads();
         // ---- S2: store tile k, phase A of tile k+1, prefetch tile k+3 --------------------
-        if (a.dbg == 2) {
-        } else if (!padded) {
-            const int total = tr * S3;
-            const int head = (int)(g0 & 1);
-            const int tail = (int)((g0 + total) & 1);
-            if (tid == 0) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                if (MODE & 1) bulk_store(a.M + g0 + head, stM + head, (uint32_t)(total - head - tail) * 8u);
-                if (MODE & 2) bulk_store(a.K + g0 + head, stK + head, (uint32_t)(total - head - tail) * 8u);
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            } else if (tid == 32 && head) {
-                if (MODE & 1) a.M[g0] = stM[0];
-                if (MODE & 2) a.K[g0] = stK[0];
-            } else if (tid == 64 && tail) {
-                if (MODE & 1) a.M[g0 + total - 1] = stM[total - 1];
-                if (MODE & 2) a.K[g0 + total - 1] = stK[total - 1];
-            }
-        } else {                                       // even ld: rows start 16B-aligned
-            if (tid == 0) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                for (int j = 0; j < tr; ++j) {
-                    if (MODE & 1) bulk_store(a.M + (orow0 + j) * a.ld, stM + j * SRr, (uint32_t)(S3 - 1) * 8u);
-                    if (MODE & 2) bulk_store(a.K + (orow0 + j) * a.ld, stK + j * SRr, (uint32_t)(S3 - 1) * 8u);
-                }
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            }
-            if (tid >= 32 && tid < 32 + tr) {
-                const int j = tid - 32;
-                if (MODE & 1) a.M[(orow0 + j) * a.ld + S3 - 1] = stM[j * SRr + S3 - 1];
-                if (MODE & 2) a.K[(orow0 + j) * a.ld + S3 - 1] = stK[j * SRr + S3 - 1];
-            }
+        if (!(a.dbg & 2)) {
+            if (MODE & 1) store_mat<P>(a, a.M, stM, d.orow0, d.tr, SRr, padded, tid);
+            if (MODE & 2) store_mat<P>(a, a.K, stK, d.orow0, d.tr, SRr, padded, tid);
+            if (tid == 0) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
-        if (haveA) phase_a<P>(a, itA, patches, qbufs, Hm, Hk, tid);
-        tile_issue<P>(a, patches, qbufs, itP, last_line, tid);    // tile k+3
+        if (dA.line >= 0) phase_a<P>(a, dA, patches, qbufs, Hm, Hk, tid);
+        if (a.dbg & 4) asm volatile("cp.async.commit_group;" ::: "memory");
+        else tile_issue<P>(a, patches, qbufs, itP, prow, last_line, tid);    // tile k+PFD
+        if (tid == 0) desc[(k + PFD) & 7] = make_desc<P>(a, itP, last_line, padded);
         if (itP.line <= last_line) it_next<P>(a, itP);
-        asm volatile("cp.async.wait_group 1;" ::: "memory");      // tile k+2 landed
+        cp_async_wait<PFD - 2>();                                  // tile k+2 landed
         if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // staging free
         __syncthreads();
-        itB = itA;
-        if (haveA) it_next<P>(a, itA);
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");

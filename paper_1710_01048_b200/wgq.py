@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libwgq.so")
+LIB_PATH = os.environ.get("WGQ_LIB") or os.path.join(_HERE, "libwgq.so")   # WGQ_LIB: kernel experiments
 
 WGQ_OK, WGQ_EINVAL, WGQ_EUNSUPPORTED, WGQ_ENOCONV, WGQ_ECUDA, WGQ_ERANGE, WGQ_ENOMEM = 0, -1, -2, -3, -4, -5, -6
 WGQ_BND_GAUSS, WGQ_BND_GL = 0, 1
