@@ -50,10 +50,11 @@ struct Cfg {
     static constexpr int STAGE = TR * SR + 2;          // doubles per staging buffer per matrix
     static constexpr int PATCH = W * V * V;
 #ifndef WGQ_LINE_PFD
-#define WGQ_LINE_PFD 4
+#define WGQ_LINE_PFD 3
 #endif
     static constexpr int PFD = WGQ_LINE_PFD;           // prefetch distance (tiles) = patch / Q buffers
-    static constexpr int SMEM = 2 * STAGE + RING * 2 * S2 + PFD * 4 * V * S + PFD * PATCH;
+    static constexpr int XB = 4 * P * 2 * V * S;       // x-boundary rows' vertex tables
+    static constexpr int SMEM = 2 * STAGE + RING * 2 * S2 + PFD * 4 * V * S + PFD * PATCH + XB;
     static_assert(W <= RING, "ring too small");
 };
 
@@ -207,21 +208,21 @@ __device__ __forceinline__ void finish_interior(const double* hm, const double* 
     }
 }
 
-// a boundary-affected row: its own vertex tables from global memory
+// a boundary-affected x-row: its own vertex tables (PM then PK, [v][o]), staged in shared
+// memory once per CTA (the 4p such rows are the same for every line)
 template <int P, int MODE>
-__device__ __forceinline__ void finish_general(int r, const double* hm, const double* hk, double* dM, double* dK,
-                                               const LineArgs& a) {
+__device__ __forceinline__ void finish_general(const double* pm, const double* hm, const double* hk, double* dM,
+                                               double* dK) {
     constexpr int S = 2 * P + 1, V = P + 2;
-    const double* pm = a.T.PM + (size_t)r * kMaxV * kMaxS;
-    const double* pk = a.T.PK + (size_t)r * kMaxV * kMaxS;
+    const double* pk = pm + V * S;
 #pragma unroll
     for (int o1 = 0; o1 < S; ++o1) {
         double s = 0.0, s1 = 0.0;
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-            const double m = __ldg(pm + v * kMaxS + o1);
+            const double m = pm[v * S + o1];
             s = fma(m, hm[v], s);
-            s1 = fma(__ldg(pk + v * kMaxS + o1), hm[v], s1);
+            s1 = fma(pk[v * S + o1], hm[v], s1);
             s1 = fma(m, hk[v], s1);
         }
         if (MODE & 1) dM[o1] = s + 0.0;
@@ -398,33 +399,33 @@ __device__ __forceinline__ void phase_a(const LineArgs& a, const TileDesc& t, co
     }
 }
 
-// Bulk store of one matrix of the staged tile (tr rows from output row orow0), without the
-// commit: the 16-byte aligned interior in one cp.async.bulk (tid 0) plus peeled odd end
-// elements; padded even ld: one bulk copy per row plus its odd last element.
+// Bulk store of one matrix of the staged tile (tr rows from output row orow0), by warp 0,
+// without the commit: lane 0 issues the 16-byte aligned interior as one cp.async.bulk, lanes
+// 1 / 2 the peeled odd end elements; padded even ld: one bulk copy per row (lane 0) and the
+// rows' odd last elements (lanes 1..tr).
 template <int P>
 __device__ __forceinline__ void store_mat(const LineArgs& a, double* out, const double* st, long long orow0, int tr,
-                                          int SRr, bool padded, int tid) {
+                                          int SRr, bool padded, int lane) {
     constexpr int S3 = Cfg<P>::S3;
     const long long g0 = orow0 * a.ld;
     if (!padded) {
         const int total = tr * S3;
         const int head = (int)(g0 & 1);
         const int tail = (int)((g0 + total) & 1);
-        if (tid == 0) {
+        if (lane == 0) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             bulk_store(out + g0 + head, st + head, (uint32_t)(total - head - tail) * 8u);
-        } else if (tid == 32 && head) {
+        } else if (lane == 1 && head) {
             out[g0] = st[0];
-        } else if (tid == 64 && tail) {
+        } else if (lane == 2 && tail) {
             out[g0 + total - 1] = st[total - 1];
         }
     } else {
-        if (tid == 0) {
+        if (lane == 0) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             for (int j = 0; j < tr; ++j) bulk_store(out + (orow0 + j) * a.ld, st + j * SRr, (uint32_t)(S3 - 1) * 8u);
-        }
-        if (tid >= 32 && tid < 32 + tr) {
-            const int j = tid - 32;
+        } else if (lane <= tr) {
+            const int j = lane - 1;
             out[(orow0 + j) * a.ld + S3 - 1] = st[j * SRr + S3 - 1];
         }
     }
@@ -440,6 +441,7 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const __grid_const
     double* Hk = Hm + RING * S2;                          // [RING][S2]
     double* qbufs = Hk + RING * S2;                       // [PFD][QyM, QyK, QzM, QzK: [V][S] each]
     double* patches = qbufs + C::PFD * 4 * V * S;         // [PFD][W][V(z)][V(y)]
+    double* xbt = patches + C::PFD * C::PATCH;            // [4P rows][PM, PK][V][S]
 
     __shared__ TileDesc desc[8];                          // tiles k .. k+PFD (ring)
     constexpr int PFD = C::PFD;
@@ -459,6 +461,15 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const __grid_const
     // issued PFD tiles ahead: under saturated HBM writes their latency is several microseconds.
     // One tile iterator (the prefetch one) runs in every thread; thread 0 publishes each
     // prefetched tile's descriptor for phases A and B.
+    // x-boundary rows r < 2P and r >= n-P: their vertex tables, once per CTA
+    for (int e = tid; e < C::XB; e += C::NT) {
+        const int i = e / (2 * V * S), rem = e % (2 * V * S), kind = rem / (V * S), v = (rem / S) % V, o = rem % S;
+        const int r = i < 2 * P ? i : n - P + (i - 2 * P);
+        xbt[e] = (kind ? a.T.PK : a.T.PM)[((size_t)r * kMaxV + v) * kMaxS + o];
+    }
+    auto xb_row = [&](int r) -> const double* {
+        return xbt + (r < 2 * P ? r : 2 * P + (r - (n - P))) * (2 * V * S);
+    };
     TileIt itP;
     PatchRow prow;
     prow.base = nullptr;
@@ -502,7 +513,7 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const __grid_const
                 finish_pair_interior<P, MODE>(hm, hk, dM, dK, SRr, second, a);
             } else {
                 if (r >= 2 * P && r <= n - 1 - P) finish_interior<P, MODE>(hm, hk, dM, dK, a);
-                else finish_general<P, MODE>(r, hm, hk, dM, dK, a);
+                else finish_general<P, MODE>(xb_row(r), hm, hk, dM, dK);
                 if (second) {
                     double hm1[V], hk1[V];
 #pragma unroll
@@ -511,13 +522,13 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const __grid_const
                         hk1[v] = shift ? hk[v + 1] : hk[v];
                     }
                     if (r + 1 >= 2 * P && r + 1 <= n - 1 - P) finish_interior<P, MODE>(hm1, hk1, dM + SRr, dK + SRr, a);
-                    else finish_general<P, MODE>(r + 1, hm1, hk1, dM + SRr, dK + SRr, a);
+                    else finish_general<P, MODE>(xb_row(r + 1), hm1, hk1, dM + SRr, dK + SRr);
                 }
             }
         }
         __syncthreads();
         // ---- S2: store tile k, phase A of tile k+1, prefetch tile k+3 --------------------
-        if (!(a.dbg & 2)) {
+        if (tid < 32 && !(a.dbg & 2)) {
             if (MODE & 1) store_mat<P>(a, a.M, stM, d.orow0, d.tr, SRr, padded, tid);
             if (MODE & 2) store_mat<P>(a, a.K, stK, d.orow0, d.tr, SRr, padded, tid);
             if (tid == 0) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
