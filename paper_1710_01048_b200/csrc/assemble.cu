@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "coef.cuh"
 #include "internal.h"
@@ -25,6 +26,12 @@ namespace {
 constexpr int kMaxWarps = 8;
 
 __device__ __constant__ double kOnes[kMaxStiffNodes * kMaxS] = {1.0};
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
 
 // per-warp staging sizes (doubles) for the node counts of the rules at hand
 struct Staging {
@@ -41,6 +48,10 @@ struct OutDev {
 struct GenericArgs {
     RowTables T;
     CoefDev coef;
+    const double* ctab;    // per-direction coefficient factor tables (TRIG_SEP, FOURIER_LOGN) or null
+    int cw;                // doubles per node in ctab
+    const int64_t* rows_list;   // if set: assemble only these rows (global ids inside the range)
+    int64_t nlist;
     int64_t n, N;
     int64_t row_begin, row_end;
     OutDev M, K;
@@ -54,7 +65,70 @@ struct Dir {
     const double* x;   // [m]
     const double* w;   // [m]
     const double* A;   // [m][kMaxS]
+    const double* ct;  // [m][cw] coefficient factors at the nodes (ctab), or null
 };
+
+// Coefficient factor tables (a3 without per-sample transcendentals): for direction a, node
+// kind (mass / stiffness), 1D row r and node k,
+//   TRIG_SEP:     F = trig_a(2 pi k_a x)                                  (cw = 1)
+//   FOURIER_LOGN: (C, S)_m = (cos, sin)(2 pi k_{m,a} x + [a = 0] theta_m) * ([a = 0] ? a_m : 1)
+// so that c = c0 + amp prod_a F_a, resp. c = exp(sum_m Re prod_a (C + i S)_m): the angle-sum
+// expansion of cos(2 pi k_m . x + theta_m) (R13), exact up to rounding.
+__global__ void k_coef_tables(const CoefDev c, int dim, RowTables T, double* tab, int cw) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t per_ak = T.N * kMaxNodes;
+    const int64_t ak = tid / per_ak;
+    if (ak >= 2 * dim) return;
+    const int a = (int)(ak / 2), kind = (int)(ak % 2);
+    const int64_t r = (tid % per_ak) / kMaxNodes;
+    const int k = (int)(tid % kMaxNodes);
+    const int m = kind == WGQ_MASS ? T.mM[r] : T.mK[r];
+    if (k >= m) return;
+    const double x = (kind == WGQ_MASS ? T.xM : T.xK)[r * kMaxNodes + k];
+    double* out = tab + tid * cw;
+    if (c.kind == WGQ_COEF_TRIG_SEP) {
+        const double arg = 2.0 * (double)c.wavenum[a] * x;   // trig(pi * arg)
+        out[0] = c.trig[a] == WGQ_TRIG_SIN ? sinpi(arg) : cospi(arg);
+    } else {
+        for (int q = 0; q < c.n_modes; ++q) {
+            const double arg = 2.0 * c.modes[q][1 + a] * x;
+            double cp = cospi(arg), sp = sinpi(arg);
+            if (a == 0) {
+                double ct, st;
+                sincos(c.modes[q][4], &st, &ct);
+                const double cc = cp * ct - sp * st, ss = sp * ct + cp * st;
+                cp = c.modes[q][0] * cc;
+                sp = c.modes[q][0] * ss;
+            }
+            out[2 * q] = cp;
+            out[2 * q + 1] = sp;
+        }
+    }
+}
+
+template <int D>
+__device__ __forceinline__ double coef_from_tables(const CoefDev& c, const double* f1, const double* f2,
+                                                   const double* f3) {
+    if (c.kind == WGQ_COEF_TRIG_SEP) {
+        double prod = f1[0];
+        if (D > 1) prod *= f2[0];
+        if (D > 2) prod *= f3[0];
+        return c.c0 + c.amp * prod;
+    }
+    double s = 0.0;
+    for (int q = 0; q < c.n_modes; ++q) {
+        const double C1 = f1[2 * q], S1 = f1[2 * q + 1];
+        if (D == 1) {
+            s += C1;
+        } else if (D == 2) {
+            s += C1 * f2[2 * q] - S1 * f2[2 * q + 1];
+        } else {
+            const double C2 = f2[2 * q], S2 = f2[2 * q + 1], C3 = f3[2 * q], S3 = f3[2 * q + 1];
+            s += C1 * (C2 * C3 - S2 * S3) - S1 * (S2 * C3 + C2 * S3);
+        }
+    }
+    return exp(s);
+}
 
 template <int D>
 __device__ __forceinline__ void stage_term(const GenericArgs& a, const Dir d1, const Dir d2, const Dir d3,
@@ -64,8 +138,14 @@ __device__ __forceinline__ void stage_term(const GenericArgs& a, const Dir d1, c
     // a3-a4: weighted coefficient samples on the node tensor
     for (int e = lane; e < n1 * n2 * n3; e += 32) {
         const int k3 = e % n3, k2 = (e / n3) % n2, k1 = e / (n3 * n2);
-        double x[3] = {d1.x[k1], d2.x[k2], d3.x[k3]};
-        W[e] = coef_eval<D>(a.coef, a.n, x) * d1.w[k1] * d2.w[k2] * d3.w[k3];
+        double cv;
+        if (a.ctab) {
+            cv = coef_from_tables<D>(a.coef, d1.ct + k1 * a.cw, d2.ct + k2 * a.cw, d3.ct + k3 * a.cw);
+        } else {
+            double x[3] = {d1.x[k1], d2.x[k2], d3.x[k3]};
+            cv = coef_eval<D>(a.coef, a.n, x);
+        }
+        W[e] = cv * d1.w[k1] * d2.w[k2] * d3.w[k3];
     }
     __syncwarp();
     // z-stage
@@ -115,10 +195,11 @@ __global__ void __launch_bounds__(kMaxWarps * 32) k_assemble_generic(const Gener
     double* T2 = T1 + a.sg.t1;
     double* T2b = T2 + a.sg.t2;
     const RowTables& T = a.T;
-    const Dir ones = {1, kOnes, kOnes, kOnes};
+    const Dir ones = {1, kOnes, kOnes, kOnes, kOnes};
 
-    for (int64_t row = a.row_begin + (int64_t)blockIdx.x * warps + warp; row < a.row_end;
-         row += (int64_t)gridDim.x * warps) {
+    const int64_t nwork = a.rows_list ? a.nlist : a.row_end - a.row_begin;
+    for (int64_t w = (int64_t)blockIdx.x * warps + warp; w < nwork; w += (int64_t)gridDim.x * warps) {
+        const int64_t row = a.rows_list ? a.rows_list[w] : a.row_begin + w;
         int64_t idx[3] = {0, 0, 0};
         int64_t rem = row;
 #pragma unroll
@@ -131,8 +212,10 @@ __global__ void __launch_bounds__(kMaxWarps * 32) k_assemble_generic(const Gener
         for (int q = 0; q < 3; ++q) {
             if (q < D) {
                 const int64_t r = idx[q];
-                dm[q] = {T.mM[r], T.xM + r * kMaxMassNodes, T.wM + r * kMaxMassNodes, T.VM + r * kMaxMassNodes * kMaxS};
-                dk[q] = {T.mK[r], T.xK + r * kMaxStiffNodes, T.wK + r * kMaxStiffNodes, T.DK + r * kMaxStiffNodes * kMaxS};
+                const double* cm = a.ctab ? a.ctab + ((int64_t)(2 * q + WGQ_MASS) * a.N + r) * kMaxNodes * a.cw : nullptr;
+                const double* ck = a.ctab ? a.ctab + ((int64_t)(2 * q + WGQ_STIFFNESS) * a.N + r) * kMaxNodes * a.cw : nullptr;
+                dm[q] = {T.mM[r], T.xM + r * kMaxMassNodes, T.wM + r * kMaxMassNodes, T.VM + r * kMaxMassNodes * kMaxS, cm};
+                dk[q] = {T.mK[r], T.xK + r * kMaxStiffNodes, T.wK + r * kMaxStiffNodes, T.DK + r * kMaxStiffNodes * kMaxS, ck};
             } else {
                 dm[q] = ones;
                 dk[q] = ones;
@@ -188,6 +271,112 @@ __global__ void __launch_bounds__(kMaxWarps * 32) k_assemble_generic(const Gener
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// 2D FOURIER_LOGN fast path on the FP64 tensor cores (C3): one warp per row, ten DMMA m8n8k4.
+//
+// Row (i1, i2) samples c at its three node tensors (mass x mass for M; stiffness-x x mass-y and
+// mass-x x stiffness-y for the two K terms).  With the factor tables (C, S)_m at the nodes
+// (k_coef_tables), the exponent of every sample is a dot product over 2 n_modes:
+//   E[x-node][y-node] = sum_m (C^x_m C^y_m - S^x_m S^y_m)          (the angle-sum expansion)
+// computed for all 8 x-nodes (4 mass, 4 stiffness, interleaved: row 2k = mass node k, row
+// 2k+1 = stiffness node k) against all 8 y-nodes (same interleave) in one 8 x 8 x 2n_modes
+// DMMA chain.  Lane (g, t) then holds E for x-node g and y-nodes (mass t, stiffness t): with
+// its weights it forms W_M (g even, mass y), W_Ky (g even, stiffness y) and W_Kx (g odd,
+// mass y) — exactly the B fragment B[k = y-node t][n = x-node g] of the y-stage products
+//   T^T_X = A2_X^T W_X^T      (A2 = B_{i2+o}(y) or B'_{i2+o}(y) at the y nodes)
+// whose C fragment (lane (g, t): T^T[o2 = g][x-node column 2t (+1)]) is in turn exactly the B
+// fragment of the x-stage products  M = A1^T T,  K = D1^T T_Kx + A1^T T_Ky  (a5, a6).
+// Rows with more than 4 nodes in a direction (GL-fallback boundary classes, R1) are left to
+// the generic kernel (shell pass).
+template <int P, int MODE>
+__global__ void __launch_bounds__(256) k_fourier2d(const GenericArgs a) {
+    constexpr int S = 2 * P + 1;
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const int warps = blockDim.x >> 5, warp = threadIdx.x >> 5;
+    const RowTables& T = a.T;
+    const int cw = a.cw, J = 2 * a.coef.n_modes;
+    const int64_t N = a.N;
+    const bool gs = g & 1;                     // x-node of row g / y-node of column g: stiffness?
+    const int kg = g >> 1;
+    for (int64_t row = a.row_begin + (int64_t)blockIdx.x * warps + warp; row < a.row_end;
+         row += (int64_t)gridDim.x * warps) {
+        const int64_t i1 = row % N, i2 = row / N;
+        const int nxm = __ldg(T.mM + i1), nxk = __ldg(T.mK + i1), nym = __ldg(T.mM + i2), nyk = __ldg(T.mK + i2);
+        if (nxm > 4 || nxk > 4 || nym > 4 || nyk > 4) continue;     // generic shell pass
+        // ---- exponent GEMM: E[x-node g][y-node n] --------------------------------------------
+        const bool xv = kg < (gs ? nxk : nxm), yv = kg < (gs ? nyk : nym);
+        const double* X = a.ctab + ((int64_t)(0 + (gs ? 1 : 0)) * N + i1) * kMaxNodes * cw + kg * cw;
+        const double* Y = a.ctab + ((int64_t)(2 + (gs ? 1 : 0)) * N + i2) * kMaxNodes * cw + kg * cw;
+        double e0 = 0.0, e1 = 0.0;
+        for (int s = 0; s < J; s += 4) {
+            const int j = s + t;
+            const bool ok = j < J;
+            const double xa = (xv && ok) ? __ldg(X + j) : 0.0;
+            double yb = (yv && ok) ? __ldg(Y + j) : 0.0;
+            if (j & 1) yb = -yb;
+            dmma(e0, e1, xa, yb);
+        }
+        // ---- weighted samples (lane (g, t): x-node g, y-nodes mass t / stiffness t) --------
+        const double wx = xv ? __ldg((gs ? T.wK : T.wM) + i1 * kMaxNodes + kg) : 0.0;
+        const double wym = t < nym ? __ldg(T.wM + i2 * kMaxNodes + t) : 0.0;
+        const double wyk = t < nyk ? __ldg(T.wK + i2 * kMaxNodes + t) : 0.0;
+        const double s0 = (xv && t < nym) ? exp(e0) * wx * wym : 0.0;
+        const double s1 = (!gs && xv && t < nyk) ? exp(e1) * wx * wyk : 0.0;
+        // ---- y-stage: A fragments A2^T[o2 = g][k2 = t] ----------------------------------------
+        const double aVy = (g < S && t < nym) ? __ldg(T.VM + (i2 * kMaxNodes + t) * kMaxS + g) : 0.0;
+        const double aDy = (g < S && t < nyk) ? __ldg(T.DK + (i2 * kMaxNodes + t) * kMaxS + g) : 0.0;
+        const double aVx = (g < S && t < nxm) ? __ldg(T.VM + (i1 * kMaxNodes + t) * kMaxS + g) : 0.0;
+        const double aDx = (g < S && t < nxk) ? __ldg(T.DK + (i1 * kMaxNodes + t) * kMaxS + g) : 0.0;
+        double m0 = 0.0, m1 = 0.0, k0 = 0.0, k1 = 0.0;
+        if (MODE & 1) {
+            double tm0 = 0.0, tm1 = 0.0;
+            dmma(tm0, tm1, aVy, gs ? 0.0 : s0);          // T_M^T: lane holds [o2 = g][x mass t] in tm0
+            dmma(m0, m1, aVx, tm0);                       // M = A1^T T_M
+        }
+        if (MODE & 2) {
+            double tx0 = 0.0, tx1 = 0.0, ty0 = 0.0, ty1 = 0.0;
+            dmma(tx0, tx1, aVy, gs ? s0 : 0.0);          // T_Kx^T: [o2 = g][x stiffness t] in tx1
+            dmma(ty0, ty1, aDy, gs ? 0.0 : s1);          // T_Ky^T: [o2 = g][x mass t] in ty0
+            dmma(k0, k1, aDx, tx1);                       // K = D1^T T_Kx + A1^T T_Ky
+            dmma(k0, k1, aVx, ty0);
+        }
+        // ---- store: lane holds (o1 = g, o2 = 2t + i) -------------------------------------------
+        const int64_t orow = row - a.row_begin;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const int o2 = 2 * t + i;
+            if (g >= S || o2 >= S) continue;
+            const double vm = (i ? m1 : m0) + 0.0, vk = (i ? k1 : k0) + 0.0;
+            if (a.M.layout == WGQ_ELL) {
+                if (MODE & 1) a.M.values[orow * a.M.ld + g + S * o2] = vm;
+                if (MODE & 2) a.K.values[orow * a.K.ld + g + S * o2] = vk;
+            } else {
+                const int lo1 = i1 - P < 0 ? (int)-i1 : -P, hi1 = i1 + P > N - 1 ? (int)(N - 1 - i1) : P;
+                const int lo2 = i2 - P < 0 ? (int)-i2 : -P, hi2 = i2 + P > N - 1 ? (int)(N - 1 - i2) : P;
+                if (g - P < lo1 || g - P > hi1 || o2 - P < lo2 || o2 - P > hi2) continue;
+                const int64_t pos = (g - P - lo1) + (int64_t)(o2 - P - lo2) * (hi1 - lo1 + 1);
+                if (MODE & 1) a.M.values[a.M.row_ptr[orow] + pos] = vm;
+                if (MODE & 2) a.K.values[a.K.row_ptr[orow] + pos] = vk;
+            }
+        }
+    }
+}
+
+template <int P>
+int launch_fourier2d_p(const GenericArgs& a, cudaStream_t st) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t rows = a.row_end - a.row_begin;
+    int64_t blocks = std::min<int64_t>((rows + 7) / 8, (int64_t)sms * 32);
+    blocks = std::max<int64_t>(blocks, 1);
+    const int mode = (a.do_mass ? 1 : 0) | (a.do_stiff ? 2 : 0);
+    if (mode == 3) k_fourier2d<P, 3><<<(unsigned)blocks, 256, 0, st>>>(a);
+    else if (mode == 1) k_fourier2d<P, 1><<<(unsigned)blocks, 256, 0, st>>>(a);
+    else k_fourier2d<P, 2><<<(unsigned)blocks, 256, 0, st>>>(a);
+    return cudaGetLastError() == cudaSuccess ? WGQ_OK : WGQ_ECUDA;
+}
+
 template <int P, int D>
 int launch_generic_pd(GenericArgs a, int maxM, int maxK, cudaStream_t st) {
     constexpr int S = 2 * P + 1;
@@ -214,7 +403,8 @@ int launch_generic_pd(GenericArgs a, int maxM, int maxK, cudaStream_t st) {
     if (cudaFuncSetAttribute(k_assemble_generic<P, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
         return WGQ_ECUDA;
-    const int64_t rows = a.row_end - a.row_begin;
+    const int64_t rows = a.rows_list ? a.nlist : a.row_end - a.row_begin;
+    if (rows <= 0) return WGQ_OK;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -254,6 +444,7 @@ int launch_assemble(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t*
         return e && e[0] == '1';
     }();
     if (!force_generic && line_kernel_applies(R, c, M, K)) return launch_line(R, T, c, M, K, stream);
+    if (!force_generic && sep_applies(c)) return launch_sep(R, T, c, M, K, stream);
     GenericArgs a{};
     a.T = T;
     a.coef = make_coef(c);
@@ -269,16 +460,66 @@ int launch_assemble(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t*
     if (!M) a.M.layout = K->layout;
     if (a.row_end <= a.row_begin) return WGQ_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    const int key = R->p * 10 + R->dim;
-    switch (key) {
-        case 21: return launch_generic_pd<2, 1>(a, T.maxM, T.maxK, st);
-        case 22: return launch_generic_pd<2, 2>(a, T.maxM, T.maxK, st);
-        case 23: return launch_generic_pd<2, 3>(a, T.maxM, T.maxK, st);
-        case 31: return launch_generic_pd<3, 1>(a, T.maxM, T.maxK, st);
-        case 32: return launch_generic_pd<3, 2>(a, T.maxM, T.maxK, st);
-        case 33: return launch_generic_pd<3, 3>(a, T.maxM, T.maxK, st);
+    // analytic coefficients: factor tables at the nodes (stream-ordered scratch, freed after)
+    double* tab = nullptr;
+    if (c->kind == WGQ_COEF_TRIG_SEP || c->kind == WGQ_COEF_FOURIER_LOGN) {
+        a.cw = c->kind == WGQ_COEF_TRIG_SEP ? 1 : 2 * a.coef.n_modes;
+        const int64_t entries = 2 * (int64_t)R->dim * R->N * kMaxNodes;
+        if (cudaMallocAsync((void**)&tab, (size_t)entries * a.cw * sizeof(double), st) != cudaSuccess) return WGQ_ENOMEM;
+        k_coef_tables<<<(unsigned)((entries + 255) / 256), 256, 0, st>>>(a.coef, R->dim, T, tab, a.cw);
+        a.ctab = tab;
     }
-    return WGQ_EUNSUPPORTED;
+    int rc = WGQ_EUNSUPPORTED;
+    const int key = R->p * 10 + R->dim;
+    int64_t* list = nullptr;
+    if (!force_generic && R->dim == 2 && c->kind == WGQ_COEF_FOURIER_LOGN && a.coef.n_modes > 0) {
+        // tensor-core pass over the rows whose directions all have <= 4 nodes, then the generic
+        // kernel over the remaining shell (rows touching a GL-fallback boundary class, R1)
+        rc = R->p == 3 ? launch_fourier2d_p<3>(a, st) : launch_fourier2d_p<2>(a, st);
+        if (rc != WGQ_OK) {
+            cudaFreeAsync(tab, st);
+            return rc;
+        }
+        std::vector<int64_t> wide;
+        for (int64_t r = 0; r < R->N; ++r) {
+            const int cls = r < R->p ? (int)r : (r >= R->n ? (int)(R->n + R->p - 1 - r) : R->p);
+            if (R->rules[WGQ_MASS][cls].m > 4 || R->rules[WGQ_STIFFNESS][cls].m > 4) wide.push_back(r);
+        }
+        std::vector<int64_t> shell;
+        if (!wide.empty()) {
+            const int64_t N = R->N;
+            for (int64_t i2 = a.row_begin / N; i2 <= (a.row_end - 1) / N; ++i2) {
+                const bool w2 = std::find(wide.begin(), wide.end(), i2) != wide.end();
+                auto add = [&](int64_t i1) {
+                    const int64_t row = i2 * N + i1;
+                    if (row >= a.row_begin && row < a.row_end) shell.push_back(row);
+                };
+                if (w2)
+                    for (int64_t i1 = 0; i1 < N; ++i1) add(i1);
+                else
+                    for (int64_t i1 : wide) add(i1);
+            }
+        }
+        if (shell.empty()) {
+            cudaFreeAsync(tab, st);
+            return WGQ_OK;
+        }
+        if (cudaMallocAsync((void**)&list, shell.size() * sizeof(int64_t), st) != cudaSuccess) return WGQ_ENOMEM;
+        cudaMemcpyAsync(list, shell.data(), shell.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st);
+        a.rows_list = list;
+        a.nlist = (int64_t)shell.size();
+    }
+    switch (key) {
+        case 21: rc = launch_generic_pd<2, 1>(a, T.maxM, T.maxK, st); break;
+        case 22: rc = launch_generic_pd<2, 2>(a, T.maxM, T.maxK, st); break;
+        case 23: rc = launch_generic_pd<2, 3>(a, T.maxM, T.maxK, st); break;
+        case 31: rc = launch_generic_pd<3, 1>(a, T.maxM, T.maxK, st); break;
+        case 32: rc = launch_generic_pd<3, 2>(a, T.maxM, T.maxK, st); break;
+        case 33: rc = launch_generic_pd<3, 3>(a, T.maxM, T.maxK, st); break;
+    }
+    if (list) cudaFreeAsync(list, st);
+    if (tab) cudaFreeAsync(tab, st);
+    return rc;
 }
 
 }  // namespace wgq

@@ -88,6 +88,11 @@ bool line_kernel_applies(const wgq_rules_s* R, const wgq_coeff_t* c, const wgq_o
 int launch_line(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, const wgq_out_t* M,
                 const wgq_out_t* K, void* stream);
 
+// separable.cu (CONST, TRIG_SEP coefficients)
+bool sep_applies(const wgq_coeff_t* c);
+int launch_sep(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, const wgq_out_t* M,
+               const wgq_out_t* K, void* stream);
+
 // grid.cu
 int launch_generate_grid(int64_t n, int dim, uint64_t seed, double sigma, int64_t plane0,
                          int64_t planes, double* grid, void* stream);

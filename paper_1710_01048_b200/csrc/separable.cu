@@ -1,0 +1,240 @@
+// Separable-coefficient fast path (SURVEY §8(a) a3-a7 for CONST and TRIG_SEP; C1, C2, C4).
+//
+// With c(x) = c0 + A prod_a f_a(x_a) (A = 0 for CONST), the row rule's sum factorises
+// completely (eq:Decompo with the coefficient split into its two separable terms):
+//
+//   M_ij = c0 prod_a uM_a[o_a] + A prod_a vM_a[o_a]
+//   K_ij = sum_a ( c0 uK_a[o_a] prod_{b!=a} uM_b[o_b] + A vK_a[o_a] prod_{b!=a} vM_b[o_b] )
+//
+// with, per direction a and 1D row r (nodes / effective weights of the row's rules, P:250,
+// P:351):
+//   uM[o] = sum_k wM_k B_{r+o}(xM_k)        vM[o] = sum_k wM_k f_a(xM_k) B_{r+o}(xM_k)
+//   uK[o] = sum_k wK_k B'_{r+o}(xK_k)       vK[o] = sum_k wK_k f_a(xK_k) B'_{r+o}(xK_k)
+//
+// — the definition's sum, reordered; exact up to rounding.  A table kernel builds the 4 x s
+// vectors of every 1D row; the assembly kernel is then a pure output stream: lanes own
+// consecutive output elements of a warp's chunk of rows (coalesced stores), each element a
+// few products of table entries (L1-resident).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "internal.h"
+
+namespace wgq {
+namespace {
+
+struct SepArgs {
+    const double* sep;     // [dim][N][4][kMaxS]: uM, vM, uK, vK
+    int64_t N;
+    int64_t row_begin, row_end;
+    double c0, amp;
+    double* Mv;
+    double* Kv;
+    int64_t ldM, ldK;
+    const int64_t* rpM;    // CSR row pointers (slab-local), or null for ELL
+    const int64_t* rpK;
+    int layout;
+};
+
+__global__ void k_sep_tables(int dim, int p, RowTables T, int kind, int trig0, int trig1, int trig2, int wn0, int wn1,
+                             int wn2, double* sep) {
+    const int S = 2 * p + 1;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t r = (tid / S) % T.N;
+    const int a = (int)(tid / (S * T.N));
+    const int o = (int)(tid % S);
+    if (a >= dim) return;
+    const int trig = a == 0 ? trig0 : (a == 1 ? trig1 : trig2);
+    const int wn = a == 0 ? wn0 : (a == 1 ? wn1 : wn2);
+    auto f = [&](double x) -> double {
+        if (kind != WGQ_COEF_TRIG_SEP) return 0.0;
+        const double arg = 2.0 * (double)wn * x;    // trig(pi * arg) = trig(2 pi k x)
+        return trig == WGQ_TRIG_SIN ? sinpi(arg) : cospi(arg);
+    };
+    double uM = 0.0, vM = 0.0, uK = 0.0, vK = 0.0;
+    for (int k = 0; k < T.mM[r]; ++k) {
+        const double w = T.wM[r * kMaxMassNodes + k];
+        const double b = T.VM[(r * kMaxMassNodes + k) * kMaxS + o];
+        uM = fma(w, b, uM);
+        vM = fma(w * f(T.xM[r * kMaxMassNodes + k]), b, vM);
+    }
+    for (int k = 0; k < T.mK[r]; ++k) {
+        const double w = T.wK[r * kMaxStiffNodes + k];
+        const double b = T.DK[(r * kMaxStiffNodes + k) * kMaxS + o];
+        uK = fma(w, b, uK);
+        vK = fma(w * f(T.xK[r * kMaxStiffNodes + k]), b, vK);
+    }
+    double* out = sep + ((int64_t)a * T.N + r) * 4 * kMaxS;
+    out[0 * kMaxS + o] = uM;
+    out[1 * kMaxS + o] = vM;
+    out[2 * kMaxS + o] = uK;
+    out[3 * kMaxS + o] = vK;
+}
+
+// position of slot (o - p per direction) inside the CSR row of (i1, i2, i3), or -1
+template <int P, int D>
+__device__ __forceinline__ int csr_pos(const int* o, const int64_t* idx, int64_t N) {
+    int pos = 0, stride = 1;
+#pragma unroll
+    for (int q = 0; q < D; ++q) {
+        const int lo = idx[q] - P < 0 ? (int)-idx[q] : -P;
+        const int hi = idx[q] + P > N - 1 ? (int)(N - 1 - idx[q]) : P;
+        if (o[q] - P < lo || o[q] - P > hi) return -1;
+        pos += (o[q] - P - lo) * stride;
+        stride *= hi - lo + 1;
+    }
+    return pos;
+}
+
+constexpr int kChunkRows = 32;
+
+template <int P, int D, int MODE>
+__global__ void __launch_bounds__(256) k_sep(const SepArgs a) {
+    constexpr int S = 2 * P + 1;
+    constexpr int NS = D == 1 ? S : (D == 2 ? S * S : S * S * S);
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t rows = a.row_end - a.row_begin;
+    for (int64_t c0row = warp * kChunkRows; c0row < rows; c0row += nwarps * kChunkRows) {
+        const int64_t nrows = min((int64_t)kChunkRows, rows - c0row);
+        const int64_t first = a.row_begin + c0row;
+        // lane's first element: row first + lane / NS, slot lane % NS; indices advanced incrementally
+        int rl = lane / NS, slot = lane % NS;
+        int64_t idx[3] = {0, 0, 0};
+        {
+            int64_t rem = first + rl;
+#pragma unroll
+            for (int q = 0; q < D; ++q) {
+                idx[q] = rem % a.N;
+                rem /= a.N;
+            }
+        }
+        while (rl < nrows) {
+            const int o[3] = {slot % S, (slot / S) % S, slot / (S * S)};
+            double uM[3], vM[3], uK[3], vK[3];
+#pragma unroll
+            for (int q = 0; q < D; ++q) {
+                const double* t = a.sep + ((int64_t)q * a.N + idx[q]) * 4 * kMaxS + o[q];
+                uM[q] = __ldg(t);
+                vM[q] = __ldg(t + kMaxS);
+                if (MODE & 2) {
+                    uK[q] = __ldg(t + 2 * kMaxS);
+                    vK[q] = __ldg(t + 3 * kMaxS);
+                }
+            }
+            const int64_t row = first + rl - a.row_begin;
+            int cpos = 0;
+            if (a.layout == WGQ_CSR) cpos = csr_pos<P, D>(o, idx, a.N);
+            if (MODE & 1) {
+                double pu = uM[0], pv = vM[0];
+#pragma unroll
+                for (int q = 1; q < D; ++q) {
+                    pu *= uM[q];
+                    pv *= vM[q];
+                }
+                const double m = fma(a.amp, pv, a.c0 * pu) + 0.0;
+                if (a.layout == WGQ_ELL) a.Mv[row * a.ldM + slot] = m;
+                else if (cpos >= 0) a.Mv[a.rpM[row] + cpos] = m;
+            }
+            if (MODE & 2) {
+                double su = 0.0, sv = 0.0;
+#pragma unroll
+                for (int t = 0; t < D; ++t) {
+                    double pu = 1.0, pv = 1.0;
+#pragma unroll
+                    for (int q = 0; q < D; ++q) {
+                        pu *= q == t ? uK[q] : uM[q];
+                        pv *= q == t ? vK[q] : vM[q];
+                    }
+                    su += pu;
+                    sv += pv;
+                }
+                const double k = fma(a.amp, sv, a.c0 * su) + 0.0;
+                if (a.layout == WGQ_ELL) a.Kv[row * a.ldK + slot] = k;
+                else if (cpos >= 0) a.Kv[a.rpK[row] + cpos] = k;
+            }
+            // advance 32 elements: slot += 32, carrying whole rows into the row indices
+            slot += 32;
+            const int adv = slot / NS;
+            slot -= adv * NS;
+            rl += adv;
+            idx[0] += adv;
+#pragma unroll
+            for (int q = 0; q + 1 < D; ++q) {
+                while (idx[q] >= a.N) {
+                    idx[q] -= a.N;
+                    ++idx[q + 1];
+                }
+            }
+        }
+    }
+}
+
+template <int P, int D>
+int launch_sep_pd(const SepArgs& a, int mode, cudaStream_t st) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t rows = a.row_end - a.row_begin;
+    const int64_t chunks = (rows + kChunkRows - 1) / kChunkRows;
+    int64_t blocks = (chunks + 7) / 8;
+    blocks = std::min<int64_t>(blocks, (int64_t)sms * 16);
+    blocks = std::max<int64_t>(blocks, 1);
+    if (mode == 3) k_sep<P, D, 3><<<(unsigned)blocks, 256, 0, st>>>(a);
+    else if (mode == 1) k_sep<P, D, 1><<<(unsigned)blocks, 256, 0, st>>>(a);
+    else k_sep<P, D, 2><<<(unsigned)blocks, 256, 0, st>>>(a);
+    return cudaGetLastError() == cudaSuccess ? WGQ_OK : WGQ_ECUDA;
+}
+
+}  // namespace
+
+bool sep_applies(const wgq_coeff_t* c) { return c->kind == WGQ_COEF_CONST || c->kind == WGQ_COEF_TRIG_SEP; }
+
+int launch_sep(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, const wgq_out_t* M,
+               const wgq_out_t* K, void* stream) {
+    const wgq_out_t* any = M ? M : K;
+    if (any->row_end <= any->row_begin) return WGQ_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int S = 2 * R->p + 1;
+    const int64_t entries = (int64_t)R->dim * R->N * 4 * kMaxS;
+    double* sep = nullptr;
+    if (cudaMallocAsync((void**)&sep, (size_t)entries * sizeof(double), st) != cudaSuccess) return WGQ_ENOMEM;
+    const int64_t threads = (int64_t)R->dim * R->N * S;
+    k_sep_tables<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(R->dim, R->p, T, c->kind, c->trig[0], c->trig[1],
+                                                                    c->trig[2], c->wavenum[0], c->wavenum[1],
+                                                                    c->wavenum[2], sep);
+    SepArgs a{};
+    a.sep = sep;
+    a.N = R->N;
+    a.row_begin = any->row_begin;
+    a.row_end = any->row_end;
+    a.c0 = c->c0;
+    a.amp = c->kind == WGQ_COEF_TRIG_SEP ? c->amp : 0.0;
+    a.layout = any->layout;
+    if (M) {
+        a.Mv = M->values;
+        a.ldM = M->ld;
+        a.rpM = M->row_ptr;
+    }
+    if (K) {
+        a.Kv = K->values;
+        a.ldK = K->ld;
+        a.rpK = K->row_ptr;
+    }
+    const int mode = (M ? 1 : 0) | (K ? 2 : 0);
+    int rc = WGQ_EUNSUPPORTED;
+    switch (R->p * 10 + R->dim) {
+        case 21: rc = launch_sep_pd<2, 1>(a, mode, st); break;
+        case 22: rc = launch_sep_pd<2, 2>(a, mode, st); break;
+        case 23: rc = launch_sep_pd<2, 3>(a, mode, st); break;
+        case 31: rc = launch_sep_pd<3, 1>(a, mode, st); break;
+        case 32: rc = launch_sep_pd<3, 2>(a, mode, st); break;
+        case 33: rc = launch_sep_pd<3, 3>(a, mode, st); break;
+    }
+    cudaFreeAsync(sep, st);
+    return rc;
+}
+
+}  // namespace wgq
