@@ -32,6 +32,12 @@ int table_for(wgq_rules_s* R, RowTables* out, void* stream) {
         if (rc != WGQ_OK) return rc;
         // the cache is used from any stream afterwards: complete the one-time build now
         if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return WGQ_ECUDA;
+        // keep stream-ordered scratch (coefficient tables) in the device pool between calls
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
         it = R->tables.emplace(dev, T).first;
     }
     *out = it->second;
@@ -145,6 +151,10 @@ void wgq_free_rules(wgq_rules_t R) {
     for (auto& kv : R->tables) {
         cudaSetDevice(kv.first);
         free_row_tables(&kv.second);
+    }
+    for (auto& kv : R->shells) {
+        cudaSetDevice(std::get<0>(kv.first));
+        if (kv.second.first) cudaFree(kv.second.first);
     }
     cudaSetDevice(cur);
     delete R;

@@ -33,6 +33,30 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
+// exp(x) for |x| < 700 in ~20 FP64 instructions: x = k ln2 + r (Cody-Waite, |r| <= ln2/2),
+// e^r by its degree-13 Taylor polynomial (truncation < 2e-16 relative), times 2^k.  Within
+// ~2 ulp of the correctly rounded value (the FOURIER_LOGN exponents are O(1), R13).
+__device__ __forceinline__ double exp_fast(double x) {
+    const double k = rint(x * 1.4426950408889634);
+    double r = fma(-k, 6.93147180369123816490e-01, x);
+    r = fma(-k, 1.90821492927058770002e-10, r);
+    double q = 1.0 / 6227020800.0;
+    q = fma(q, r, 1.0 / 479001600.0);
+    q = fma(q, r, 1.0 / 39916800.0);
+    q = fma(q, r, 1.0 / 3628800.0);
+    q = fma(q, r, 1.0 / 362880.0);
+    q = fma(q, r, 1.0 / 40320.0);
+    q = fma(q, r, 1.0 / 5040.0);
+    q = fma(q, r, 1.0 / 720.0);
+    q = fma(q, r, 1.0 / 120.0);
+    q = fma(q, r, 1.0 / 24.0);
+    q = fma(q, r, 1.0 / 6.0);
+    q = fma(q, r, 0.5);
+    q = fma(q, r, 1.0);
+    q = fma(q, r, 1.0);
+    return q * __longlong_as_double((long long)(1023 + (int)k) << 52);
+}
+
 // per-warp staging sizes (doubles) for the node counts of the rules at hand
 struct Staging {
     int w, t1, t2, per_warp;
@@ -288,75 +312,111 @@ __global__ void __launch_bounds__(kMaxWarps * 32) k_assemble_generic(const Gener
 // fragment of the x-stage products  M = A1^T T,  K = D1^T T_Kx + A1^T T_Ky  (a5, a6).
 // Rows with more than 4 nodes in a direction (GL-fallback boundary classes, R1) are left to
 // the generic kernel (shell pass).
-template <int P, int MODE>
+constexpr int kF2dSeg = 32;   // rows of one x-line per work item (the y-side data is loaded once)
+
+template <int P, int MODE, int KSMAX>
 __global__ void __launch_bounds__(256) k_fourier2d(const GenericArgs a) {
-    constexpr int S = 2 * P + 1;
+    constexpr int S = 2 * P + 1;                        // KSMAX: k-steps of 4 over 2 n_modes
     const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
     const int warps = blockDim.x >> 5, warp = threadIdx.x >> 5;
     const RowTables& T = a.T;
     const int cw = a.cw, J = 2 * a.coef.n_modes;
-    const int64_t N = a.N;
+    const int N = (int)a.N;
     const bool gs = g & 1;                     // x-node of row g / y-node of column g: stiffness?
     const int kg = g >> 1;
-    for (int64_t row = a.row_begin + (int64_t)blockIdx.x * warps + warp; row < a.row_end;
-         row += (int64_t)gridDim.x * warps) {
-        const int64_t i1 = row % N, i2 = row / N;
-        const int nxm = __ldg(T.mM + i1), nxk = __ldg(T.mK + i1), nym = __ldg(T.mM + i2), nyk = __ldg(T.mK + i2);
-        if (nxm > 4 || nxk > 4 || nym > 4 || nyk > 4) continue;     // generic shell pass
-        // ---- exponent GEMM: E[x-node g][y-node n] --------------------------------------------
-        const bool xv = kg < (gs ? nxk : nxm), yv = kg < (gs ? nyk : nym);
-        const double* X = a.ctab + ((int64_t)(0 + (gs ? 1 : 0)) * N + i1) * kMaxNodes * cw + kg * cw;
+    const int segs = (N + kF2dSeg - 1) / kF2dSeg;
+    const int line0 = (int)(a.row_begin / N), line1 = (int)((a.row_end - 1) / N);
+    const int64_t items = (int64_t)(line1 - line0 + 1) * segs;
+    for (int64_t it = (int64_t)blockIdx.x * warps + warp; it < items; it += (int64_t)gridDim.x * warps) {
+        const int i2 = line0 + (int)(it / segs);
+        const int x0 = max((int)((int64_t)(it % segs) * kF2dSeg), (int)(a.row_begin - (int64_t)i2 * N));
+        const int x1 = min((int)((int64_t)(it % segs) * kF2dSeg + kF2dSeg), (int)min((int64_t)N, a.row_end - (int64_t)i2 * N));
+        // ---- y-side data of the line: counts, exponent B fragments, weights, y-stage A fragments
+        const int nym = __ldg(T.mM + i2), nyk = __ldg(T.mK + i2);
+        if (nym > 4 || nyk > 4) continue;                  // whole line in the generic shell pass
+        const bool yv = kg < (gs ? nyk : nym);
         const double* Y = a.ctab + ((int64_t)(2 + (gs ? 1 : 0)) * N + i2) * kMaxNodes * cw + kg * cw;
-        double e0 = 0.0, e1 = 0.0;
-        for (int s = 0; s < J; s += 4) {
-            const int j = s + t;
-            const bool ok = j < J;
-            const double xa = (xv && ok) ? __ldg(X + j) : 0.0;
-            double yb = (yv && ok) ? __ldg(Y + j) : 0.0;
-            if (j & 1) yb = -yb;
-            dmma(e0, e1, xa, yb);
+        double yb[KSMAX];
+#pragma unroll
+        for (int s = 0; s < KSMAX; ++s) {
+            const int j = 4 * s + t;
+            double v = (yv && j < J) ? __ldg(Y + j) : 0.0;
+            yb[s] = (j & 1) ? -v : v;
         }
-        // ---- weighted samples (lane (g, t): x-node g, y-nodes mass t / stiffness t) --------
-        const double wx = xv ? __ldg((gs ? T.wK : T.wM) + i1 * kMaxNodes + kg) : 0.0;
         const double wym = t < nym ? __ldg(T.wM + i2 * kMaxNodes + t) : 0.0;
         const double wyk = t < nyk ? __ldg(T.wK + i2 * kMaxNodes + t) : 0.0;
-        const double s0 = (xv && t < nym) ? exp(e0) * wx * wym : 0.0;
-        const double s1 = (!gs && xv && t < nyk) ? exp(e1) * wx * wyk : 0.0;
-        // ---- y-stage: A fragments A2^T[o2 = g][k2 = t] ----------------------------------------
         const double aVy = (g < S && t < nym) ? __ldg(T.VM + (i2 * kMaxNodes + t) * kMaxS + g) : 0.0;
         const double aDy = (g < S && t < nyk) ? __ldg(T.DK + (i2 * kMaxNodes + t) * kMaxS + g) : 0.0;
-        const double aVx = (g < S && t < nxm) ? __ldg(T.VM + (i1 * kMaxNodes + t) * kMaxS + g) : 0.0;
-        const double aDx = (g < S && t < nxk) ? __ldg(T.DK + (i1 * kMaxNodes + t) * kMaxS + g) : 0.0;
-        double m0 = 0.0, m1 = 0.0, k0 = 0.0, k1 = 0.0;
-        if (MODE & 1) {
-            double tm0 = 0.0, tm1 = 0.0;
-            dmma(tm0, tm1, aVy, gs ? 0.0 : s0);          // T_M^T: lane holds [o2 = g][x mass t] in tm0
-            dmma(m0, m1, aVx, tm0);                       // M = A1^T T_M
-        }
-        if (MODE & 2) {
-            double tx0 = 0.0, tx1 = 0.0, ty0 = 0.0, ty1 = 0.0;
-            dmma(tx0, tx1, aVy, gs ? s0 : 0.0);          // T_Kx^T: [o2 = g][x stiffness t] in tx1
-            dmma(ty0, ty1, aDy, gs ? 0.0 : s1);          // T_Ky^T: [o2 = g][x mass t] in ty0
-            dmma(k0, k1, aDx, tx1);                       // K = D1^T T_Kx + A1^T T_Ky
-            dmma(k0, k1, aVx, ty0);
-        }
-        // ---- store: lane holds (o1 = g, o2 = 2t + i) -------------------------------------------
-        const int64_t orow = row - a.row_begin;
+        const int64_t orow0 = (int64_t)i2 * N - a.row_begin;
+        // x-side data of row i1, loaded one row ahead (the L2 latency of row i1+1's loads
+        // overlaps row i1's tensor-core / exp chain)
+        struct XData {
+            int nxm, nxk;
+            double xa[KSMAX], wx, aVx, aDx;
+        };
+        auto load_x = [&](int i1, XData& d) {
+            d.nxm = __ldg(T.mM + i1);
+            d.nxk = __ldg(T.mK + i1);
+            const bool xv = kg < (gs ? d.nxk : d.nxm);
+            const double* X = a.ctab + ((int64_t)(gs ? 1 : 0) * N + i1) * kMaxNodes * cw + kg * cw;
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-            const int o2 = 2 * t + i;
-            if (g >= S || o2 >= S) continue;
-            const double vm = (i ? m1 : m0) + 0.0, vk = (i ? k1 : k0) + 0.0;
-            if (a.M.layout == WGQ_ELL) {
-                if (MODE & 1) a.M.values[orow * a.M.ld + g + S * o2] = vm;
-                if (MODE & 2) a.K.values[orow * a.K.ld + g + S * o2] = vk;
-            } else {
-                const int lo1 = i1 - P < 0 ? (int)-i1 : -P, hi1 = i1 + P > N - 1 ? (int)(N - 1 - i1) : P;
-                const int lo2 = i2 - P < 0 ? (int)-i2 : -P, hi2 = i2 + P > N - 1 ? (int)(N - 1 - i2) : P;
-                if (g - P < lo1 || g - P > hi1 || o2 - P < lo2 || o2 - P > hi2) continue;
-                const int64_t pos = (g - P - lo1) + (int64_t)(o2 - P - lo2) * (hi1 - lo1 + 1);
-                if (MODE & 1) a.M.values[a.M.row_ptr[orow] + pos] = vm;
-                if (MODE & 2) a.K.values[a.K.row_ptr[orow] + pos] = vk;
+            for (int s = 0; s < KSMAX; ++s) {
+                const int j = 4 * s + t;
+                d.xa[s] = (4 * s < J && xv && j < J) ? __ldg(X + j) : 0.0;
+            }
+            d.wx = xv ? __ldg((gs ? T.wK : T.wM) + i1 * kMaxNodes + kg) : 0.0;
+            d.aVx = (g < S && t < d.nxm) ? __ldg(T.VM + (i1 * kMaxNodes + t) * kMaxS + g) : 0.0;
+            d.aDx = (g < S && t < d.nxk) ? __ldg(T.DK + (i1 * kMaxNodes + t) * kMaxS + g) : 0.0;
+        };
+        XData nx;
+        if (x0 < x1) load_x(x0, nx);
+        for (int i1 = x0; i1 < x1; ++i1) {
+            const XData cx = nx;
+            if (i1 + 1 < x1) load_x(i1 + 1, nx);
+            if (cx.nxm > 4 || cx.nxk > 4) continue;        // generic shell pass
+            // ---- exponent GEMM: E[x-node g][y-node n] (B fragments of the line in yb) -------
+            const bool xv = kg < (gs ? cx.nxk : cx.nxm);
+            double e0 = 0.0, e1 = 0.0;
+#pragma unroll
+            for (int s = 0; s < KSMAX; ++s) {
+                if (4 * s >= J) break;
+                dmma(e0, e1, cx.xa[s], yb[s]);
+            }
+            // ---- weighted samples (lane (g, t): x-node g, y-nodes mass t / stiffness t) ----
+            const double s0 = (xv && t < nym) ? exp_fast(e0) * cx.wx * wym : 0.0;
+            const double s1 = (!gs && xv && t < nyk) ? exp_fast(e1) * cx.wx * wyk : 0.0;
+            const double aVx = cx.aVx, aDx = cx.aDx;
+            double m0 = 0.0, m1 = 0.0, k0 = 0.0, k1 = 0.0;
+            if (MODE & 1) {
+                double tm0 = 0.0, tm1 = 0.0;
+                dmma(tm0, tm1, aVy, gs ? 0.0 : s0);      // T_M^T: lane holds [o2 = g][x mass t] in tm0
+                dmma(m0, m1, aVx, tm0);                   // M = A1^T T_M
+            }
+            if (MODE & 2) {
+                double tx0 = 0.0, tx1 = 0.0, ty0 = 0.0, ty1 = 0.0;
+                dmma(tx0, tx1, aVy, gs ? s0 : 0.0);      // T_Kx^T: [o2 = g][x stiffness t] in tx1
+                dmma(ty0, ty1, aDy, gs ? 0.0 : s1);      // T_Ky^T: [o2 = g][x mass t] in ty0
+                dmma(k0, k1, aDx, tx1);                   // K = D1^T T_Kx + A1^T T_Ky
+                dmma(k0, k1, aVx, ty0);
+            }
+            // ---- store: lane holds (o1 = g, o2 = 2t + i) ---------------------------------------
+            const int64_t orow = orow0 + i1;
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const int o2 = 2 * t + i;
+                if (g >= S || o2 >= S) continue;
+                const double vm = (i ? m1 : m0) + 0.0, vk = (i ? k1 : k0) + 0.0;
+                if (a.M.layout == WGQ_ELL) {
+                    if (MODE & 1) a.M.values[orow * a.M.ld + g + S * o2] = vm;
+                    if (MODE & 2) a.K.values[orow * a.K.ld + g + S * o2] = vk;
+                } else {
+                    const int lo1 = i1 - P < 0 ? -i1 : -P, hi1 = i1 + P > N - 1 ? N - 1 - i1 : P;
+                    const int lo2 = i2 - P < 0 ? -i2 : -P, hi2 = i2 + P > N - 1 ? N - 1 - i2 : P;
+                    if (g - P < lo1 || g - P > hi1 || o2 - P < lo2 || o2 - P > hi2) continue;
+                    const int64_t pos = (g - P - lo1) + (int64_t)(o2 - P - lo2) * (hi1 - lo1 + 1);
+                    if (MODE & 1) a.M.values[a.M.row_ptr[orow] + pos] = vm;
+                    if (MODE & 2) a.K.values[a.K.row_ptr[orow] + pos] = vk;
+                }
             }
         }
     }
@@ -367,13 +427,20 @@ int launch_fourier2d_p(const GenericArgs& a, cudaStream_t st) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t rows = a.row_end - a.row_begin;
-    int64_t blocks = std::min<int64_t>((rows + 7) / 8, (int64_t)sms * 32);
+    const int64_t segs = (a.N + kF2dSeg - 1) / kF2dSeg;
+    const int64_t items = ((a.row_end - 1) / a.N - a.row_begin / a.N + 1) * segs;
+    int64_t blocks = std::min<int64_t>((items + 7) / 8, (int64_t)sms * 32);
     blocks = std::max<int64_t>(blocks, 1);
     const int mode = (a.do_mass ? 1 : 0) | (a.do_stiff ? 2 : 0);
-    if (mode == 3) k_fourier2d<P, 3><<<(unsigned)blocks, 256, 0, st>>>(a);
-    else if (mode == 1) k_fourier2d<P, 1><<<(unsigned)blocks, 256, 0, st>>>(a);
-    else k_fourier2d<P, 2><<<(unsigned)blocks, 256, 0, st>>>(a);
+    if (a.coef.n_modes <= 8) {
+        if (mode == 3) k_fourier2d<P, 3, 4><<<(unsigned)blocks, 256, 0, st>>>(a);
+        else if (mode == 1) k_fourier2d<P, 1, 4><<<(unsigned)blocks, 256, 0, st>>>(a);
+        else k_fourier2d<P, 2, 4><<<(unsigned)blocks, 256, 0, st>>>(a);
+    } else {
+        if (mode == 3) k_fourier2d<P, 3, 8><<<(unsigned)blocks, 256, 0, st>>>(a);
+        else if (mode == 1) k_fourier2d<P, 1, 8><<<(unsigned)blocks, 256, 0, st>>>(a);
+        else k_fourier2d<P, 2, 8><<<(unsigned)blocks, 256, 0, st>>>(a);
+    }
     return cudaGetLastError() == cudaSuccess ? WGQ_OK : WGQ_ECUDA;
 }
 
@@ -437,6 +504,45 @@ CoefDev make_coef(const wgq_coeff_t* c) {
 
 }  // namespace
 
+int shell_rows_2d(wgq_rules_s* R, int64_t row_begin, int64_t row_end, const int64_t** rows, int64_t* count) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return WGQ_ECUDA;
+    std::lock_guard<std::mutex> lock(R->mu);
+    const auto key = std::make_tuple(dev, row_begin, row_end);
+    auto it = R->shells.find(key);
+    if (it == R->shells.end()) {
+        // 1D rows whose rule has more than 4 nodes (the GL-fallback boundary classes, R1)
+        std::vector<int64_t> wide;
+        for (int64_t r = 0; r < R->N; ++r) {
+            const int cls = r < R->p ? (int)r : (r >= R->n ? (int)(R->n + R->p - 1 - r) : R->p);
+            if (R->rules[WGQ_MASS][cls].m > 4 || R->rules[WGQ_STIFFNESS][cls].m > 4) wide.push_back(r);
+        }
+        std::vector<int64_t> shell;
+        const int64_t N = R->N;
+        for (int64_t i2 = row_begin / N; !wide.empty() && i2 <= (row_end - 1) / N; ++i2) {
+            const bool w2 = std::find(wide.begin(), wide.end(), i2) != wide.end();
+            auto add = [&](int64_t i1) {
+                const int64_t row = i2 * N + i1;
+                if (row >= row_begin && row < row_end) shell.push_back(row);
+            };
+            if (w2)
+                for (int64_t i1 = 0; i1 < N; ++i1) add(i1);
+            else
+                for (int64_t i1 : wide) add(i1);
+        }
+        int64_t* d = nullptr;
+        if (!shell.empty()) {
+            if (cudaMalloc((void**)&d, shell.size() * sizeof(int64_t)) != cudaSuccess) return WGQ_ENOMEM;
+            if (cudaMemcpy(d, shell.data(), shell.size() * sizeof(int64_t), cudaMemcpyHostToDevice) != cudaSuccess)
+                return WGQ_ECUDA;
+        }
+        it = R->shells.emplace(key, std::make_pair(d, (int64_t)shell.size())).first;
+    }
+    *rows = it->second.first;
+    *count = it->second.second;
+    return WGQ_OK;
+}
+
 int launch_assemble(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, const wgq_out_t* M,
                     const wgq_out_t* K, void* stream) {
     static const bool force_generic = [] {
@@ -471,7 +577,6 @@ int launch_assemble(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t*
     }
     int rc = WGQ_EUNSUPPORTED;
     const int key = R->p * 10 + R->dim;
-    int64_t* list = nullptr;
     if (!force_generic && R->dim == 2 && c->kind == WGQ_COEF_FOURIER_LOGN && a.coef.n_modes > 0) {
         // tensor-core pass over the rows whose directions all have <= 4 nodes, then the generic
         // kernel over the remaining shell (rows touching a GL-fallback boundary class, R1)
@@ -480,34 +585,15 @@ int launch_assemble(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t*
             cudaFreeAsync(tab, st);
             return rc;
         }
-        std::vector<int64_t> wide;
-        for (int64_t r = 0; r < R->N; ++r) {
-            const int cls = r < R->p ? (int)r : (r >= R->n ? (int)(R->n + R->p - 1 - r) : R->p);
-            if (R->rules[WGQ_MASS][cls].m > 4 || R->rules[WGQ_STIFFNESS][cls].m > 4) wide.push_back(r);
-        }
-        std::vector<int64_t> shell;
-        if (!wide.empty()) {
-            const int64_t N = R->N;
-            for (int64_t i2 = a.row_begin / N; i2 <= (a.row_end - 1) / N; ++i2) {
-                const bool w2 = std::find(wide.begin(), wide.end(), i2) != wide.end();
-                auto add = [&](int64_t i1) {
-                    const int64_t row = i2 * N + i1;
-                    if (row >= a.row_begin && row < a.row_end) shell.push_back(row);
-                };
-                if (w2)
-                    for (int64_t i1 = 0; i1 < N; ++i1) add(i1);
-                else
-                    for (int64_t i1 : wide) add(i1);
-            }
-        }
-        if (shell.empty()) {
+        const int64_t* shell = nullptr;
+        int64_t nshell = 0;
+        rc = shell_rows_2d(const_cast<wgq_rules_s*>(R), a.row_begin, a.row_end, &shell, &nshell);
+        if (rc != WGQ_OK || nshell == 0) {
             cudaFreeAsync(tab, st);
-            return WGQ_OK;
+            return rc;
         }
-        if (cudaMallocAsync((void**)&list, shell.size() * sizeof(int64_t), st) != cudaSuccess) return WGQ_ENOMEM;
-        cudaMemcpyAsync(list, shell.data(), shell.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st);
-        a.rows_list = list;
-        a.nlist = (int64_t)shell.size();
+        a.rows_list = shell;
+        a.nlist = nshell;
     }
     switch (key) {
         case 21: rc = launch_generic_pd<2, 1>(a, T.maxM, T.maxK, st); break;
@@ -517,7 +603,6 @@ int launch_assemble(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t*
         case 32: rc = launch_generic_pd<3, 2>(a, T.maxM, T.maxK, st); break;
         case 33: rc = launch_generic_pd<3, 3>(a, T.maxM, T.maxK, st); break;
     }
-    if (list) cudaFreeAsync(list, st);
     if (tab) cudaFreeAsync(tab, st);
     return rc;
 }

@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <map>
 #include <mutex>
+#include <tuple>
 
 #include "wgq.h"
 
@@ -60,6 +61,9 @@ struct wgq_rules_s {
     wgq::ClassRule rules[2][wgq::kMaxP + 1];
     std::mutex mu;
     std::map<int, wgq::RowTables> tables;   // per CUDA device
+    // shell rows (rows touching a GL-fallback boundary class) of a row range, per device:
+    // (device, row_begin, row_end) -> device array of global row ids (built once, reused)
+    std::map<std::tuple<int, int64_t, int64_t>, std::pair<int64_t*, int64_t>> shells;
 };
 
 namespace wgq {
@@ -76,6 +80,8 @@ int build_row_tables(const wgq_rules_s* R, RowTables* T, void* stream);
 void free_row_tables(RowTables* T);
 
 // assemble.cu
+// Device array of the 2D shell rows of [row_begin, row_end) (cached in the rules handle).
+int shell_rows_2d(wgq_rules_s* R, int64_t row_begin, int64_t row_end, const int64_t** rows, int64_t* count);
 int launch_assemble(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c,
                     const wgq_out_t* M, const wgq_out_t* K, void* stream);
 int launch_csr_structure(const wgq_rules_s* R, int64_t row_begin, int64_t row_end,

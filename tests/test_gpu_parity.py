@@ -77,11 +77,16 @@ def test_all_rows_all_coefficients(p, d, n):
             compare(g[k], ref[k], (p, d, n, name, k), sc[k])
 
 
-@pytest.mark.parametrize("p,d,n", [(2, 2, 9), (3, 3, 4)])
-def test_gl_boundary_mode(p, d, n):
+@pytest.mark.parametrize("p,d,n,kind", [(2, 2, 9, "trig"), (3, 3, 4, "trig"), (3, 2, 10, "fourier"), (2, 2, 7, "fourier")])
+def test_gl_boundary_mode(p, d, n, kind):
+    """WGQ_BND_GL: every boundary class uses GL per element (up to p(p+1) nodes), which sends
+    the 2D FOURIER rows touching them through the generic shell pass."""
     N = n + p
     rows = np.arange(N ** d)
-    desc = {"kind": "trig_sep", "c0": 1.0, "amp": 0.5, "trig": ("sin",) * d, "wavenum": (1,) * d}
+    if kind == "trig":
+        desc = {"kind": "trig_sep", "c0": 1.0, "amp": 0.5, "trig": ("sin",) * d, "wavenum": (1,) * d}
+    else:
+        desc = inputs.coefficient({"kind": "fourier_logn", "seed": 11, "n_modes": 8, "amp": 0.3}, d)
     g, _ = gpu_assemble(p, n, d, desc, bnd=1)
     ref = oasm.assemble_rows(p, n, d, rows, desc, mode="gl")
     sc = oasm.assemble_rows(p, n, d, rows, desc, mode="gl", absolute=True)
@@ -112,14 +117,22 @@ def test_slabs_bitwise_equal_and_padded_ld():
             assert np.array_equal(part[k][:, :343], full[k][lo:hi]), (lo, hi, k)
 
 
-def test_csr_matches_ell():
+@pytest.mark.parametrize("p,d,n,kind", [(2, 3, 5, "trig"), (3, 2, 9, "fourier"), (2, 2, 6, "fourier"),
+                                        (3, 1, 12, "const"), (3, 3, 4, "fourier")])
+def test_csr_matches_ell(p, d, n, kind):
+    """CSR values equal the ELL values at the structural columns, for every kernel family
+    (separable, 2D tensor-core FOURIER incl. its shell pass, generic)."""
     from paper_1710_01048_b200 import api, wgq
-    p, d, n = 2, 3, 5
     rules = wgq.Rules(p, n, d)
-    desc = {"kind": "trig_sep", "c0": 1.0, "amp": 0.3, "trig": ("sin",) * 3, "wavenum": (1,) * 3}
+    if kind == "trig":
+        desc = {"kind": "trig_sep", "c0": 1.0, "amp": 0.3, "trig": ("sin",) * d, "wavenum": (1,) * d}
+    elif kind == "const":
+        desc = {"kind": "const", "c0": 2.5}
+    else:
+        desc = inputs.coefficient({"kind": "fourier_logn", "seed": 7, "n_modes": 8, "amp": 0.3}, d)
     c = api.coefficient(desc)
     ell = api.assemble(rules, c)
-    lo, hi = 17, rules.n_rows - 11
+    lo, hi = min(17, rules.n_rows // 4), rules.n_rows - min(11, rules.n_rows // 4)
     row_ptr, col_idx, vals = api.assemble_csr(rules, c, row_begin=lo, row_end=hi)
     torch.cuda.synchronize()
     rp, ci = row_ptr.cpu().numpy(), col_idx.cpu().numpy()

@@ -49,5 +49,5 @@ for mode in a.dbg.split(","):
         ts.append(e0.elapsed_time(e1))
     ts.sort()
     res[mode] = {"best_ms": round(ts[0], 4), "median_ms": round(ts[len(ts) // 2], 4),
-                 "GBs": round(alg / ts[0] / 1e6, 1)}
+                 "GBs": round(alg / ts[0] / 1e6, 1), "all": [round(x, 3) for x in ts]}
 print(json.dumps({"config": cfg["name"], "n": cfg["n"], "rows": rules.n_rows, "modes": res}))
