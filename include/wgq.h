@@ -154,6 +154,26 @@ int wgq_assemble_mass_stiffness(wgq_rules_t rules, const wgq_coeff_t* c,
 int wgq_csr_structure(wgq_rules_t rules, int64_t row_begin, int64_t row_end,
                       int64_t* row_ptr, int32_t* col_idx, void* stream);
 
+/* ---- load vector (eq:Load) --------------------------------
+ * b[i - row_begin] = sum_k [prod_a w^M_{i_a,k_a}] f(x^M_k) for rows [row_begin, row_end):
+ * row i's own mass-kind weighted rule (the measure B_i, eq:GaussQuadSys P:249-252) applied
+ * to f, a coefficient descriptor (GRID f must cover the rows' vertex planes as for the
+ * assembly).  Exact when f lies in the row's spline space (constants, linear functions).
+ * b: caller-owned DEVICE double[row_end - row_begin].  Enqueued on `stream`; errors as for
+ * the assembly (WGQ_EINVAL for a null b / bad range / bad descriptor). */
+int wgq_assemble_load(wgq_rules_t rules, const wgq_coeff_t* f, int64_t row_begin, int64_t row_end,
+                      double* b, void* stream);
+
+/* ---- matrix-free application (the consumer of the row-wise scheme)
+ * y_M[i - row_begin] = sum_j M_ij u_j and y_K[i - row_begin] = sum_j K_ij u_j for rows
+ * [row_begin, row_end), M and K exactly as wgq_assemble_* defines them for (rules, c): each
+ * row is formed on the fly and contracted with u, nothing is stored.  u: DEVICE vector of
+ * the global rows [u_row0, u_row0 + u_rows), which must contain every column of the rows
+ * (slowest-axis planes z0-p .. z1+p of the slab, clipped to the mesh), else WGQ_ERANGE.
+ * y_M, y_K: caller-owned DEVICE double[row_end - row_begin]; either may be NULL (not both). */
+int wgq_apply(wgq_rules_t rules, const wgq_coeff_t* c, const double* u, int64_t u_row0, int64_t u_rows,
+              int64_t row_begin, int64_t row_end, double* y_M, double* y_K, void* stream);
+
 /* ---- end to end from/to HOST memory ---------------------------------------------------
  * Blocking convenience call for callers whose inputs and outputs live in host memory:
  * uploads the coefficient (for GRID, c->grid is a HOST pointer to the vertex planes

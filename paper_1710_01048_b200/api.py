@@ -84,3 +84,22 @@ def assemble_csr(rules, coeff, kinds=("mass", "stiffness"), row_begin=0, row_end
     else:
         wgq.wgq_assemble_stiffness(rules, coeff, descs["stiffness"], stream)
     return row_ptr, col_idx, vals
+
+
+def assemble_load(rules, f, row_begin=0, row_end=None, out=None, stream=None):
+    """Load vector b_i = int f B_i by the rows' mass rules (eq:Load) for rows [row_begin, row_end)."""
+    if row_end is None:
+        row_end = rules.n_rows
+    b = out if out is not None else torch.empty(row_end - row_begin, dtype=torch.float64, device="cuda")
+    wgq.wgq_assemble_load(rules, f, row_begin, row_end, b, stream)
+    return b
+
+
+def apply(rules, coeff, u, kinds=("mass", "stiffness"), row_begin=0, row_end=None, u_row0=0, stream=None):
+    """Matrix-free y = A u for the rows [row_begin, row_end) (u: global rows from u_row0)."""
+    if row_end is None:
+        row_end = rules.n_rows
+    rows = row_end - row_begin
+    y = {k: torch.empty(rows, dtype=torch.float64, device="cuda") for k in kinds}
+    wgq.wgq_apply(rules, coeff, u, u_row0, row_begin, row_end, y.get("mass"), y.get("stiffness"), stream)
+    return y

@@ -205,6 +205,48 @@ int wgq_assemble_mass_stiffness(wgq_rules_t R, const wgq_coeff_t* c, const wgq_o
     return assemble(R, c, M, K, stream);
 }
 
+int wgq_assemble_load(wgq_rules_t R, const wgq_coeff_t* f, int64_t row_begin, int64_t row_end, double* b,
+                      void* stream) {
+    if (!R || row_begin < 0 || row_end < row_begin || row_end > ipow(R->N, R->dim)) return WGQ_EINVAL;
+    if (row_end > row_begin && !b) return WGQ_EINVAL;
+    wgq_out_t range{};
+    range.row_begin = row_begin;
+    range.row_end = row_end;
+    int rc;
+    if ((rc = check_coeff(R, f, &range)) != WGQ_OK) return rc;
+    if (row_end == row_begin) return WGQ_OK;
+    RowTables T;
+    if ((rc = table_for(R, &T, stream)) != WGQ_OK) return rc;
+    return launch_load(R, T, f, row_begin, row_end, b, stream);
+}
+
+int wgq_apply(wgq_rules_t R, const wgq_coeff_t* c, const double* u, int64_t u_row0, int64_t u_rows, int64_t row_begin,
+              int64_t row_end, double* y_M, double* y_K, void* stream) {
+    if (!R || row_begin < 0 || row_end < row_begin || row_end > ipow(R->N, R->dim)) return WGQ_EINVAL;
+    if (row_end == row_begin) return WGQ_OK;
+    if (!u || (!y_M && !y_K) || u_row0 < 0 || u_rows < 0) return WGQ_EINVAL;
+    // u must hold every column of the rows: the slowest-axis planes z0-p .. z1+p (clipped)
+    const int64_t plane_rows = ipow(R->N, R->dim - 1);
+    const int64_t z0 = row_begin / plane_rows, z1 = (row_end - 1) / plane_rows;
+    const int64_t need_lo = (z0 - R->p > 0 ? z0 - R->p : 0) * plane_rows;
+    const int64_t need_hi = (z1 + R->p + 1 < R->N ? z1 + R->p + 1 : R->N) * plane_rows;
+    if (R->dim == 1) {
+        if (u_row0 > (row_begin - R->p > 0 ? row_begin - R->p : 0) ||
+            u_row0 + u_rows < (row_end + R->p < R->N ? row_end + R->p : R->N))
+            return WGQ_ERANGE;
+    } else if (u_row0 > need_lo || u_row0 + u_rows < need_hi) {
+        return WGQ_ERANGE;
+    }
+    wgq_out_t range{};
+    range.row_begin = row_begin;
+    range.row_end = row_end;
+    int rc;
+    if ((rc = check_coeff(R, c, &range)) != WGQ_OK) return rc;
+    RowTables T;
+    if ((rc = table_for(R, &T, stream)) != WGQ_OK) return rc;
+    return launch_apply(R, T, c, u, u_row0, row_begin, row_end, y_M, y_K, stream);
+}
+
 int wgq_csr_structure(wgq_rules_t R, int64_t row_begin, int64_t row_end, int64_t* row_ptr, int32_t* col_idx,
                       void* stream) {
     if (!R || !row_ptr || row_begin < 0 || row_end < row_begin || row_end > ipow(R->N, R->dim)) return WGQ_EINVAL;

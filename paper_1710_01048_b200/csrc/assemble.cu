@@ -76,6 +76,12 @@ struct GenericArgs {
     int cw;                // doubles per node in ctab
     const int64_t* rows_list;   // if set: assemble only these rows (global ids inside the range)
     int64_t nlist;
+    // matrix-free mode (wgq_apply): instead of storing row i, y[i] = sum_j A_ij u[j - u_row0]
+    int apply;
+    const double* u;
+    int64_t u_row0;
+    double* yM;
+    double* yK;
     int64_t n, N;
     int64_t row_begin, row_end;
     OutDev M, K;
@@ -266,6 +272,40 @@ __global__ void __launch_bounds__(kMaxWarps * 32) k_assemble_generic(const Gener
         }
         // a7: store (x + 0.0 turns a -0.0 from all-zero products into +0.0)
         const int64_t orow = row - a.row_begin;
+        if (a.apply) {
+            // matrix-free: dot the row with u over its structural columns, reduce over the warp
+            double pm = 0.0, pk = 0.0;
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) {
+                const int slot = lane + 32 * j;
+                if (slot >= NS) continue;
+                const int o[3] = {slot % S1 - P, (slot / S1) % S2 - (D >= 2 ? P : 0), slot / (S1 * S2) - (D >= 3 ? P : 0)};
+                int64_t col = 0, stride = 1;
+                bool ok = true;
+#pragma unroll
+                for (int q = 0; q < D; ++q) {
+                    const int64_t jq = idx[q] + o[q];
+                    ok = ok && jq >= 0 && jq < a.N;
+                    col += jq * stride;
+                    stride *= a.N;
+                }
+                if (!ok) continue;
+                const double uj = __ldg(a.u + (col - a.u_row0));
+                pm = fma(accM[j], uj, pm);
+                pk = fma(accK[j], uj, pk);
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                pm += __shfl_xor_sync(0xffffffffu, pm, off);
+                pk += __shfl_xor_sync(0xffffffffu, pk, off);
+            }
+            if (lane == 0) {
+                if (a.yM) a.yM[orow] = pm;
+                if (a.yK) a.yK[orow] = pk;
+            }
+            __syncwarp();
+            continue;
+        }
 #pragma unroll
         for (int j = 0; j < NJ; ++j) {
             const int slot = lane + 32 * j;
@@ -502,6 +542,130 @@ CoefDev make_coef(const wgq_coeff_t* c) {
     return d;
 }
 
+// ---------------------------------------------------------------------------------------------
+// Load vector (eq:Load): b_i = sum_k [prod_a w^M_{i_a,k_a}] f(x^M_k),
+// row i's mass-kind rule applied to f.  One thread per row.
+//  * GRID f (multilinear, R6): with PW[r][v] = sum_k w^M_k lambda_v(x_k) = sum_o PM[r][v][o]
+//    (partition of unity), b_i = sum_v g[bz+vz][by+vy][bx+vx] prod_a PW_a[v_a] — the same sum
+//    reordered (vertex projection, as in the line kernel).
+//  * analytic f: the node-tensor sum with the coefficient factor tables (or c0).
+__global__ void k_vertex_weights(RowTables T, int p, double* PW) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= T.N * kMaxV) return;
+    const int64_t r = e / kMaxV;
+    const int v = (int)(e % kMaxV);
+    double s = 0.0;
+    for (int o = 0; o < 2 * p + 1; ++o) s += T.PM[(r * kMaxV + v) * kMaxS + o];   // the row's 2p+1 neighbours
+    PW[e] = s;
+}
+
+template <int P, int D>
+__global__ void __launch_bounds__(256) k_load(const GenericArgs a, const double* PW, double* b) {
+    constexpr int V = P + 2;
+    const int64_t rows = a.row_end - a.row_begin;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < rows; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = a.row_begin + t;
+        int64_t idx[3] = {0, 0, 0};
+        int64_t rem = row;
+#pragma unroll
+        for (int q = 0; q < D; ++q) {
+            idx[q] = rem % a.N;
+            rem /= a.N;
+        }
+        double acc = 0.0;
+        if (a.coef.kind == WGQ_COEF_GRID) {
+            const int64_t nv = a.n + 1;
+            int64_t base[3];
+#pragma unroll
+            for (int q = 0; q < D; ++q) base[q] = idx[q] - P > 0 ? idx[q] - P : 0;
+            const int Vz = D >= 3 ? V : 1, Vy = D >= 2 ? V : 1;
+            for (int vz = 0; vz < Vz; ++vz) {
+                const double wz = D >= 3 ? PW[idx[2] * kMaxV + vz] : 1.0;
+                for (int vy = 0; vy < Vy; ++vy) {
+                    const double wy = D >= 2 ? PW[idx[1] * kMaxV + vy] : 1.0;
+                    const int64_t zz = D >= 3 ? base[2] + vz : 0, yy = D >= 2 ? base[1] + vy : 0;
+                    const int64_t zrow = D == 3 ? zz : (D == 2 ? yy : 0);
+                    if (wz * wy == 0.0 || zz > a.n || yy > a.n) continue;
+                    double sx = 0.0;
+#pragma unroll
+                    for (int vx = 0; vx < V; ++vx) {
+                        const int64_t xx = base[0] + vx;
+                        const double wx = PW[idx[0] * kMaxV + vx];
+                        if (wx == 0.0 || xx > a.n) continue;
+                        const double* g;
+                        if (D == 1) g = a.coef.grid + (xx - a.coef.plane0);
+                        else if (D == 2) g = a.coef.grid + (zrow - a.coef.plane0) * nv + xx;
+                        else g = a.coef.grid + ((zz - a.coef.plane0) * nv + yy) * nv + xx;
+                        sx = fma(wx, __ldg(g), sx);
+                    }
+                    acc = fma(wz * wy, sx, acc);
+                }
+            }
+        } else {
+            const RowTables& T = a.T;
+            const int n1 = T.mM[idx[0]], n2 = D >= 2 ? T.mM[idx[1]] : 1, n3 = D >= 3 ? T.mM[idx[2]] : 1;
+            for (int k3 = 0; k3 < n3; ++k3) {
+                const double w3 = D >= 3 ? T.wM[idx[2] * kMaxMassNodes + k3] : 1.0;
+                for (int k2 = 0; k2 < n2; ++k2) {
+                    const double w2 = D >= 2 ? T.wM[idx[1] * kMaxMassNodes + k2] : 1.0;
+                    for (int k1 = 0; k1 < n1; ++k1) {
+                        const double w1 = T.wM[idx[0] * kMaxMassNodes + k1];
+                        double cv = a.coef.c0;
+                        if (a.ctab) {
+                            const int64_t k[3] = {k1, k2, k3};
+                            const double* f[3];
+#pragma unroll
+                            for (int q = 0; q < 3; ++q)
+                                f[q] = q < D ? a.ctab + ((int64_t)(2 * q + WGQ_MASS) * a.N + idx[q]) * kMaxNodes * a.cw + k[q] * a.cw
+                                             : nullptr;
+                            cv = coef_from_tables<D>(a.coef, f[0], f[1], f[2]);
+                        }
+                        acc = fma(w1 * w2 * w3, cv, acc);
+                    }
+                }
+            }
+        }
+        b[t] = acc;
+    }
+}
+
+template <int P, int D>
+int launch_load_pd(const GenericArgs& a, const double* PW, double* b, cudaStream_t st) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t rows = a.row_end - a.row_begin;
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((rows + 255) / 256, (int64_t)sms * 16));
+    k_load<P, D><<<(unsigned)blocks, 256, 0, st>>>(a, PW, b);
+    return cudaGetLastError() == cudaSuccess ? WGQ_OK : WGQ_ECUDA;
+}
+
+// coefficient factor tables for an analytic kind (stream-ordered scratch) or nullptr
+int coef_tables(const wgq_rules_s* R, const RowTables& T, GenericArgs& a, const wgq_coeff_t* c, cudaStream_t st,
+                double** tab) {
+    *tab = nullptr;
+    if (c->kind != WGQ_COEF_TRIG_SEP && c->kind != WGQ_COEF_FOURIER_LOGN) return WGQ_OK;
+    a.cw = c->kind == WGQ_COEF_TRIG_SEP ? 1 : 2 * a.coef.n_modes;
+    if (a.cw == 0) a.cw = 1;
+    const int64_t entries = 2 * (int64_t)R->dim * R->N * kMaxNodes;
+    if (cudaMallocAsync((void**)tab, (size_t)entries * a.cw * sizeof(double), st) != cudaSuccess) return WGQ_ENOMEM;
+    k_coef_tables<<<(unsigned)((entries + 255) / 256), 256, 0, st>>>(a.coef, R->dim, T, *tab, a.cw);
+    a.ctab = *tab;
+    return WGQ_OK;
+}
+
+GenericArgs base_args(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, int64_t row_begin,
+                      int64_t row_end) {
+    GenericArgs a{};
+    a.T = T;
+    a.coef = make_coef(c);
+    a.n = R->n;
+    a.N = R->N;
+    a.row_begin = row_begin;
+    a.row_end = row_end;
+    return a;
+}
+
 }  // namespace
 
 int shell_rows_2d(wgq_rules_s* R, int64_t row_begin, int64_t row_end, const int64_t** rows, int64_t* count) {
@@ -596,6 +760,62 @@ int launch_assemble(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t*
         a.nlist = nshell;
     }
     switch (key) {
+        case 21: rc = launch_generic_pd<2, 1>(a, T.maxM, T.maxK, st); break;
+        case 22: rc = launch_generic_pd<2, 2>(a, T.maxM, T.maxK, st); break;
+        case 23: rc = launch_generic_pd<2, 3>(a, T.maxM, T.maxK, st); break;
+        case 31: rc = launch_generic_pd<3, 1>(a, T.maxM, T.maxK, st); break;
+        case 32: rc = launch_generic_pd<3, 2>(a, T.maxM, T.maxK, st); break;
+        case 33: rc = launch_generic_pd<3, 3>(a, T.maxM, T.maxK, st); break;
+    }
+    if (tab) cudaFreeAsync(tab, st);
+    return rc;
+}
+
+int launch_load(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, int64_t row_begin, int64_t row_end,
+                double* b, void* stream) {
+    if (row_end <= row_begin) return WGQ_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    GenericArgs a = base_args(R, T, c, row_begin, row_end);
+    double* tab = nullptr;
+    double* PW = nullptr;
+    int rc = coef_tables(R, T, a, c, st, &tab);
+    if (rc != WGQ_OK) return rc;
+    if (c->kind == WGQ_COEF_GRID) {
+        if (cudaMallocAsync((void**)&PW, (size_t)R->N * kMaxV * sizeof(double), st) != cudaSuccess) return WGQ_ENOMEM;
+        k_vertex_weights<<<(unsigned)((R->N * kMaxV + 255) / 256), 256, 0, st>>>(T, R->p, PW);
+    }
+    rc = WGQ_EUNSUPPORTED;
+    switch (R->p * 10 + R->dim) {
+        case 21: rc = launch_load_pd<2, 1>(a, PW, b, st); break;
+        case 22: rc = launch_load_pd<2, 2>(a, PW, b, st); break;
+        case 23: rc = launch_load_pd<2, 3>(a, PW, b, st); break;
+        case 31: rc = launch_load_pd<3, 1>(a, PW, b, st); break;
+        case 32: rc = launch_load_pd<3, 2>(a, PW, b, st); break;
+        case 33: rc = launch_load_pd<3, 3>(a, PW, b, st); break;
+    }
+    if (tab) cudaFreeAsync(tab, st);
+    if (PW) cudaFreeAsync(PW, st);
+    return rc;
+}
+
+int launch_apply(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, const double* u, int64_t u_row0,
+                 int64_t row_begin, int64_t row_end, double* yM, double* yK, void* stream) {
+    if (row_end <= row_begin) return WGQ_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    GenericArgs a = base_args(R, T, c, row_begin, row_end);
+    a.apply = 1;
+    a.u = u;
+    a.u_row0 = u_row0;
+    a.yM = yM;
+    a.yK = yK;
+    a.do_mass = yM != nullptr;
+    a.do_stiff = yK != nullptr;
+    a.M.layout = WGQ_ELL;
+    double* tab = nullptr;
+    int rc = coef_tables(R, T, a, c, st, &tab);
+    if (rc != WGQ_OK) return rc;
+    rc = WGQ_EUNSUPPORTED;
+    switch (R->p * 10 + R->dim) {
         case 21: rc = launch_generic_pd<2, 1>(a, T.maxM, T.maxK, st); break;
         case 22: rc = launch_generic_pd<2, 2>(a, T.maxM, T.maxK, st); break;
         case 23: rc = launch_generic_pd<2, 3>(a, T.maxM, T.maxK, st); break;

@@ -89,6 +89,12 @@ int launch_csr_structure(const wgq_rules_s* R, int64_t row_begin, int64_t row_en
 int launch_row_moments(const wgq_rules_s* R, const wgq_out_t* A, double* out, void* stream);
 int launch_checksum(const wgq_rules_s* R, const wgq_out_t* A, unsigned long long* out, void* stream);
 
+// load vector / matrix-free application (assemble.cu)
+int launch_load(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, int64_t row_begin, int64_t row_end,
+                double* b, void* stream);
+int launch_apply(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, const double* u, int64_t u_row0,
+                 int64_t row_begin, int64_t row_end, double* yM, double* yK, void* stream);
+
 // assemble_line.cu (GRID coefficient, d = 3, ELL)
 bool line_kernel_applies(const wgq_rules_s* R, const wgq_coeff_t* c, const wgq_out_t* M, const wgq_out_t* K);
 int launch_line(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, const wgq_out_t* M,

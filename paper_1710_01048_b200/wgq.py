@@ -68,6 +68,8 @@ def lib():
         "wgq_assemble_mass_stiffness": (c_int, [vp, ctypes.POINTER(wgq_coeff_t), ctypes.POINTER(wgq_out_t),
                                                 ctypes.POINTER(wgq_out_t), vp]),
         "wgq_csr_structure": (c_int, [vp, c_i64, c_i64, vp, vp, vp]),
+        "wgq_assemble_load": (c_int, [vp, ctypes.POINTER(wgq_coeff_t), c_i64, c_i64, vp, vp]),
+        "wgq_apply": (c_int, [vp, ctypes.POINTER(wgq_coeff_t), vp, c_i64, c_i64, c_i64, c_i64, vp, vp, vp]),
         "wgq_generate_grid": (c_int, [c_i64, c_int, ctypes.c_uint64, ctypes.c_double, c_i64, c_i64, vp, vp]),
         "wgq_row_moments": (c_int, [vp, ctypes.POINTER(wgq_out_t), vp, vp]),
         "wgq_checksum": (c_int, [vp, ctypes.POINTER(wgq_out_t), vp, vp]),
@@ -86,7 +88,8 @@ def lib():
 def exported_symbols():
     return ["wgq_strerror", "wgq_version", "wgq_build_rules", "wgq_build_rules_ex", "wgq_free_rules",
             "wgq_rules_info", "wgq_rules_query", "wgq_nnz", "wgq_assemble_mass", "wgq_assemble_stiffness",
-            "wgq_assemble_mass_stiffness", "wgq_csr_structure", "wgq_generate_grid", "wgq_row_moments",
+            "wgq_assemble_mass_stiffness", "wgq_csr_structure", "wgq_assemble_load", "wgq_apply",
+            "wgq_generate_grid", "wgq_row_moments",
             "wgq_checksum", "wgq_assemble_host", "wgq_host_alloc", "wgq_host_free"]
 
 
@@ -182,6 +185,7 @@ def make_coeff(desc, grid=None, plane0=0):
         if grid is None:
             raise ValueError("grid coefficient needs a device grid tensor")
         c.grid = grid.data_ptr()
+        keep.append(grid)                  # the descriptor holds a raw pointer: keep the tensor alive
         c.grid_plane0 = int(plane0)
         c.grid_planes = int(grid.shape[0])
     else:
@@ -223,6 +227,17 @@ def wgq_csr_structure(rules, row_begin, row_end, row_ptr, col_idx, stream=None):
     _check("wgq_csr_structure", lib().wgq_csr_structure(rules.handle, row_begin, row_end, row_ptr.data_ptr(),
                                                         col_idx.data_ptr() if col_idx is not None else None,
                                                         _stream(stream)))
+
+
+def wgq_assemble_load(rules, f, row_begin, row_end, b, stream=None):
+    _check("wgq_assemble_load", lib().wgq_assemble_load(rules.handle, ctypes.byref(f), row_begin, row_end, b.data_ptr(),
+                                                        _stream(stream)))
+
+
+def wgq_apply(rules, coeff, u, u_row0, row_begin, row_end, yM=None, yK=None, stream=None):
+    ptr = (lambda t: t.data_ptr() if t is not None else None)
+    _check("wgq_apply", lib().wgq_apply(rules.handle, ctypes.byref(coeff), u.data_ptr(), u_row0, u.numel(), row_begin,
+                                        row_end, ptr(yM), ptr(yK), _stream(stream)))
 
 
 def wgq_generate_grid(n_elems, dim, seed, sigma, plane0, planes, grid, stream=None):

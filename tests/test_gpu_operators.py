@@ -1,0 +1,124 @@
+"""GPU parity of the load vector and the matrix-free product against
+the oracle (oracle/operators.py), through the C-ABI (wgq_assemble_load, wgq_apply).
+
+Tolerances as for the matrices (north_star, R12): relative Frobenius <= 1e-12 and
+max entrywise relative <= 1e-10; for y = A u the entrywise denominator is floored at the
+rounding scale sum_j |A|_ij |u_j| (|A| = the oracle's absolute-value assembly), since a
+random u makes y_i a cancelling sum.
+"""
+import numpy as np
+import pytest
+
+import inputs
+from oracle import assemble as oasm
+from oracle import operators as oops
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+REL_F, REL_E = 1e-12, 1e-10
+FLOOR = 64 * np.finfo(np.float64).eps / REL_E
+
+
+def check(g, ref, scale, what):
+    nrm = np.linalg.norm(ref)
+    relf = np.linalg.norm(g - ref) / (nrm if nrm > 0 else 1.0)
+    den = np.maximum(np.maximum(np.abs(ref), 1e-14 * np.max(np.abs(ref))), FLOOR * scale)
+    rele = np.max(np.abs(g - ref) / np.where(den > 0, den, 1.0))
+    assert relf <= REL_F, (what, relf)
+    assert rele <= REL_E, (what, rele)
+
+
+def coeff_cases(d):
+    return [("const", {"kind": "const", "c0": 1.3}),
+            ("trig", {"kind": "trig_sep", "c0": 1.0, "amp": 0.5, "trig": ("sin", "cos", "sin")[:d],
+                      "wavenum": (1, 1, 2)[:d]}),
+            ("fourier", inputs.coefficient({"kind": "fourier_logn", "seed": inputs.SEED, "n_modes": 8, "amp": 0.3}, d)),
+            ("grid", {"kind": "grid", "seed": 4, "sigma": 0.5})]
+
+
+def coef_obj(desc, n, d):
+    from paper_1710_01048_b200 import api
+    grid = inputs.lognormal_grid(n, seed=desc["seed"], dim=d) if desc["kind"] == "grid" else None
+    gt = torch.from_numpy(np.ascontiguousarray(grid)).cuda() if grid is not None else None
+    return api.coefficient(desc, gt, 0), grid
+
+
+SMALL = [(2, 1, 20), (3, 1, 17), (2, 2, 9), (3, 2, 8), (2, 3, 5), (3, 3, 4), (3, 3, 3)]
+
+
+@pytest.mark.parametrize("p,d,n", SMALL)
+def test_load_vector_all_coefficients(p, d, n):
+    from paper_1710_01048_b200 import api, wgq
+    rules = wgq.Rules(p, n, d)
+    rows = np.arange(rules.n_rows)
+    for name, desc in coeff_cases(d):
+        c, grid = coef_obj(desc, n, d)
+        b = api.assemble_load(rules, c)
+        torch.cuda.synchronize()
+        ref = oops.load_rows(p, n, d, rows, desc, grid=grid)
+        check(b.cpu().numpy(), ref, np.abs(ref), (p, d, n, name))
+
+
+@pytest.mark.parametrize("p,d,n", SMALL)
+def test_apply_all_coefficients(p, d, n):
+    from paper_1710_01048_b200 import api, wgq
+    rules = wgq.Rules(p, n, d)
+    rows = np.arange(rules.n_rows)
+    u = np.random.default_rng(p * 100 + d * 10 + n).standard_normal(rules.n_rows)
+    ut = torch.from_numpy(u).cuda()
+    for name, desc in coeff_cases(d):
+        c, grid = coef_obj(desc, n, d)
+        y = api.apply(rules, c, ut)
+        torch.cuda.synchronize()
+        absA = oasm.assemble_rows(p, n, d, rows, desc, grid=grid, absolute=True)
+        for kind in ("mass", "stiffness"):
+            ref = oops.apply_rows(p, n, d, rows, desc, u, kind, grid=grid)
+            scale = np.array([absA[kind][i][oasm.ell_columns(p, n, d, r) >= 0] @
+                              np.abs(u[oasm.ell_columns(p, n, d, r)[oasm.ell_columns(p, n, d, r) >= 0]])
+                              for i, r in enumerate(rows)])
+            check(y[kind].cpu().numpy(), ref, scale, (p, d, n, name, kind))
+
+
+def test_apply_slab_matches_full_and_checks_u_range():
+    """A z-slab with u holding only its planes +- p gives the full result's rows; too short a
+    u is rejected (WGQ_ERANGE)."""
+    from paper_1710_01048_b200 import api, wgq
+    p, d, n = 3, 3, 6
+    rules = wgq.Rules(p, n, d)
+    N = rules.N
+    u = torch.from_numpy(np.random.default_rng(3).standard_normal(rules.n_rows)).cuda()
+    desc = inputs.coefficient({"kind": "fourier_logn", "seed": 2, "n_modes": 8, "amp": 0.3}, d)
+    c = api.coefficient(desc)
+    full = api.apply(rules, c, u)
+    z0, z1 = 3, 6                                         # rows of planes 3..5
+    lo, hi = max(0, z0 - p) * N * N, min(N, z1 + p) * N * N
+    part = api.apply(rules, c, u[lo:hi], row_begin=z0 * N * N, row_end=z1 * N * N, u_row0=lo)
+    torch.cuda.synchronize()
+    for k in ("mass", "stiffness"):
+        assert torch.equal(part[k], full[k][z0 * N * N:z1 * N * N])
+    with pytest.raises(wgq.WgqError):
+        api.apply(rules, c, u[lo + N * N:hi], row_begin=z0 * N * N, row_end=z1 * N * N, u_row0=lo + N * N)
+
+
+def test_load_full_size_c5_sampled_rows():
+    """C5's mesh and device-generated grid: every boundary row class plus random rows."""
+    from paper_1710_01048_b200 import api, wgq
+    cfg = inputs.config("C5")
+    p, n, d = cfg["p"], cfg["n"], cfg["dim"]
+    rules = wgq.Rules(p, n, d)
+    grid, plane0 = api.make_grid(rules, cfg["coeff"]["seed"], cfg["coeff"]["sigma"], 0, rules.n_rows)
+    c = api.coefficient({"kind": "grid"}, grid, plane0)
+    b = api.assemble_load(rules, c)
+    torch.cuda.synchronize()
+    N = rules.N
+    rng = np.random.default_rng(5)
+    edge = list(range(0, 2 * p + 2)) + list(range(N - 2 * p - 2, N))
+    rows = sorted({sum(int(rng.choice(edge) if rng.random() < 0.5 else rng.integers(0, N)) * N ** a
+                       for a in range(d)) for _ in range(300)})
+    zs = sorted({r // (N * N) for r in rows})
+    host = inputs.lognormal_grid(n, seed=cfg["coeff"]["seed"])
+    ref = oops.load_rows(p, n, d, np.array(rows), {"kind": "grid"}, grid=host)
+    got = b.cpu().numpy()[rows]
+    check(got, ref, np.abs(ref), "C5 load")
+    assert len(zs) > 3

@@ -24,6 +24,7 @@ ap.add_argument("--n", type=int, default=None)
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--dbg", default="0")
 ap.add_argument("--ld", type=int, default=None)
+ap.add_argument("--op", default="assemble", choices=["assemble", "load", "apply"])
 a = ap.parse_args()
 cfg = inputs.config(a.config, a.n)
 rules = wgq.Rules(cfg["p"], cfg["n"], cfg["dim"])
@@ -31,23 +32,34 @@ grid, plane0 = (None, 0)
 if cfg["coeff"]["kind"] == "grid":
     grid, plane0 = api.make_grid(rules, cfg["coeff"]["seed"], cfg["coeff"]["sigma"], 0, rules.n_rows)
 coef = api.coefficient(inputs.coefficient(cfg["coeff"], cfg["dim"]), grid, plane0)
-out = {k: api.alloc_ell(rules, 0, rules.n_rows, a.ld) for k in cfg["kinds"]}
+out = {k: api.alloc_ell(rules, 0, rules.n_rows, a.ld) for k in cfg["kinds"]} if a.op == "assemble" else None
+u = torch.randn(rules.n_rows, dtype=torch.float64, device="cuda") if a.op == "apply" else None
+bvec = torch.empty(rules.n_rows, dtype=torch.float64, device="cuda") if a.op == "load" else None
+
+
+def run():
+    if a.op == "assemble":
+        api.assemble(rules, coef, cfg["kinds"], out=out)
+    elif a.op == "load":
+        api.assemble_load(rules, coef, out=bvec)
+    else:
+        api.apply(rules, coef, u, cfg["kinds"])
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
-alg = rules.n_rows * rules.stencil * 8 * len(cfg["kinds"])
+alg = rules.n_rows * rules.stencil * 8 * len(cfg["kinds"]) if a.op == "assemble" else rules.n_rows * 8
 res = {}
 for mode in a.dbg.split(","):
     os.environ["WGQ_LINE_DBG"] = mode
-    api.assemble(rules, coef, cfg["kinds"], out=out)
+    run()
     ts = []
     for _ in range(a.reps):
         flush.fill_(1)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        api.assemble(rules, coef, cfg["kinds"], out=out)
+        run()
         e1.record()
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
     ts.sort()
     res[mode] = {"best_ms": round(ts[0], 4), "median_ms": round(ts[len(ts) // 2], 4),
                  "GBs": round(alg / ts[0] / 1e6, 1), "all": [round(x, 3) for x in ts]}
-print(json.dumps({"config": cfg["name"], "n": cfg["n"], "rows": rules.n_rows, "modes": res}))
+print(json.dumps({"config": cfg["name"], "op": a.op, "n": cfg["n"], "rows": rules.n_rows, "modes": res}))
