@@ -801,6 +801,12 @@ int launch_load(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, 
 int launch_apply(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, const double* u, int64_t u_row0,
                  int64_t row_begin, int64_t row_end, double* yM, double* yK, void* stream) {
     if (row_end <= row_begin) return WGQ_OK;
+    static const bool force_generic = [] {
+        const char* e = getenv("WGQ_FORCE_GENERIC");
+        return e && e[0] == '1';
+    }();
+    if (!force_generic && line_apply_applies(R, c))
+        return launch_line_apply(R, T, c, u, u_row0, row_begin, row_end, yM, yK, stream);
     cudaStream_t st = (cudaStream_t)stream;
     GenericArgs a = base_args(R, T, c, row_begin, row_end);
     a.apply = 1;

@@ -54,6 +54,7 @@ struct Cfg {
 #endif
     static constexpr int PFD = WGQ_LINE_PFD;           // prefetch distance (tiles) = patch / Q buffers
     static constexpr int XB = 4 * P * 2 * V * S;       // x-boundary rows' vertex tables
+    static constexpr int URING = 48;                   // u columns (apply): window + prefetched columns
     static constexpr int SMEM = 2 * STAGE + RING * 2 * S2 + PFD * 4 * V * S + PFD * PATCH + XB;
     static_assert(W <= RING, "ring too small");
 };
@@ -72,6 +73,11 @@ struct LineArgs {
     // (kernel parameters: constant-bank operands, no global state shared between handles)
     double PMh[kMaxV][kMaxS], PKi[kMaxV][kMaxS];
     int dbg;   // profiling only (WGQ_LINE_DBG bits): 1 = skip compute, 2 = skip stores, 4 = skip loads
+    // matrix-free application (k_line_apply): y = A u over the rows, u from global row u_row0
+    const double* u;
+    long long u_row0;
+    double* yM;
+    double* yK;
 };
 
 // L2 policies: the assembled matrices stream through L2 once (evict_first), the vertex grid
@@ -238,13 +244,19 @@ struct TileIt {
     int qs;      // Q buffer of the line: line ordinal % PFD
     int ps;      // patch buffer of the tile: tile ordinal % PFD
     int lo, hi;  // vertex planes the tile adds to the line's H ring
+    // basis columns X of u (matrix-free application): the line's columns occupy consecutive
+    // positions of a ring, column X at lpos + X - X0 (mod the ring size)
+    int X0, lpos, ulo, uhi;   // line's first column, its ring position, new columns [ulo, uhi]
 };
 
 template <int P>
-__device__ __forceinline__ void it_planes(TileIt& t) {
+__device__ __forceinline__ void it_planes(TileIt& t, int N) {
     constexpr int V = P + 2;
     t.lo = t.t0 == t.x0 ? max(0, t.x0 - P) : max(0, t.t0 - 1 - P) + V;
     t.hi = max(0, min(t.t0 + Cfg<P>::TR, t.x1) - 1 - P) + V - 1;
+    t.X0 = max(0, t.x0 - P);
+    t.ulo = t.t0 == t.x0 ? t.X0 : min(N - 1, t.t0 - 1 + P) + 1;
+    t.uhi = min(N - 1, min(t.t0 + Cfg<P>::TR, t.x1) - 1 + P);
 }
 
 template <int P>
@@ -261,8 +273,9 @@ __device__ __forceinline__ void it_init(const LineArgs& a, TileIt& t) {
     t.line = a.row_begin / a.N + blockIdx.x;
     t.qs = 0;
     t.ps = 0;
+    t.lpos = 0;
     it_line<P>(a, t);
-    it_planes<P>(t);
+    it_planes<P>(t, a.N);
 }
 
 template <int P>
@@ -270,18 +283,19 @@ __device__ __forceinline__ void it_next(const LineArgs& a, TileIt& t) {
     t.t0 += Cfg<P>::TR;
     t.ps = t.ps == Cfg<P>::PFD - 1 ? 0 : t.ps + 1;
     if (t.t0 >= t.x1) {
+        t.lpos = (t.lpos + min(a.N - 1, t.x1 - 1 + P) - t.X0 + 1) % Cfg<P>::URING;   // finished line's columns
         t.line += gridDim.x;
         t.qs = t.qs == Cfg<P>::PFD - 1 ? 0 : t.qs + 1;
         it_line<P>(a, t);
     }
-    it_planes<P>(t);
+    it_planes<P>(t, a.N);
 }
 
 // Issue (cp.async, one commit group) everything tile t reads from global memory: its new
 // vertex planes into patch buffer t.ps and, for a line's first tile, the line's y/z vertex
 // tables into Q buffer t.qs (and the thread's patch row).  An exhausted iterator commits an
 // empty group.
-template <int P>
+template <int P, int NT = Cfg<P>::NT>
 __device__ __forceinline__ void tile_issue(const LineArgs& a, double* patches, double* qbufs, const TileIt& t,
                                            PatchRow& pr, int last_line, int tid) {
     using C = Cfg<P>;
@@ -290,7 +304,7 @@ __device__ __forceinline__ void tile_issue(const LineArgs& a, double* patches, d
         if (t.t0 == t.x0) {
             patch_row_init<P>(a, pr, t.i2, t.i3, tid);
             double* Q = qbufs + t.qs * (4 * V * S);
-            for (int e = tid; e < 4 * V * S; e += C::NT) {
+            for (int e = tid; e < 4 * V * S; e += NT) {
                 const int which = e / (V * S), v = (e / S) % V, o = e % S;
                 const int r = which < 2 ? t.i2 : t.i3;
                 cp_async8(Q + e, ((which & 1) ? a.T.PK : a.T.PM) + ((size_t)r * kMaxV + v) * kMaxS + o, true);
@@ -309,6 +323,7 @@ struct TileDesc {
     int ps, qs;        // patch / Q buffers
     int pad;           // staging offset aligning the tile's first element
     long long orow0;   // output row of the tile's first row
+    int Xlo, Xhi, upos;  // apply: the tile's u columns [Xlo, Xhi], ring position of Xlo
 };
 
 template <int P>
@@ -323,6 +338,9 @@ __device__ __forceinline__ TileDesc make_desc(const LineArgs& a, const TileIt& t
     d.qs = t.qs;
     d.orow0 = (long long)t.line * a.N + t.t0 - a.row_begin;
     d.pad = padded ? 0 : (int)((d.orow0 * a.ld) & 1);
+    d.Xlo = max(0, t.t0 - P);
+    d.Xhi = t.uhi;
+    d.upos = (t.lpos + d.Xlo - t.X0) % Cfg<P>::URING;
     return d;
 }
 
@@ -340,13 +358,13 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // permuted, column 2t+i <-> vz = t + 4i, so each lane ends A1 holding exactly its A2 A-fragment
 // (TT[g][t], TT[g][t+4]): no shuffle or shared-memory round trip between the two products.
 // Padding rows / columns (o2, o3 >= S, vy, vz >= V) carry zero coefficients.
-template <int P>
+template <int P, int NT = Cfg<P>::NT, int HS = Cfg<P>::S2>
 __device__ __forceinline__ void phase_a(const LineArgs& a, const TileDesc& t, const double* patches,
                                         const double* qbufs, double* Hm, double* Hk, int tid) {
     using C = Cfg<P>;
     constexpr int V = C::V, S = C::S, S2 = C::S2, RING = C::RING;
     constexpr int KS = (V + 3) / 4;                    // k-steps of 4 (p=3: 2, p=2: 1)
-    constexpr int NW = C::NT / 32;
+    constexpr int NW = NT / 32;
     const int lane = tid & 31, warp = tid >> 5, g = lane >> 2, tq = lane & 3;
     const double* Q = qbufs + t.qs * (4 * V * S);
     double aYM[KS], aYK[KS], bZM[KS], bZK[KS];
@@ -385,8 +403,8 @@ __device__ __forceinline__ void phase_a(const LineArgs& a, const TileDesc& t, co
         const int slot = (t.lo + j) & (RING - 1);
         const int o3 = 2 * tq;
         if (g < S) {
-            double* hm = Hm + slot * S2 + g;
-            double* hk = Hk + slot * S2 + g;
+            double* hm = Hm + slot * HS + g;
+            double* hk = Hk + slot * HS + g;
             if (o3 < S) {
                 hm[S * o3] = hM0;
                 hk[S * o3] = hK0;
@@ -546,6 +564,187 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const __grid_const
     if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// ---------------------------------------------------------------------------------------------
+// Matrix-free application y = A u on the GRID line structure.
+//
+// Row i of M is sum_vx PMx[vx][o1] HM[bx+vx][o2,o3] (the assembly's phase B), so
+//   y^M_i = sum_{vx,o1} PMx[vx][o1] D_M(bx+vx, i1-p+o1),   D_X(c, X) = sum_{o2,o3} H_X[c][o2,o3] u[X][i2-p+o2][i3-p+o3]
+//   y^K_i = sum_{vx,o1} PKx[vx][o1] D_M(..) + PMx[vx][o1] D_K(..)
+// — the definition y_i = sum_j A_ij u_j with the sums reordered.  Per tile of TR rows the D
+// values for all (vertex plane c, column X) of the tile's window are one (16 x 49) x (49 x 16)
+// product per matrix on the FP64 tensor cores (8 DMMA m8n8k4 items of 13 k-steps, one or two
+// per warp); the H planes come from the assembly's phase A, the u columns X (49 values each)
+// are prefetched with the vertex patches into a ring.  Nothing is stored but y.
+template <int P, int MODE>
+__global__ void __launch_bounds__(256, 3) k_line_apply(const __grid_constant__ LineArgs a) {
+    using C = Cfg<P>;
+    constexpr int S = C::S, S2 = C::S2, V = C::V, RING = C::RING, URING = C::URING, PFD = C::PFD;
+    // 8 warps: one D item, one phase-A plane and one output row each per tile
+    constexpr int NT = 256;
+    constexpr int HS = (S2 + 3) / 4 * 4 + ((S2 + 3) / 4 % 2 == 0 ? 4 : 0);   // row stride = 4 (mod 8): conflict-free fragments
+    extern __shared__ __align__(128) double sm[];
+    double* Hm = sm;                                      // [RING][HS]
+    double* Hk = Hm + RING * HS;
+    double* qbufs = Hk + RING * HS;                       // [PFD][4][V][S]
+    double* patches = qbufs + PFD * 4 * V * S;            // [PFD][W][V][V]
+    double* xbt = patches + PFD * C::PATCH;               // [4P][2][V][S]
+    double* U = xbt + C::XB;                              // [URING][HS]
+    double* Dm = U + URING * HS;                          // [16][16]  D_M(c - b0, X - Xlo)
+    double* Dk = Dm + 256;
+    double* pint = Dk + 256;                              // [2][V][S]: interior P^ (h, 1/h folded)
+    __shared__ TileDesc desc[8];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n = a.n, N = a.N;
+    const int last_line = (a.row_end - 1) / N;
+    for (int e = tid; e < C::XB; e += NT) {
+        const int i = e / (2 * V * S), rem = e % (2 * V * S), kind = rem / (V * S), v = (rem / S) % V, o = rem % S;
+        const int r = i < 2 * P ? i : n - P + (i - 2 * P);
+        xbt[e] = (kind ? a.T.PK : a.T.PM)[((size_t)r * kMaxV + v) * kMaxS + o];
+    }
+    for (int e = tid; e < 2 * V * S; e += NT) pint[e] = e < V * S ? a.PMh[e / S][e % S] : a.PKi[(e - V * S) / S][e % S];
+    auto issue = [&](const TileIt& t, PatchRow& pr) {
+        if (t.line <= last_line) {
+            const long long N2 = (long long)N * N;
+            for (int e = tid; e < (t.uhi - t.ulo + 1) * S2; e += NT) {
+                const int X = t.ulo + e / S2, o23 = e % S2, o2 = o23 % S, o3 = o23 / S;
+                const int iy = t.i2 - P + o2, iz = t.i3 - P + o3;
+                const bool ok = iy >= 0 && iy < N && iz >= 0 && iz < N;
+                const long long g = ok ? (long long)iz * N2 + (long long)iy * N + X - a.u_row0 : 0;
+                cp_async8(U + ((t.lpos + X - t.X0) % URING) * HS + o23, a.u + g, ok);
+            }
+        }
+        tile_issue<P, NT>(a, patches, qbufs, t, pr, last_line, tid);     // commits the group
+    };
+    TileIt itP;
+    PatchRow prow;
+    prow.base = nullptr;
+    it_init<P>(a, itP);
+    for (int k = 0; k < PFD; ++k) {
+        issue(itP, prow);
+        if (tid == 0) desc[k] = make_desc<P>(a, itP, last_line, false);
+        if (itP.line <= last_line) it_next<P>(a, itP);
+    }
+    cp_async_wait<PFD - 1>();
+    __syncthreads();
+    {
+        const TileDesc d0 = desc[0];
+        if (d0.line >= 0) phase_a<P, NT, HS>(a, d0, patches, qbufs, Hm, Hk, tid);
+    }
+    cp_async_wait<PFD - 2>();
+    __syncthreads();
+    const int g = lane >> 2, t4 = lane & 3;
+    // lane-resident interior x-row coefficients of the final contraction: pairs q = lane, lane+32
+    int qv[2], qo[2];
+    double qm[2], qk[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int q = min(lane + 32 * h, V * S - 1);
+        qv[h] = q / S;
+        qo[h] = q % S;
+        qm[h] = a.PMh[qv[h]][qo[h]];
+        qk[h] = a.PKi[qv[h]][qo[h]];
+    }
+    for (int k = 0;; ++k) {
+        const TileDesc d = desc[k & 7];
+        if (d.line < 0) break;
+        const TileDesc dA = desc[(k + 1) & 7];
+        const int b0 = max(0, d.t0 - P);
+        const int hi_plane = max(0, d.t0 + d.tr - 1 - P) + V - 1;
+        // ---- S1a: D_X = H_X (planes b0..) x U (columns Xlo..) on the tensor cores ----------
+        {
+            const int kind = warp >> 2, mt = (warp >> 1) & 1, nt = warp & 1;
+            const double* H = kind ? Hk : Hm;
+            const int c = b0 + 8 * mt + g, X = d.Xlo + 8 * nt + g;
+            const bool cv = c <= hi_plane, xv = X <= d.Xhi;
+            const double* hrow = H + (c & (RING - 1)) * HS;
+            const double* urow = U + ((d.upos + 8 * nt + g) % URING) * HS;
+            double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;     // two chains: even / odd k-steps
+#pragma unroll
+            for (int s = 0; s < (S2 + 3) / 4; ++s) {
+                const int o = 4 * s + t4;
+                const double av = (cv && o < S2) ? hrow[o] : 0.0;
+                const double bv = (xv && o < S2) ? urow[o] : 0.0;
+                if (s & 1) dmma(e0, e1, av, bv);
+                else dmma(d0, d1, av, bv);
+            }
+            double* D = kind ? Dk : Dm;
+            D[(8 * mt + g) * 16 + 8 * nt + 2 * t4] = d0 + e0;
+            D[(8 * mt + g) * 16 + 8 * nt + 2 * t4 + 1] = d1 + e1;
+        }
+        __syncthreads();
+        // ---- S1b: rows of tile k (one per warp), phase A of tile k+1, prefetch tile k+PFD ----
+        {                                                  // warp j finishes row t0 + j
+            const int j = warp;
+            double ym = 0.0, yk = 0.0;
+            if (j < d.tr) {
+                const int r = d.t0 + j;
+                if (r >= 2 * P && r <= n - 1 - P && d.t0 >= P) {
+                    // interior row: b_r - b0 = j, X - Xlo = j + o1; lane-resident P^ coefficients
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        if (h == 1 && lane + 32 >= V * S) break;
+                        const int di = (j + qv[h]) * 16 + j + qo[h];
+                        const double dm = Dm[di];
+                        ym = fma(qm[h], dm, ym);
+                        yk = fma(qk[h], dm, yk);
+                        yk = fma(qm[h], Dk[di], yk);
+                    }
+                } else {
+                    const int br = max(0, r - P);
+                    const bool interior = r >= 2 * P && r <= n - 1 - P;
+                    const double* pm = interior ? pint : xbt + (r < 2 * P ? r : 2 * P + (r - (n - P))) * (2 * V * S);
+                    for (int q = lane; q < V * S; q += 32) {
+                        const int vx = q / S, o1 = q % S;
+                        const int X = r - P + o1;
+                        if (X < 0 || X >= N) continue;
+                        const int di = (br + vx - b0) * 16 + (X - d.Xlo);
+                        const double dm = Dm[di];
+                        const double cm = pm[vx * S + o1];
+                        ym = fma(cm, dm, ym);
+                        yk = fma(pm[V * S + vx * S + o1], dm, yk);
+                        yk = fma(cm, Dk[di], yk);
+                    }
+                }
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                ym += __shfl_xor_sync(0xffffffffu, ym, off);
+                yk += __shfl_xor_sync(0xffffffffu, yk, off);
+            }
+            if (lane == 0 && j < d.tr) {
+                if (MODE & 1) a.yM[d.orow0 + j] = ym;
+                if (MODE & 2) a.yK[d.orow0 + j] = yk;
+            }
+        }
+        if (dA.line >= 0) phase_a<P, NT, HS>(a, dA, patches, qbufs, Hm, Hk, tid);
+        issue(itP, prow);                                            // tile k+PFD
+        if (tid == 0) desc[(k + PFD) & 7] = make_desc<P>(a, itP, last_line, false);
+        if (itP.line <= last_line) it_next<P>(a, itP);
+        cp_async_wait<PFD - 2>();                                    // tile k+2 landed
+        __syncthreads();
+    }
+    cp_async_wait<0>();
+}
+
+template <int P, int MODE>
+int launch_apply_p(const LineArgs& a, cudaStream_t st) {
+    using C = Cfg<P>;
+    constexpr int HS = (C::S2 + 3) / 4 * 4 + ((C::S2 + 3) / 4 % 2 == 0 ? 4 : 0);
+    const size_t smem = (size_t)(2 * C::RING * HS + C::PFD * 4 * C::V * C::S + C::PFD * C::PATCH + C::XB +
+                                 C::URING * HS + 512 + 2 * C::V * C::S) * sizeof(double);
+    auto kern = k_line_apply<P, MODE>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return WGQ_ECUDA;
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
+    const int64_t lines = (a.row_end - 1) / a.N - a.row_begin / a.N + 1;
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(lines, (int64_t)sms * std::max(per_sm, 1)));
+    kern<<<(unsigned)blocks, 256, smem, st>>>(a);
+    return cudaGetLastError() == cudaSuccess ? WGQ_OK : WGQ_ECUDA;
+}
+
 template <int P, int MODE>
 int launch_line_p(const LineArgs& a, cudaStream_t st) {
     using C = Cfg<P>;
@@ -618,6 +817,42 @@ int launch_line(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, 
     if (a.row_end <= a.row_begin) return WGQ_OK;
     cudaStream_t st = (cudaStream_t)stream;
     return R->p == 3 ? launch_line_mode<3>(a, mode, st) : launch_line_mode<2>(a, mode, st);
+}
+
+bool line_apply_applies(const wgq_rules_s* R, const wgq_coeff_t* c) {
+    return c->kind == WGQ_COEF_GRID && R->dim == 3 && R->n >= R->p + 1;
+}
+
+int launch_line_apply(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, const double* u,
+                      int64_t u_row0, int64_t row_begin, int64_t row_end, double* yM, double* yK, void* stream) {
+    if (row_end <= row_begin) return WGQ_OK;
+    LineArgs a{};
+    a.T = T;
+    a.grid = c->grid;
+    a.plane0 = (int)c->grid_plane0;
+    a.planes = (int)c->grid_planes;
+    a.n = (int)R->n;
+    a.N = (int)R->N;
+    a.row_begin = (int)row_begin;
+    a.row_end = (int)row_end;
+    a.ld = 0;
+    a.h = 1.0 / (double)R->n;
+    a.inv_h = (double)R->n;
+    double PM[kMaxV][kMaxS], PK[kMaxV][kMaxS];
+    interior_vertex_tables(R->p, R->rules[WGQ_MASS][R->p], R->rules[WGQ_STIFFNESS][R->p], PM, PK);
+    for (int v = 0; v < kMaxV; ++v)
+        for (int o1 = 0; o1 < kMaxS; ++o1) {
+            a.PMh[v][o1] = PM[v][o1] * a.h;
+            a.PKi[v][o1] = PK[v][o1] * a.inv_h;
+        }
+    a.u = u;
+    a.u_row0 = u_row0;
+    a.yM = yM;
+    a.yK = yK;
+    const int mode = (yM ? 1 : 0) | (yK ? 2 : 0);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (R->p == 3) return mode == 3 ? launch_apply_p<3, 3>(a, st) : (mode == 1 ? launch_apply_p<3, 1>(a, st) : launch_apply_p<3, 2>(a, st));
+    return mode == 3 ? launch_apply_p<2, 3>(a, st) : (mode == 1 ? launch_apply_p<2, 1>(a, st) : launch_apply_p<2, 2>(a, st));
 }
 
 }  // namespace wgq
