@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ld", type=int, default=None)
+    ap.add_argument("--no-extras", action="store_true", help="skip the secondary measurements (other configs, operators)")
     return ap.parse_args()
 
 
@@ -298,6 +299,12 @@ def main():
     if not args.no_e2e:
         e2e = run_e2e(args, cfg, rules, row_begin, row_end, ld, world, rank, local, nnz_all)
 
+    extras = None
+    if rank == 0 and world == 1 and not args.no_extras:
+        del out
+        torch.cuda.empty_cache()
+        extras = run_extras(rules, coef, peak)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         v, sample, cores, el = run_oracle(cfg, args.cpu_seconds)
@@ -313,10 +320,58 @@ def main():
                            "layout": "ELL", "parallelism": f"z-slab x{world}",
                            "l2": "flushed (512 MB write) between timed steps; outputs >> L2"},
                 "gpu_launches": args.steps * 1,
-                "roofline": roof, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu}
+                "roofline": roof, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu, "extras": extras}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def _time_ms(fn, reps=5, flush=None):
+    """Median device time (CUDA events on the current stream) of fn(), L2 flushed before each."""
+    import torch
+    fn()
+    ts = []
+    for _ in range(reps):
+        if flush is not None:
+            flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return float(np.median(ts))
+
+
+def run_extras(rules5, coef5, peak):
+    """Secondary measurements (not the headline): the other BASELINE configs' assembly (parity
+    cases; their kernels differ: separable, 2D tensor-core FOURIER) against the same HBM
+    roofline, and the SURVEY §8(f) operators at C5 — load vector and matrix-free y = M u, K u."""
+    import torch
+
+    from paper_1710_01048_b200 import api, wgq
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")
+    out = {"configs": {}, "operators": {}}
+    for name in ("C1", "C2", "C3", "C4"):
+        cfg = inputs.config(name)
+        r = wgq.Rules(cfg["p"], cfg["n"], cfg["dim"])
+        c = api.coefficient(inputs.coefficient(cfg["coeff"], cfg["dim"]))
+        o = {k: api.alloc_ell(r, 0, r.n_rows) for k in cfg["kinds"]}
+        ms = _time_ms(lambda: api.assemble(r, c, cfg["kinds"], out=o), flush=flush)
+        alg = r.n_rows * r.stencil * 8 * len(cfg["kinds"])
+        nnz = wgq.wgq_nnz(r, 0, r.n_rows) * len(cfg["kinds"])
+        out["configs"][cfg["name"]] = {"ms": round(ms, 4), "nnz_per_s": nnz / (ms / 1e3),
+                                       "hbm_gbs": round(alg / ms / 1e6, 1), "hbm_frac": round(alg / ms / 1e6 / peak, 4)}
+        del o
+    n_rows = rules5.n_rows
+    b = torch.empty(n_rows, dtype=torch.float64, device="cuda")
+    ms = _time_ms(lambda: api.assemble_load(rules5, coef5, out=b), flush=flush)
+    out["operators"]["load_vector_C5"] = {"ms": round(ms, 4), "rows_per_s": n_rows / (ms / 1e3)}
+    u = torch.randn(n_rows, dtype=torch.float64, device="cuda")
+    ms = _time_ms(lambda: api.apply(rules5, coef5, u), flush=flush)
+    out["operators"]["apply_MK_C5"] = {"ms": round(ms, 4), "rows_per_s": n_rows / (ms / 1e3),
+                                       "note": "matrix-free y_M = M u and y_K = K u, nothing stored"}
+    return out
 
 
 def run_e2e(args, cfg, rules, row_begin, row_end, ld, world, rank, local, nnz_all):
