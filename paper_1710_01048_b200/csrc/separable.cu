@@ -87,11 +87,45 @@ __device__ __forceinline__ int csr_pos(const int* o, const int64_t* idx, int64_t
     return pos;
 }
 
+// The value formulas, shared by both kernels so that ELL and CSR values are bitwise equal.
+// y/z (line) constants of a slot: P = uM2 uM3, Q = vM2 vM3, PK = uK2 uM3 + uM2 uK3, QK likewise.
+template <int D>
+__device__ __forceinline__ void sep_consts(const double* f2, const double* f3, double& P, double& Q, double& PK,
+                                           double& QK) {
+    // f = {uM, vM, uK, vK} of direction 2 / 3 at the slot's offset
+    if (D == 1) {
+        P = Q = 1.0;
+        PK = QK = 0.0;
+    } else if (D == 2) {
+        P = f2[0];
+        Q = f2[1];
+        PK = f2[2];
+        QK = f2[3];
+    } else {
+        P = f2[0] * f3[0];
+        Q = f2[1] * f3[1];
+        PK = fma(f2[2], f3[0], f2[0] * f3[2]);
+        QK = fma(f2[3], f3[1], f2[1] * f3[3]);
+    }
+}
+
+__device__ __forceinline__ double sep_mass(double c0, double amp, double uM1, double vM1, double P, double Q) {
+    return fma(amp, vM1 * Q, c0 * (uM1 * P)) + 0.0;
+}
+
+template <int D>
+__device__ __forceinline__ double sep_stiff(double c0, double amp, double uM1, double vM1, double uK1, double vK1,
+                                            double P, double Q, double PK, double QK) {
+    const double su = D >= 2 ? fma(uK1, P, uM1 * PK) : uK1;
+    const double sv = D >= 2 ? fma(vK1, Q, vM1 * QK) : vK1;
+    return fma(amp, sv, c0 * su) + 0.0;
+}
+
 constexpr int kChunkRows = 32;
 
-template <int P, int D, int MODE>
+template <int P_, int D, int MODE>
 __global__ void __launch_bounds__(256) k_sep(const SepArgs a) {
-    constexpr int S = 2 * P + 1;
+    constexpr int S = 2 * P_ + 1;
     constexpr int NS = D == 1 ? S : (D == 2 ? S * S : S * S * S);
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -113,45 +147,25 @@ __global__ void __launch_bounds__(256) k_sep(const SepArgs a) {
         }
         while (rl < nrows) {
             const int o[3] = {slot % S, (slot / S) % S, slot / (S * S)};
-            double uM[3], vM[3], uK[3], vK[3];
+            double f[3][4];
 #pragma unroll
             for (int q = 0; q < D; ++q) {
                 const double* t = a.sep + ((int64_t)q * a.N + idx[q]) * 4 * kMaxS + o[q];
-                uM[q] = __ldg(t);
-                vM[q] = __ldg(t + kMaxS);
-                if (MODE & 2) {
-                    uK[q] = __ldg(t + 2 * kMaxS);
-                    vK[q] = __ldg(t + 3 * kMaxS);
-                }
+#pragma unroll
+                for (int c = 0; c < 4; ++c) f[q][c] = (c < 2 || (MODE & 2)) ? __ldg(t + c * kMaxS) : 0.0;
             }
+            double P, Q, PK, QK;
+            sep_consts<D>(f[D >= 2 ? 1 : 0], f[D >= 3 ? 2 : 0], P, Q, PK, QK);
             const int64_t row = first + rl - a.row_begin;
             int cpos = 0;
-            if (a.layout == WGQ_CSR) cpos = csr_pos<P, D>(o, idx, a.N);
+            if (a.layout == WGQ_CSR) cpos = csr_pos<P_, D>(o, idx, a.N);
             if (MODE & 1) {
-                double pu = uM[0], pv = vM[0];
-#pragma unroll
-                for (int q = 1; q < D; ++q) {
-                    pu *= uM[q];
-                    pv *= vM[q];
-                }
-                const double m = fma(a.amp, pv, a.c0 * pu) + 0.0;
+                const double m = sep_mass(a.c0, a.amp, f[0][0], f[0][1], P, Q);
                 if (a.layout == WGQ_ELL) a.Mv[row * a.ldM + slot] = m;
                 else if (cpos >= 0) a.Mv[a.rpM[row] + cpos] = m;
             }
             if (MODE & 2) {
-                double su = 0.0, sv = 0.0;
-#pragma unroll
-                for (int t = 0; t < D; ++t) {
-                    double pu = 1.0, pv = 1.0;
-#pragma unroll
-                    for (int q = 0; q < D; ++q) {
-                        pu *= q == t ? uK[q] : uM[q];
-                        pv *= q == t ? vK[q] : vM[q];
-                    }
-                    su += pu;
-                    sv += pv;
-                }
-                const double k = fma(a.amp, sv, a.c0 * su) + 0.0;
+                const double k = sep_stiff<D>(a.c0, a.amp, f[0][0], f[0][1], f[0][2], f[0][3], P, Q, PK, QK);
                 if (a.layout == WGQ_ELL) a.Kv[row * a.ldK + slot] = k;
                 else if (cpos >= 0) a.Kv[a.rpK[row] + cpos] = k;
             }
@@ -172,6 +186,67 @@ __global__ void __launch_bounds__(256) k_sep(const SepArgs a) {
     }
 }
 
+// ELL fast variant (s^d <= 128): a warp walks a segment of one x-line.  Lane l owns the
+// slots l + 32 j of every row (j < R); the y/z factors of those slots are line constants kept
+// in registers (P = uM2 uM3, Q = vM2 vM3 and the stiffness combinations PK, QK), so a row
+// costs each lane the four x-factors of its slots, a few FMAs and coalesced 256-byte stores.
+constexpr int kSepSeg = 32;
+
+template <int P, int D, int MODE>
+__global__ void __launch_bounds__(256) k_sep_line(const SepArgs a) {
+    constexpr int S = 2 * P + 1;
+    constexpr int NS = D == 1 ? S : (D == 2 ? S * S : S * S * S);
+    constexpr int R = (NS + 31) / 32;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t N = a.N;
+    const int64_t segs = (N + kSepSeg - 1) / kSepSeg;
+    const int64_t line0 = a.row_begin / N, line1 = (a.row_end - 1) / N;
+    const int64_t items = (line1 - line0 + 1) * segs;
+    int o1[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) o1[j] = (lane + 32 * j) % S;
+    for (int64_t it = warp; it < items; it += nwarps) {
+        const int64_t line = line0 + it / segs;
+        const int64_t x0 = max((it % segs) * kSepSeg, a.row_begin - line * N);
+        const int64_t x1 = min((it % segs) * kSepSeg + kSepSeg, min(N, a.row_end - line * N));
+        if (x0 >= x1) continue;
+        const int64_t i2 = D >= 2 ? line % N : 0, i3 = D >= 3 ? line / N : 0;
+        // line constants per owned slot
+        double cP[R], cQ[R], cPK[R], cQK[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+            const int slot = min(lane + 32 * j, NS - 1);
+            const int o23 = slot / S, o2 = o23 % S, o3 = o23 / S;
+            double f2[4], f3[4];
+            const double* t2 = a.sep + ((int64_t)1 * N + i2) * 4 * kMaxS + o2;
+            const double* t3 = a.sep + ((int64_t)2 * N + i3) * 4 * kMaxS + o3;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                f2[c] = __ldg(t2 + c * kMaxS);
+                f3[c] = D >= 3 ? __ldg(t3 + c * kMaxS) : 0.0;
+            }
+            sep_consts<D>(f2, f3, cP[j], cQ[j], cPK[j], cQK[j]);
+        }
+        for (int64_t i1 = x0; i1 < x1; ++i1) {
+            const int64_t orow = line * N + i1 - a.row_begin;
+            const double* t1 = a.sep + i1 * 4 * kMaxS;
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+                const int slot = lane + 32 * j;
+                if (slot >= NS) continue;
+                const double uM1 = __ldg(t1 + o1[j]), vM1 = __ldg(t1 + kMaxS + o1[j]);
+                if (MODE & 1) a.Mv[orow * a.ldM + slot] = sep_mass(a.c0, a.amp, uM1, vM1, cP[j], cQ[j]);
+                if (MODE & 2) {
+                    const double uK1 = __ldg(t1 + 2 * kMaxS + o1[j]), vK1 = __ldg(t1 + 3 * kMaxS + o1[j]);
+                    a.Kv[orow * a.ldK + slot] = sep_stiff<D>(a.c0, a.amp, uM1, vM1, uK1, vK1, cP[j], cQ[j], cPK[j], cQK[j]);
+                }
+            }
+        }
+    }
+}
+
 template <int P, int D>
 int launch_sep_pd(const SepArgs& a, int mode, cudaStream_t st) {
     int dev = 0, sms = 148;
@@ -182,6 +257,18 @@ int launch_sep_pd(const SepArgs& a, int mode, cudaStream_t st) {
     int64_t blocks = (chunks + 7) / 8;
     blocks = std::min<int64_t>(blocks, (int64_t)sms * 16);
     blocks = std::max<int64_t>(blocks, 1);
+    constexpr int NS = D == 1 ? 2 * P + 1 : (D == 2 ? (2 * P + 1) * (2 * P + 1) : (2 * P + 1) * (2 * P + 1) * (2 * P + 1));
+    if constexpr (NS <= 128 && D == 3) {
+      if (a.layout == WGQ_ELL) {
+        const int64_t segs = (a.N + kSepSeg - 1) / kSepSeg;
+        const int64_t items = ((a.row_end - 1) / a.N - a.row_begin / a.N + 1) * segs;
+        int64_t b2 = std::max<int64_t>(1, std::min<int64_t>((items + 7) / 8, (int64_t)sms * 16));
+        if (mode == 3) k_sep_line<P, D, 3><<<(unsigned)b2, 256, 0, st>>>(a);
+        else if (mode == 1) k_sep_line<P, D, 1><<<(unsigned)b2, 256, 0, st>>>(a);
+        else k_sep_line<P, D, 2><<<(unsigned)b2, 256, 0, st>>>(a);
+        return cudaGetLastError() == cudaSuccess ? WGQ_OK : WGQ_ECUDA;
+      }
+    }
     if (mode == 3) k_sep<P, D, 3><<<(unsigned)blocks, 256, 0, st>>>(a);
     else if (mode == 1) k_sep<P, D, 1><<<(unsigned)blocks, 256, 0, st>>>(a);
     else k_sep<P, D, 2><<<(unsigned)blocks, 256, 0, st>>>(a);
