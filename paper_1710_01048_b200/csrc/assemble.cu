@@ -441,6 +441,29 @@ __global__ void __launch_bounds__(256) k_fourier2d(const GenericArgs a) {
             }
             // ---- store: lane holds (o1 = g, o2 = 2t + i) ---------------------------------------
             const int64_t orow = orow0 + i1;
+            if (a.apply) {
+                // matrix-free: y_i = sum over the lane's two columns of A_ij u_j, warp-reduced
+                double pm = 0.0, pk = 0.0;
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const int o2 = 2 * t + i;
+                    const int j1 = i1 + g - P, j2 = i2 + o2 - P;
+                    if (g >= S || o2 >= S || j1 < 0 || j1 >= N || j2 < 0 || j2 >= N) continue;
+                    const double uj = __ldg(a.u + ((int64_t)j2 * N + j1 - a.u_row0));
+                    pm = fma(i ? m1 : m0, uj, pm);
+                    pk = fma(i ? k1 : k0, uj, pk);
+                }
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) {
+                    pm += __shfl_xor_sync(0xffffffffu, pm, off);
+                    pk += __shfl_xor_sync(0xffffffffu, pk, off);
+                }
+                if (lane == 0) {
+                    if (MODE & 1) a.yM[orow] = pm;
+                    if (MODE & 2) a.yK[orow] = pk;
+                }
+                continue;
+            }
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
                 const int o2 = 2 * t + i;
@@ -629,12 +652,80 @@ __global__ void __launch_bounds__(256) k_load(const GenericArgs a, const double*
     }
 }
 
+// GRID load vector on the line structure (D = 2, 3): a warp takes 32 consecutive rows of one
+// x-line; lane l first forms G[c] = sum_{vy,vz} g[bz+vz][by+vy][c] PWy[vy] PWz[vz] for the
+// vertex planes c = c0 + l (+32) of the segment (coalesced loads along x), then row i1 = x0 + l
+// gathers b = sum_vx PWx[i1][vx] G[bx+vx] from its neighbours' registers (warp shuffles).
+template <int P, int D>
+__global__ void __launch_bounds__(256) k_load_grid_line(const GenericArgs a, const double* PW, double* b) {
+    constexpr int V = P + 2;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t N = a.N, nv = a.n + 1;
+    const int64_t segs = (N + 31) / 32;
+    const int64_t line0 = a.row_begin / N, line1 = (a.row_end - 1) / N;
+    const int64_t items = (line1 - line0 + 1) * segs;
+    for (int64_t it = warp; it < items; it += nwarps) {
+        const int64_t line = line0 + it / segs;
+        const int64_t x0 = (it % segs) * 32;
+        const int64_t i2 = line % N, i3 = D >= 3 ? line / N : 0;
+        const int64_t by = max((int64_t)0, i2 - P), bz = max((int64_t)0, i3 - P);
+        const int64_t c0 = max((int64_t)0, x0 - P);
+        double G[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int64_t c = c0 + lane + 32 * h;
+            double acc = 0.0;
+            if (c <= a.n && (h == 0 || lane < V - 1)) {      // the segment's planes c0 .. c0+31+V-1
+                for (int vz = 0; vz < (D >= 3 ? V : 1); ++vz) {
+                    const int64_t z = bz + vz;
+                    const double wz = D >= 3 ? PW[i3 * kMaxV + vz] : 1.0;
+                    if (D >= 3 && (wz == 0.0 || z > a.n)) continue;
+                    double sy = 0.0;
+#pragma unroll
+                    for (int vy = 0; vy < V; ++vy) {
+                        const int64_t y = by + vy;
+                        const double wy = PW[i2 * kMaxV + vy];
+                        if (wy == 0.0 || y > a.n) continue;
+                        const double* g = D >= 3 ? a.coef.grid + ((z - a.coef.plane0) * nv + y) * nv + c
+                                                 : a.coef.grid + (y - a.coef.plane0) * nv + c;
+                        sy = fma(wy, __ldg(g), sy);
+                    }
+                    acc = fma(wz, sy, acc);
+                }
+            }
+            G[h] = acc;
+        }
+        const int64_t i1 = x0 + lane;
+        const int64_t row = line * N + i1;
+        const bool mine = i1 < N && row >= a.row_begin && row < a.row_end;
+        const int64_t bx = max((int64_t)0, i1 - P);
+        double acc = 0.0;
+#pragma unroll
+        for (int vx = 0; vx < V; ++vx) {
+            const int src = (int)(bx + vx - c0);                       // 0 .. 35
+            const double g0 = __shfl_sync(0xffffffffu, G[0], src & 31);
+            const double g1 = __shfl_sync(0xffffffffu, G[1], src & 31);
+            const double wx = mine ? PW[i1 * kMaxV + vx] : 0.0;
+            acc = fma(wx, src < 32 ? g0 : g1, acc);
+        }
+        if (mine) b[row - a.row_begin] = acc;
+    }
+}
+
 template <int P, int D>
 int launch_load_pd(const GenericArgs& a, const double* PW, double* b, cudaStream_t st) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t rows = a.row_end - a.row_begin;
+    if (D >= 2 && a.coef.kind == WGQ_COEF_GRID) {
+        const int64_t items = ((a.row_end - 1) / a.N - a.row_begin / a.N + 1) * ((a.N + 31) / 32);
+        const int64_t b2 = std::max<int64_t>(1, std::min<int64_t>((items + 7) / 8, (int64_t)sms * 16));
+        k_load_grid_line<P, D><<<(unsigned)b2, 256, 0, st>>>(a, PW, b);
+        return cudaGetLastError() == cudaSuccess ? WGQ_OK : WGQ_ECUDA;
+    }
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((rows + 255) / 256, (int64_t)sms * 16));
     k_load<P, D><<<(unsigned)blocks, 256, 0, st>>>(a, PW, b);
     return cudaGetLastError() == cudaSuccess ? WGQ_OK : WGQ_ECUDA;
@@ -820,6 +911,19 @@ int launch_apply(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c,
     double* tab = nullptr;
     int rc = coef_tables(R, T, a, c, st, &tab);
     if (rc != WGQ_OK) return rc;
+    if (!force_generic && R->dim == 2 && c->kind == WGQ_COEF_FOURIER_LOGN && a.coef.n_modes > 0) {
+        // tensor-core rows, then the generic kernel over the shell rows (as for the assembly)
+        rc = R->p == 3 ? launch_fourier2d_p<3>(a, st) : launch_fourier2d_p<2>(a, st);
+        const int64_t* shell = nullptr;
+        int64_t nshell = 0;
+        if (rc == WGQ_OK) rc = shell_rows_2d(const_cast<wgq_rules_s*>(R), row_begin, row_end, &shell, &nshell);
+        if (rc != WGQ_OK || nshell == 0) {
+            cudaFreeAsync(tab, st);
+            return rc;
+        }
+        a.rows_list = shell;
+        a.nlist = nshell;
+    }
     rc = WGQ_EUNSUPPORTED;
     switch (R->p * 10 + R->dim) {
         case 21: rc = launch_generic_pd<2, 1>(a, T.maxM, T.maxK, st); break;
