@@ -37,6 +37,16 @@ def _worker(rank, world, port, p, n, dim, q):
         got, lo = wdist.exchange_halo(owned, p, n, N, dim)
         lo2, hi2 = wdist.needed_vertex_planes(p, n, N, dim, rank, world)
         ok_halo = lo == lo2 and torch.equal(got, full[lo2:hi2 + 1])
+        # u halo for the matrix-free product: own planes +- p from the neighbours
+        u_full = torch.arange(N ** dim, dtype=torch.float64) * 0.5 + 3.0
+        b, e = api.slab_rows(N, dim, rank, world)
+        u_ext, u0 = wdist.exchange_u_halo(u_full[b:e].clone(), p, N, dim)
+        plane_rows = N ** (dim - 1)
+        ulo, uhi = wdist.needed_u_planes(p, N, dim, rank, world)
+        ok_u = (u0 == ulo * plane_rows and torch.equal(u_ext, u_full[ulo * plane_rows:uhi * plane_rows])
+                and (e <= b or (u0 <= max(0, b // plane_rows - p) * plane_rows
+                                and u0 + u_ext.numel() >= min(N, (e - 1) // plane_rows + p + 1) * plane_rows)))
+        ok_halo = ok_halo and ok_u
         # reductions: hash wraps mod 2^64, sums add
         local = torch.zeros(3, dtype=torch.float64)
         local[0:1].view(torch.int64)[0] = (2 ** 63 - 5) if rank == 0 else 11
