@@ -116,3 +116,24 @@ def test_library_rules_match_paper_and_oracle(L):
                     if cls == p and (kind, p) in paper:
                         pt, po = paper[(kind, p)]
                         assert np.allclose(tau[:len(pt)], pt, atol=1e-14) and np.allclose(om[:len(po)], po, atol=1e-14)
+
+
+def test_operator_argument_errors(L):
+    """wgq_assemble_load / wgq_apply validate before any device work (no GPU needed)."""
+    r = wgq.Rules(3, 6, 3)
+    c = wgq.make_coeff({"kind": "const", "c0": 1.0})
+    assert L.wgq_assemble_load(r.handle, ctypes.byref(c), 0, 10, None, None) == wgq.WGQ_EINVAL
+    assert L.wgq_assemble_load(r.handle, ctypes.byref(c), 5, 4, 8, None) == wgq.WGQ_EINVAL
+    assert L.wgq_assemble_load(r.handle, ctypes.byref(c), 0, r.n_rows + 1, 8, None) == wgq.WGQ_EINVAL
+    assert L.wgq_assemble_load(r.handle, ctypes.byref(c), 3, 3, None, None) == wgq.WGQ_OK      # empty range
+    N = r.N
+    z0, z1 = 4, 6                                              # rows of planes 4, 5: need u planes 1..8
+    rb, re_ = z0 * N * N, z1 * N * N
+    # no outputs / no u
+    assert L.wgq_apply(r.handle, ctypes.byref(c), 8, 0, r.n_rows, rb, re_, None, None, None) == wgq.WGQ_EINVAL
+    assert L.wgq_apply(r.handle, ctypes.byref(c), None, 0, r.n_rows, rb, re_, 8, None, None) == wgq.WGQ_EINVAL
+    # u must cover planes z0-p .. z1+p-1 (clipped): one plane short on either side is an error
+    lo, hi = (z0 - 3) * N * N, min(N, z1 + 3) * N * N
+    assert L.wgq_apply(r.handle, ctypes.byref(c), 8, lo + N * N, hi - lo - N * N, rb, re_, 8, None, None) == wgq.WGQ_ERANGE
+    assert L.wgq_apply(r.handle, ctypes.byref(c), 8, lo, hi - lo - N * N, rb, re_, 8, None, None) == wgq.WGQ_ERANGE
+    assert L.wgq_apply(r.handle, ctypes.byref(c), 8, lo, hi - lo, 7, 7, 8, None, None) == wgq.WGQ_OK   # empty range
