@@ -136,6 +136,15 @@ int wgq_rules_info(wgq_rules_t rules, int* p, int64_t* n_elems, int* dim,
 int wgq_rules_query(wgq_rules_t rules, int cls, int kind, int* m,
                     double* tau, double* omega, double* max_residual);
 
+/* Basis-evaluation counts (experiment E3).  For the full mesh of
+ * the handle and kind = WGQ_MASS / WGQ_STIFFNESS: the number of evaluations of the 2p+1
+ * interacting functions (B resp. B') that are nonzero at the points of every row's rule where
+ * the weight B_i (B'_i) is nonzero, summed over rows (a tensor row costs the product over its
+ * directions): *gaussian for this library's weighted Gaussian rules, *newton_cotes for the
+ * knot-and-midpoint point sets of the weighted Newton-Cotes rules the paper compares against.
+ * Host only; WGQ_EINVAL for bad arguments. */
+int wgq_eval_counts(wgq_rules_t rules, int kind, int64_t* gaussian, int64_t* newton_cotes);
+
 /* Structural nonzeros of rows [row_begin, row_end) (per matrix). */
 int wgq_nnz(wgq_rules_t rules, int64_t row_begin, int64_t row_end, int64_t* nnz);
 

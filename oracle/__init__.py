@@ -23,8 +23,10 @@ the paper (``PAPER.md``, cited as ``P:<line>`` with the LaTeX equation label):
                      used only as an independent check for c == 1.
 * ``operators``   -- the load vector (eq:Load) and the matrix-free product
                      y = A u by the plain definition.
+* ``counts``      -- basis-evaluation counts of the Gaussian vs Newton-Cotes weighted
+                     schemes (experiment E3).
 
 It shares no code, tables or constants with the CUDA library.  The seeded input
 generators in ``inputs/`` are the only module both sides use.
 """
-from . import spline, quadrature, rules, coeff, assemble, elementwise, operators  # noqa: F401
+from . import spline, quadrature, rules, coeff, assemble, elementwise, operators, counts  # noqa: F401

@@ -247,6 +247,12 @@ int wgq_apply(wgq_rules_t R, const wgq_coeff_t* c, const double* u, int64_t u_ro
     return launch_apply(R, T, c, u, u_row0, row_begin, row_end, y_M, y_K, stream);
 }
 
+int wgq_eval_counts(wgq_rules_t R, int kind, int64_t* gaussian, int64_t* newton_cotes) {
+    if (!R || !gaussian || !newton_cotes || (kind != WGQ_MASS && kind != WGQ_STIFFNESS)) return WGQ_EINVAL;
+    eval_counts(R, kind, gaussian, newton_cotes);
+    return WGQ_OK;
+}
+
 int wgq_csr_structure(wgq_rules_t R, int64_t row_begin, int64_t row_end, int64_t* row_ptr, int32_t* col_idx,
                       void* stream) {
     if (!R || !row_ptr || row_begin < 0 || row_end < row_begin || row_end > ipow(R->N, R->dim)) return WGQ_EINVAL;

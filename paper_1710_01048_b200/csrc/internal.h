@@ -75,6 +75,9 @@ int build_class_rules(int p, int bnd, ClassRule out[2][kMaxP + 1]);
 void interior_vertex_tables(int p, const ClassRule& mass, const ClassRule& stiff, double PM[kMaxV][kMaxS],
                             double PK[kMaxV][kMaxS]);
 
+// Basis-evaluation counts of the Gaussian and Newton-Cotes weighted schemes (E3).
+void eval_counts(const wgq_rules_s* R, int kind, int64_t* gaussian, int64_t* newton_cotes);
+
 // tables.cu
 int build_row_tables(const wgq_rules_s* R, RowTables* T, void* stream);
 void free_row_tables(RowTables* T);

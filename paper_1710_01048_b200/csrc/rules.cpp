@@ -480,4 +480,47 @@ int build_class_rules(int p, int bnd, ClassRule out[2][kMaxP + 1]) {
     return WGQ_OK;
 }
 
+// Basis-evaluation counts (experiment E3): per 1D row, the number
+// of the 2p+1 interacting functions (mass: B, stiffness: B') that are nonzero at each point of
+// the row's rule where the weight B_r (B'_r) is nonzero — for the weighted Gaussian rules built
+// here and for the weighted Newton-Cotes point set of Calabro et al. (the knots and element
+// midpoints of supp B_r).  A tensor row costs the product over directions, so
+// the n^d mesh costs (sum_r count(r))^d.
+void eval_counts(const wgq_rules_s* R, int kind, int64_t* gaussian, int64_t* newton_cotes) {
+    const int p = R->p;
+    const int64_t n = R->n, N = R->N;
+    const int order = kind == WGQ_MASS ? 0 : 1;
+    Knots K = unit_open_knots(p, (int)n);
+    auto nonzero_at = [&](int64_t r, real x) {
+        int c = 0;
+        for (int o = -p; o <= p; ++o) {
+            const int64_t j = r + o;
+            if (j >= 0 && j < N && fabsl(bval(K, (int)j, x, order)) > 1e-12L) ++c;
+        }
+        return c;
+    };
+    int64_t g = 0, nc = 0;
+    for (int64_t r = 0; r < N; ++r) {
+        const int cls = r < p ? (int)r : (r >= n ? (int)(n + p - 1 - r) : p);
+        const ClassRule& rule = R->rules[kind][cls];
+        for (int k = 0; k < rule.m; ++k) {
+            const real tau = (real)rule.tau[k];
+            const real x = r < p ? tau : (r >= n ? (real)n - tau : (real)(r - p) + tau);
+            if (fabsl(bval(K, (int)r, x, order)) > 1e-12L) g += nonzero_at(r, x);
+        }
+        const int64_t a = std::max<int64_t>(0, r - p), b = std::min<int64_t>(n, r + 1);   // supp B_r = [a, b]
+        for (int64_t q = 2 * a; q <= 2 * b; ++q) {                  // knots (q even) and midpoints (q odd)
+            const real x = (real)q / 2.0L;
+            if (fabsl(bval(K, (int)r, x, order)) > 1e-12L) nc += nonzero_at(r, x);
+        }
+    }
+    int64_t G = 1, C = 1;
+    for (int a = 0; a < R->dim; ++a) {
+        G *= g;
+        C *= nc;
+    }
+    *gaussian = G;
+    *newton_cotes = C;
+}
+
 }  // namespace wgq

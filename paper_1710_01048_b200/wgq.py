@@ -63,6 +63,7 @@ def lib():
                                    ctypes.POINTER(c_i64), ctypes.POINTER(c_i64), ctypes.POINTER(c_int)]),
         "wgq_rules_query": (c_int, [vp, c_int, c_int, ctypes.POINTER(c_int), dp, dp, dp]),
         "wgq_nnz": (c_int, [vp, c_i64, c_i64, ctypes.POINTER(c_i64)]),
+        "wgq_eval_counts": (c_int, [vp, c_int, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),
         "wgq_assemble_mass": (c_int, [vp, ctypes.POINTER(wgq_coeff_t), ctypes.POINTER(wgq_out_t), vp]),
         "wgq_assemble_stiffness": (c_int, [vp, ctypes.POINTER(wgq_coeff_t), ctypes.POINTER(wgq_out_t), vp]),
         "wgq_assemble_mass_stiffness": (c_int, [vp, ctypes.POINTER(wgq_coeff_t), ctypes.POINTER(wgq_out_t),
@@ -87,7 +88,7 @@ def lib():
 
 def exported_symbols():
     return ["wgq_strerror", "wgq_version", "wgq_build_rules", "wgq_build_rules_ex", "wgq_free_rules",
-            "wgq_rules_info", "wgq_rules_query", "wgq_nnz", "wgq_assemble_mass", "wgq_assemble_stiffness",
+            "wgq_rules_info", "wgq_rules_query", "wgq_nnz", "wgq_eval_counts", "wgq_assemble_mass", "wgq_assemble_stiffness",
             "wgq_assemble_mass_stiffness", "wgq_csr_structure", "wgq_assemble_load", "wgq_apply",
             "wgq_generate_grid", "wgq_row_moments",
             "wgq_checksum", "wgq_assemble_host", "wgq_host_alloc", "wgq_host_free"]
@@ -147,6 +148,13 @@ def wgq_rules_query(rules, cls, kind):
     res = ctypes.c_double()
     _check("wgq_rules_query", lib().wgq_rules_query(rules.handle, cls, kind, ctypes.byref(m), tau, om, ctypes.byref(res)))
     return np.array(tau[:m.value]), np.array(om[:m.value]), res.value
+
+
+def wgq_eval_counts(rules, kind):
+    """(Gaussian, Newton-Cotes) basis-evaluation counts of the handle's mesh (E3)."""
+    g, c = ctypes.c_int64(), ctypes.c_int64()
+    _check("wgq_eval_counts", lib().wgq_eval_counts(rules.handle, kind, ctypes.byref(g), ctypes.byref(c)))
+    return g.value, c.value
 
 
 def wgq_nnz(rules, row_begin, row_end):
