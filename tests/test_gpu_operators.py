@@ -122,3 +122,38 @@ def test_load_full_size_c5_sampled_rows():
     got = b.cpu().numpy()[rows]
     check(got, ref, np.abs(ref), "C5 load")
     assert len(zs) > 3
+
+
+@pytest.mark.parametrize("name", ["C5", "C3"])
+def test_apply_full_size_sampled_rows(name):
+    """y = M u, K u at the BASELINE sizes (C5: GRID line kernel, C3: 2D tensor-core kernel) on a
+    sample of rows covering every boundary class; u is a seeded random vector."""
+    from paper_1710_01048_b200 import api, wgq
+    cfg = inputs.config(name)
+    p, n, d = cfg["p"], cfg["n"], cfg["dim"]
+    rules = wgq.Rules(p, n, d)
+    N = rules.N
+    if cfg["coeff"]["kind"] == "grid":
+        grid, plane0 = api.make_grid(rules, cfg["coeff"]["seed"], cfg["coeff"]["sigma"], 0, rules.n_rows)
+        c = api.coefficient({"kind": "grid"}, grid, plane0)
+        desc, host = {"kind": "grid"}, inputs.lognormal_grid(n, seed=cfg["coeff"]["seed"])
+    else:
+        desc, host = inputs.coefficient(cfg["coeff"], d), None
+        c = api.coefficient(desc)
+    u = np.random.default_rng(17).standard_normal(rules.n_rows)
+    y = api.apply(rules, c, torch.from_numpy(u).cuda())
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(9)
+    edge = list(range(0, 2 * p + 2)) + list(range(N - 2 * p - 2, N))
+    rows = np.array(sorted({sum(int(rng.choice(edge) if rng.random() < 0.5 else rng.integers(0, N)) * N ** a
+                                for a in range(d)) for _ in range(120)}))
+    A = oasm.assemble_rows(p, n, d, rows, desc, grid=host)
+    absA = oasm.assemble_rows(p, n, d, rows, desc, grid=host, absolute=True)
+    for kind in ("mass", "stiffness"):
+        ref, scale = [], []
+        for i, r in enumerate(rows):
+            cols = oasm.ell_columns(p, n, d, int(r))
+            ok = cols >= 0
+            ref.append(A[kind][i][ok] @ u[cols[ok]])
+            scale.append(absA[kind][i][ok] @ np.abs(u[cols[ok]]))
+        check(y[kind].cpu().numpy()[rows], np.array(ref), np.array(scale), (name, kind))
