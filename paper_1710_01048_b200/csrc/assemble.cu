@@ -678,21 +678,26 @@ __global__ void __launch_bounds__(256) k_load_grid_line(const GenericArgs a, con
             const int64_t c = c0 + lane + 32 * h;
             double acc = 0.0;
             if (c <= a.n && (h == 0 || lane < V - 1)) {      // the segment's planes c0 .. c0+31+V-1
+                // all V (x V) loads issued before the sums (fully unrolled, predicated)
+                double gv[D >= 3 ? V : 1][V];
+#pragma unroll
                 for (int vz = 0; vz < (D >= 3 ? V : 1); ++vz) {
                     const int64_t z = bz + vz;
-                    const double wz = D >= 3 ? PW[i3 * kMaxV + vz] : 1.0;
-                    if (D >= 3 && (wz == 0.0 || z > a.n)) continue;
-                    double sy = 0.0;
 #pragma unroll
                     for (int vy = 0; vy < V; ++vy) {
                         const int64_t y = by + vy;
-                        const double wy = PW[i2 * kMaxV + vy];
-                        if (wy == 0.0 || y > a.n) continue;
+                        const bool ok = y <= a.n && (D < 3 || z <= a.n);
                         const double* g = D >= 3 ? a.coef.grid + ((z - a.coef.plane0) * nv + y) * nv + c
                                                  : a.coef.grid + (y - a.coef.plane0) * nv + c;
-                        sy = fma(wy, __ldg(g), sy);
+                        gv[vz][vy] = ok ? __ldg(g) : 0.0;
                     }
-                    acc = fma(wz, sy, acc);
+                }
+#pragma unroll
+                for (int vz = 0; vz < (D >= 3 ? V : 1); ++vz) {
+                    double sy = 0.0;
+#pragma unroll
+                    for (int vy = 0; vy < V; ++vy) sy = fma(PW[i2 * kMaxV + vy], gv[vz][vy], sy);
+                    acc = fma(D >= 3 ? PW[i3 * kMaxV + vz] : 1.0, sy, acc);
                 }
             }
             G[h] = acc;
@@ -714,12 +719,108 @@ __global__ void __launch_bounds__(256) k_load_grid_line(const GenericArgs a, con
     }
 }
 
+// 3D GRID load vector, y-sliding variant: a warp owns (i3, a 32-row x segment, a chunk of
+// consecutive y-lines).  Lane l first reduces over z for its vertex plane c = c0 + l:
+// Hz[y] = sum_vz PWz[vz] g[bz+vz][y][c] (5 loads, reused by the 5 lines whose window holds y),
+// slides a 5-deep window of Hz over y, forms G = sum_vy PWy[vy] Hz[by+vy] per line and finishes
+// the row i1 = x0 + l with warp shuffles as in k_load_grid_line.
+constexpr int kLoadYChunk = 32;
+
+template <int P>
+__global__ void __launch_bounds__(256) k_load_grid_yslide(const GenericArgs a, const double* PW, double* b) {
+    constexpr int V = P + 2;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t N = a.N, nv = a.n + 1, n = a.n;
+    const int64_t xsegs = (N + 31) / 32, ychunks = (N + kLoadYChunk - 1) / kLoadYChunk;
+    const int64_t plane_rows = N * N;
+    const int64_t z0 = a.row_begin / plane_rows, z1 = (a.row_end - 1) / plane_rows;
+    const int64_t items = (z1 - z0 + 1) * xsegs * ychunks;
+    for (int64_t it = warp; it < items; it += nwarps) {
+        const int64_t i3 = z0 + it / (xsegs * ychunks);
+        const int64_t rem = it % (xsegs * ychunks);
+        const int64_t x0 = (rem / ychunks) * 32, ya = (rem % ychunks) * kLoadYChunk;
+        const int64_t yb = min(N, ya + kLoadYChunk);
+        const int64_t bz = max((int64_t)0, i3 - P);
+        const int64_t c0 = max((int64_t)0, x0 - P);
+        double pwz[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) pwz[v] = PW[i3 * kMaxV + v];
+        // Hz for the lane's planes c0 + lane (h = 0) and c0 + 32 + lane (h = 1, lanes < V-1)
+        auto hz = [&](int64_t y, int h) -> double {
+            const int64_t c = c0 + lane + 32 * h;
+            if (y > n || c > n || (h == 1 && lane >= V - 1)) return 0.0;
+            double gv[V];
+#pragma unroll
+            for (int vz = 0; vz < V; ++vz) {
+                const int64_t z = bz + vz;
+                gv[vz] = z <= n ? __ldg(a.coef.grid + ((z - a.coef.plane0) * nv + y) * nv + c) : 0.0;
+            }
+            double s = 0.0;
+#pragma unroll
+            for (int vz = 0; vz < V; ++vz) s = fma(pwz[vz], gv[vz], s);
+            return s;
+        };
+        // window W[v] = Hz[by + v] for the current line (by = max(0, i2 - P))
+        double W0[V], W1[V];
+        int64_t wby = max((int64_t)0, ya - P);
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            W0[v] = hz(wby + v, 0);
+            W1[v] = hz(wby + v, 1);
+        }
+        for (int64_t i2 = ya; i2 < yb; ++i2) {
+            const int64_t by = max((int64_t)0, i2 - P);
+            if (by != wby) {                                   // slide by one vertex row
+#pragma unroll
+                for (int v = 0; v + 1 < V; ++v) {
+                    W0[v] = W0[v + 1];
+                    W1[v] = W1[v + 1];
+                }
+                W0[V - 1] = hz(by + V - 1, 0);
+                W1[V - 1] = hz(by + V - 1, 1);
+                wby = by;
+            }
+            double G0 = 0.0, G1 = 0.0;
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                const double w = PW[i2 * kMaxV + v];
+                G0 = fma(w, W0[v], G0);
+                G1 = fma(w, W1[v], G1);
+            }
+            const int64_t i1 = x0 + lane;
+            const int64_t row = (i3 * N + i2) * N + i1;
+            const bool mine = i1 < N && row >= a.row_begin && row < a.row_end;
+            const int64_t bx = max((int64_t)0, i1 - P);
+            double acc = 0.0;
+#pragma unroll
+            for (int vx = 0; vx < V; ++vx) {
+                const int src = (int)(bx + vx - c0);
+                const double g0 = __shfl_sync(0xffffffffu, G0, src & 31);
+                const double g1 = __shfl_sync(0xffffffffu, G1, src & 31);
+                const double wx = mine ? PW[i1 * kMaxV + vx] : 0.0;
+                acc = fma(wx, src < 32 ? g0 : g1, acc);
+            }
+            if (mine) b[row - a.row_begin] = acc;
+        }
+    }
+}
+
 template <int P, int D>
 int launch_load_pd(const GenericArgs& a, const double* PW, double* b, cudaStream_t st) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t rows = a.row_end - a.row_begin;
+    if (D == 3 && a.coef.kind == WGQ_COEF_GRID) {
+        const int64_t pr = a.N * a.N;
+        const int64_t items = ((a.row_end - 1) / pr - a.row_begin / pr + 1) * ((a.N + 31) / 32) *
+                              ((a.N + kLoadYChunk - 1) / kLoadYChunk);
+        const int64_t b3 = std::max<int64_t>(1, std::min<int64_t>((items + 7) / 8, (int64_t)sms * 16));
+        k_load_grid_yslide<P><<<(unsigned)b3, 256, 0, st>>>(a, PW, b);
+        return cudaGetLastError() == cudaSuccess ? WGQ_OK : WGQ_ECUDA;
+    }
     if (D >= 2 && a.coef.kind == WGQ_COEF_GRID) {
         const int64_t items = ((a.row_end - 1) / a.N - a.row_begin / a.N + 1) * ((a.N + 31) / 32);
         const int64_t b2 = std::max<int64_t>(1, std::min<int64_t>((items + 7) / 8, (int64_t)sms * 16));
