@@ -239,15 +239,29 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.current_stream()
 
+    # setup, reported separately: host rule build, device tables, grid generation
+    setup = {}
+    t0 = time.perf_counter()
     rules = wgq.Rules(p, n, d)
+    setup["rules_host_ms"] = round((time.perf_counter() - t0) * 1e3, 3)
     N = rules.N
     row_begin, row_end = api.slab_rows(N, d, rank, world)
     rows = row_end - row_begin
     ld = args.ld or rules.stencil
     grid, plane0 = (None, 0)
+    torch.cuda.synchronize()
     if cfg["coeff"]["kind"] == "grid":
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
         grid, plane0 = api.make_grid(rules, cfg["coeff"]["seed"], cfg["coeff"]["sigma"], row_begin, row_end)
+        e1.record()
+        torch.cuda.synchronize()
+        setup["grid_generation_ms"] = round(e0.elapsed_time(e1), 3)
     coef = api.coefficient(inputs.coefficient(cfg["coeff"], d), grid, plane0)
+    t0 = time.perf_counter()
+    api.assemble_load(rules, coef, row_begin, min(row_end, row_begin + 1))   # first device call: row tables
+    torch.cuda.synchronize()
+    setup["device_tables_ms"] = round((time.perf_counter() - t0) * 1e3, 3)
     out = {k: api.alloc_ell(rules, row_begin, row_end, ld) for k in kinds}
     nnz_rank = wgq.wgq_nnz(rules, row_begin, row_end) * len(kinds)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")     # 512 MB > L2
@@ -320,7 +334,8 @@ def main():
                            "layout": "ELL", "parallelism": f"z-slab x{world}",
                            "l2": "flushed (512 MB write) between timed steps; outputs >> L2"},
                 "gpu_launches": args.steps * 1,
-                "roofline": roof, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu, "extras": extras}
+                "roofline": roof, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu, "extras": extras,
+                "setup": setup}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -371,6 +386,14 @@ def run_extras(rules5, coef5, peak):
     ms = _time_ms(lambda: api.apply(rules5, coef5, u), flush=flush)
     out["operators"]["apply_MK_C5"] = {"ms": round(ms, 4), "rows_per_s": n_rows / (ms / 1e3),
                                        "note": "matrix-free y_M = M u and y_K = K u, nothing stored"}
+    # peak microbenchmarks of this box, same session (tools/peaks.cu, built by build())
+    exe = os.path.join(ROOT, "tools", "peaks")
+    if os.path.exists(exe):
+        try:
+            r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+            out["box_peaks"] = json.loads(r.stdout.strip().splitlines()[-1])
+        except Exception as e:          # the headline numbers do not depend on it
+            out["box_peaks"] = {"error": str(e)[:200]}
     return out
 
 

@@ -45,6 +45,11 @@ def build(force=False, verbose=False):
         objs.append(obj)
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB] + objs + ["-lcudart"]
     subprocess.run(cmd, check=True)
+    # peak microbenchmarks (write-only HBM, copy, DFMA) used by bench.py's extras
+    peaks_src = os.path.join(ROOT, "tools", "peaks.cu")
+    if os.path.exists(peaks_src):
+        subprocess.run([NVCC, "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-o",
+                        os.path.join(ROOT, "tools", "peaks"), peaks_src], check=True)
     return LIB
 
 
