@@ -592,6 +592,7 @@ __global__ void __launch_bounds__(256, 3) k_line_apply(const __grid_constant__ L
     double* Dm = U + URING * HS;                          // [16][16]  D_M(c - b0, X - Xlo)
     double* Dk = Dm + 256;
     double* pint = Dk + 256;                              // [2][V][S]: interior P^ (h, 1/h folded)
+    double* zrow = pint + 2 * V * S;                      // [HS] zeros: operand row of invalid planes / columns
     __shared__ TileDesc desc[8];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n = a.n, N = a.N;
@@ -602,15 +603,46 @@ __global__ void __launch_bounds__(256, 3) k_line_apply(const __grid_constant__ L
         xbt[e] = (kind ? a.T.PK : a.T.PM)[((size_t)r * kMaxV + v) * kMaxS + o];
     }
     for (int e = tid; e < 2 * V * S; e += NT) pint[e] = e < V * S ? a.PMh[e / S][e % S] : a.PKi[(e - V * S) / S][e % S];
+    // zero rows and the padding columns [S2, HS) of the H and U rows: the D fragments then need no masks
+    for (int e = tid; e < HS; e += NT) zrow[e] = 0.0;
+    for (int e = tid; e < (2 * RING + URING) * (HS - S2); e += NT) {
+        const int row = e / (HS - S2), col = S2 + e % (HS - S2);
+        (row < 2 * RING ? Hm + row * HS : U + (row - 2 * RING) * HS)[col] = 0.0;
+    }
+    // u loads: thread tid owns elements e = tid + NT m (m < MU) of a tile's new columns, laid
+    // out as [x-offset block][o23][x-offset & 7] so a warp reads contiguous runs along X; the
+    // (o23, x-offset) of each element is fixed, its global row offset changes once per line
+    constexpr int MU = (16 * S2 + NT - 1) / NT;
+    int uxo[MU], uo23[MU];
+    long long ubase[MU];
+#pragma unroll
+    for (int m = 0; m < MU; ++m) {
+        const int e = tid + NT * m;
+        uxo[m] = (e & 7) + 8 * (e / (8 * S2));
+        uo23[m] = (e >> 3) % S2;
+        ubase[m] = -1;
+    }
     auto issue = [&](const TileIt& t, PatchRow& pr) {
         if (t.line <= last_line) {
-            const long long N2 = (long long)N * N;
-            for (int e = tid; e < (t.uhi - t.ulo + 1) * S2; e += NT) {
-                const int X = t.ulo + e / S2, o23 = e % S2, o2 = o23 % S, o3 = o23 / S;
-                const int iy = t.i2 - P + o2, iz = t.i3 - P + o3;
-                const bool ok = iy >= 0 && iy < N && iz >= 0 && iz < N;
-                const long long g = ok ? (long long)iz * N2 + (long long)iy * N + X - a.u_row0 : 0;
-                cp_async8(U + ((t.lpos + X - t.X0) % URING) * HS + o23, a.u + g, ok);
+            if (t.t0 == t.x0) {                                // new line: the rows' global offsets
+                const long long N2 = (long long)N * N;
+#pragma unroll
+                for (int m = 0; m < MU; ++m) {
+                    const int o2 = uo23[m] % S, o3 = uo23[m] / S;
+                    const int iy = t.i2 - P + o2, iz = t.i3 - P + o3;
+                    ubase[m] = (iy >= 0 && iy < N && iz >= 0 && iz < N) ? (long long)iz * N2 + (long long)iy * N - a.u_row0 : -1;
+                }
+            }
+            const int nx = t.uhi - t.ulo + 1;
+            const int rpos = t.lpos - t.X0;
+#pragma unroll
+            for (int m = 0; m < MU; ++m) {
+                if (uxo[m] >= nx || uxo[m] >= 16) continue;
+                const int X = t.ulo + uxo[m];
+                const bool ok = ubase[m] >= 0;
+                int pos = rpos + X;
+                pos = pos >= URING ? pos % URING : pos;
+                cp_async8(U + pos * HS + uo23[m], a.u + (ok ? ubase[m] + X : 0), ok);
             }
         }
         tile_issue<P, NT>(a, patches, qbufs, t, pr, last_line, tid);     // commits the group
@@ -633,17 +665,6 @@ __global__ void __launch_bounds__(256, 3) k_line_apply(const __grid_constant__ L
     cp_async_wait<PFD - 2>();
     __syncthreads();
     const int g = lane >> 2, t4 = lane & 3;
-    // lane-resident interior x-row coefficients of the final contraction: pairs q = lane, lane+32
-    int qv[2], qo[2];
-    double qm[2], qk[2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const int q = min(lane + 32 * h, V * S - 1);
-        qv[h] = q / S;
-        qo[h] = q % S;
-        qm[h] = a.PMh[qv[h]][qo[h]];
-        qk[h] = a.PKi[qv[h]][qo[h]];
-    }
     for (int k = 0;; ++k) {
         const TileDesc d = desc[k & 7];
         if (d.line < 0) break;
@@ -656,16 +677,13 @@ __global__ void __launch_bounds__(256, 3) k_line_apply(const __grid_constant__ L
             const double* H = kind ? Hk : Hm;
             const int c = b0 + 8 * mt + g, X = d.Xlo + 8 * nt + g;
             const bool cv = c <= hi_plane, xv = X <= d.Xhi;
-            const double* hrow = H + (c & (RING - 1)) * HS;
-            const double* urow = U + ((d.upos + 8 * nt + g) % URING) * HS;
+            const double* hrow = (cv ? H + (c & (RING - 1)) * HS : zrow) + t4;
+            const double* urow = (xv ? U + ((d.upos + 8 * nt + g) % URING) * HS : zrow) + t4;
             double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;     // two chains: even / odd k-steps
 #pragma unroll
-            for (int s = 0; s < (S2 + 3) / 4; ++s) {
-                const int o = 4 * s + t4;
-                const double av = (cv && o < S2) ? hrow[o] : 0.0;
-                const double bv = (xv && o < S2) ? urow[o] : 0.0;
-                if (s & 1) dmma(e0, e1, av, bv);
-                else dmma(d0, d1, av, bv);
+            for (int s = 0; s < ((a.dbg & 8) ? 0 : (S2 + 3) / 4); ++s) {      // padding columns are zero: no masks
+                if (s & 1) dmma(e0, e1, hrow[4 * s], urow[4 * s]);
+                else dmma(d0, d1, hrow[4 * s], urow[4 * s]);
             }
             double* D = kind ? Dk : Dm;
             D[(8 * mt + g) * 16 + 8 * nt + 2 * t4] = d0 + e0;
@@ -673,45 +691,38 @@ __global__ void __launch_bounds__(256, 3) k_line_apply(const __grid_constant__ L
         }
         __syncthreads();
         // ---- S1b: rows of tile k (one per warp), phase A of tile k+1, prefetch tile k+PFD ----
-        {                                                  // warp j finishes row t0 + j
-            const int j = warp;
+        if (warp == 0) {
+            // warp 0 finishes all rows of the tile: lane (j, vq) = row t0 + j, vertex planes
+            // vx = vq (+4); y = sum_{vx,o1} P[vx][o1] D(b_r + vx, r - p + o1), reduced over 4 lanes
+            const int j = lane >> 2, vq = lane & 3;
             double ym = 0.0, yk = 0.0;
             if (j < d.tr) {
-                const int r = d.t0 + j;
-                if (r >= 2 * P && r <= n - 1 - P && d.t0 >= P) {
-                    // interior row: b_r - b0 = j, X - Xlo = j + o1; lane-resident P^ coefficients
+                const int r = d.t0 + j, br = max(0, r - P);
+                const bool interior = r >= 2 * P && r <= n - 1 - P;
+                const double* pm = interior ? pint : xbt + (r < 2 * P ? r : 2 * P + (r - (n - P))) * (2 * V * S);
+                const double* pk = pm + V * S;
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        if (h == 1 && lane + 32 >= V * S) break;
-                        const int di = (j + qv[h]) * 16 + j + qo[h];
-                        const double dm = Dm[di];
-                        ym = fma(qm[h], dm, ym);
-                        yk = fma(qk[h], dm, yk);
-                        yk = fma(qm[h], Dk[di], yk);
-                    }
-                } else {
-                    const int br = max(0, r - P);
-                    const bool interior = r >= 2 * P && r <= n - 1 - P;
-                    const double* pm = interior ? pint : xbt + (r < 2 * P ? r : 2 * P + (r - (n - P))) * (2 * V * S);
-                    for (int q = lane; q < V * S; q += 32) {
-                        const int vx = q / S, o1 = q % S;
+                for (int vv = 0; vv < 2; ++vv) {
+                    const int vx = vq + 4 * vv;
+                    if (vx >= V) break;
+                    const double* dmr = Dm + (br + vx - b0) * 16 - d.Xlo;
+                    const double* dkr = Dk + (br + vx - b0) * 16 - d.Xlo;
+#pragma unroll
+                    for (int o1 = 0; o1 < S; ++o1) {
                         const int X = r - P + o1;
                         if (X < 0 || X >= N) continue;
-                        const int di = (br + vx - b0) * 16 + (X - d.Xlo);
-                        const double dm = Dm[di];
-                        const double cm = pm[vx * S + o1];
+                        const double dm = dmr[X], cm = pm[vx * S + o1];
                         ym = fma(cm, dm, ym);
-                        yk = fma(pm[V * S + vx * S + o1], dm, yk);
-                        yk = fma(cm, Dk[di], yk);
+                        yk = fma(pk[vx * S + o1], dm, yk);
+                        yk = fma(cm, dkr[X], yk);
                     }
                 }
             }
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                ym += __shfl_xor_sync(0xffffffffu, ym, off);
-                yk += __shfl_xor_sync(0xffffffffu, yk, off);
-            }
-            if (lane == 0 && j < d.tr) {
+            ym += __shfl_xor_sync(0xffffffffu, ym, 1);
+            yk += __shfl_xor_sync(0xffffffffu, yk, 1);
+            ym += __shfl_xor_sync(0xffffffffu, ym, 2);
+            yk += __shfl_xor_sync(0xffffffffu, yk, 2);
+            if (vq == 0 && j < d.tr) {
                 if (MODE & 1) a.yM[d.orow0 + j] = ym;
                 if (MODE & 2) a.yK[d.orow0 + j] = yk;
             }
@@ -731,7 +742,7 @@ int launch_apply_p(const LineArgs& a, cudaStream_t st) {
     using C = Cfg<P>;
     constexpr int HS = (C::S2 + 3) / 4 * 4 + ((C::S2 + 3) / 4 % 2 == 0 ? 4 : 0);
     const size_t smem = (size_t)(2 * C::RING * HS + C::PFD * 4 * C::V * C::S + C::PFD * C::PATCH + C::XB +
-                                 C::URING * HS + 512 + 2 * C::V * C::S) * sizeof(double);
+                                 C::URING * HS + 512 + 2 * C::V * C::S + HS) * sizeof(double);
     auto kern = k_line_apply<P, MODE>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return WGQ_ECUDA;
@@ -849,6 +860,7 @@ int launch_line_apply(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_
     a.u_row0 = u_row0;
     a.yM = yM;
     a.yK = yK;
+    if (const char* e = getenv("WGQ_LINE_DBG")) a.dbg = atoi(e);
     const int mode = (yM ? 1 : 0) | (yK ? 2 : 0);
     cudaStream_t st = (cudaStream_t)stream;
     if (R->p == 3) return mode == 3 ? launch_apply_p<3, 3>(a, st) : (mode == 1 ? launch_apply_p<3, 1>(a, st) : launch_apply_p<3, 2>(a, st));
