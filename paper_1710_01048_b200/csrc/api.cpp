@@ -156,6 +156,10 @@ void wgq_free_rules(wgq_rules_t R) {
         cudaSetDevice(std::get<0>(kv.first));
         if (kv.second.first) cudaFree(kv.second.first);
     }
+    for (auto& kv : R->sep_vectors) {
+        cudaSetDevice(kv.first[0]);
+        cudaFree(kv.second);
+    }
     cudaSetDevice(cur);
     delete R;
 }

@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <map>
 #include <mutex>
+#include <array>
 #include <tuple>
 
 #include "wgq.h"
@@ -64,6 +65,8 @@ struct wgq_rules_s {
     // shell rows (rows touching a GL-fallback boundary class) of a row range, per device:
     // (device, row_begin, row_end) -> device array of global row ids (built once, reused)
     std::map<std::tuple<int, int64_t, int64_t>, std::pair<int64_t*, int64_t>> shells;
+    // separable-coefficient vectors (separable.cu), per (device, kind, trig[3], wavenum[3])
+    std::map<std::array<int, 8>, double*> sep_vectors;
 };
 
 namespace wgq {

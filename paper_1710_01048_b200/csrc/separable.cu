@@ -18,6 +18,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
+#include <mutex>
 
 #include "internal.h"
 
@@ -285,13 +287,32 @@ int launch_sep(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, c
     if (any->row_end <= any->row_begin) return WGQ_OK;
     cudaStream_t st = (cudaStream_t)stream;
     const int S = 2 * R->p + 1;
-    const int64_t entries = (int64_t)R->dim * R->N * 4 * kMaxS;
+    // the 4 x s vectors depend on the rules and the factors f_a only (c0, amp enter the value
+    // formulas): built once per (device, kind, trig, wavenum) and cached in the rules handle
     double* sep = nullptr;
-    if (cudaMallocAsync((void**)&sep, (size_t)entries * sizeof(double), st) != cudaSuccess) return WGQ_ENOMEM;
-    const int64_t threads = (int64_t)R->dim * R->N * S;
-    k_sep_tables<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(R->dim, R->p, T, c->kind, c->trig[0], c->trig[1],
-                                                                    c->trig[2], c->wavenum[0], c->wavenum[1],
-                                                                    c->wavenum[2], sep);
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const bool trig = c->kind == WGQ_COEF_TRIG_SEP;
+        const std::array<int, 8> key = {dev, c->kind, trig ? c->trig[0] : 0, trig ? c->trig[1] : 0, trig ? c->trig[2] : 0,
+                                        trig ? c->wavenum[0] : 0, trig ? c->wavenum[1] : 0, trig ? c->wavenum[2] : 0};
+        wgq_rules_s* Rm = const_cast<wgq_rules_s*>(R);
+        std::lock_guard<std::mutex> lock(Rm->mu);
+        auto it = Rm->sep_vectors.find(key);
+        if (it == Rm->sep_vectors.end()) {
+            const int64_t entries = (int64_t)R->dim * R->N * 4 * kMaxS;
+            if (cudaMalloc((void**)&sep, (size_t)entries * sizeof(double)) != cudaSuccess) return WGQ_ENOMEM;
+            const int64_t threads = (int64_t)R->dim * R->N * S;
+            k_sep_tables<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(R->dim, R->p, T, c->kind, c->trig[0],
+                                                                            c->trig[1], c->trig[2], c->wavenum[0],
+                                                                            c->wavenum[1], c->wavenum[2], sep);
+            // used from any stream afterwards: complete the one-time build now
+            if (cudaStreamSynchronize(st) != cudaSuccess) return WGQ_ECUDA;
+            Rm->sep_vectors.emplace(key, sep);
+        } else {
+            sep = it->second;
+        }
+    }
     SepArgs a{};
     a.sep = sep;
     a.N = R->N;
@@ -320,7 +341,6 @@ int launch_sep(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, c
         case 32: rc = launch_sep_pd<3, 2>(a, mode, st); break;
         case 33: rc = launch_sep_pd<3, 3>(a, mode, st); break;
     }
-    cudaFreeAsync(sep, st);
     return rc;
 }
 
