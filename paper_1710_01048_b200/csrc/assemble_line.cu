@@ -73,6 +73,7 @@ struct LineArgs {
     // (kernel parameters: constant-bank operands, no global state shared between handles)
     double PMh[kMaxV][kMaxS], PKi[kMaxV][kMaxS];
     int dbg;   // profiling only (WGQ_LINE_DBG bits): 1 = skip compute, 2 = skip stores, 4 = skip loads
+    long long csr_base;   // CSR: global position of row_begin's first entry (closed form)
     // matrix-free application (k_line_apply): y = A u over the rows, u from global row u_row0
     const double* u;
     long long u_row0;
@@ -218,11 +219,12 @@ __device__ __forceinline__ void finish_interior(const double* hm, const double* 
 // memory once per CTA (the 4p such rows are the same for every line)
 template <int P, int MODE>
 __device__ __forceinline__ void finish_general(const double* pm, const double* hm, const double* hk, double* dM,
-                                               double* dK) {
+                                               double* dK, int lo1 = 0, int hi1 = 2 * P) {
     constexpr int S = 2 * P + 1, V = P + 2;
     const double* pk = pm + V * S;
 #pragma unroll
     for (int o1 = 0; o1 < S; ++o1) {
+        if (o1 < lo1 || o1 > hi1) continue;             // CSR: columns outside the mesh are not stored
         double s = 0.0, s1 = 0.0;
 #pragma unroll
         for (int v = 0; v < V; ++v) {
@@ -315,6 +317,20 @@ __device__ __forceinline__ void tile_issue(const LineArgs& a, double* patches, d
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
+// CSR structure in closed form: a(r) = structural columns of 1D row r,
+// A(r) = sum_{r' < r} a(r'), S = A(N); row (i1,i2,i3) starts at A(i3) S^2 + a(i3)(A(i2) S + a(i2) A(i1)).
+__host__ __device__ __forceinline__ long long csr_a(long long r, int p, long long N) {
+    return (r + p < N - 1 ? r + p : N - 1) - (r - p > 0 ? r - p : 0) + 1;
+}
+__host__ __device__ __forceinline__ long long csr_A(long long r, int p, long long N) {
+    const long long m = r < p ? r : p, q = r - (N - p) > 0 ? r - (N - p) : 0;
+    return (2 * p + 1) * r - (m * p - m * (m - 1) / 2) - q * (q + 1) / 2;
+}
+__host__ __device__ __forceinline__ long long csr_start(long long row, int p, long long N) {
+    const long long i1 = row % N, i2 = (row / N) % N, i3 = row / (N * N), S = csr_A(N, p, N);
+    return csr_A(i3, p, N) * S * S + csr_a(i3, p, N) * (csr_A(i2, p, N) * S + csr_a(i2, p, N) * csr_A(i1, p, N));
+}
+
 // What every warp needs to know about a tile; written by thread 0 when the tile is prefetched.
 struct TileDesc {
     int line;          // -1: past the CTA's last tile
@@ -324,6 +340,10 @@ struct TileDesc {
     int pad;           // staging offset aligning the tile's first element
     long long orow0;   // output row of the tile's first row
     int Xlo, Xhi, upos;  // apply: the tile's u columns [Xlo, Xhi], ring position of Xlo
+    // CSR: slab-local position of the tile's first entry, entries per x-row unit (a2 a3), the
+    // y/z validity boxes (offset indices lo..hi of the 2p+1) and a2
+    long long cs0;
+    int w23, lo2, hi2, lo3, hi3, a2;
 };
 
 template <int P>
@@ -341,6 +361,16 @@ __device__ __forceinline__ TileDesc make_desc(const LineArgs& a, const TileIt& t
     d.Xlo = max(0, t.t0 - P);
     d.Xhi = t.uhi;
     d.upos = (t.lpos + d.Xlo - t.X0) % Cfg<P>::URING;
+    if (a.csr_base >= 0 && t.line <= last_line) {
+        const long long N = a.N;
+        d.cs0 = csr_start((long long)t.line * N + t.t0, P, N) - a.csr_base;
+        d.a2 = (int)csr_a(t.i2, P, N);
+        d.w23 = d.a2 * (int)csr_a(t.i3, P, N);
+        d.lo2 = max(0, P - t.i2);
+        d.hi2 = min(2 * P, (int)N - 1 - t.i2 + P);
+        d.lo3 = max(0, P - t.i3);
+        d.hi3 = min(2 * P, (int)N - 1 - t.i3 + P);
+    }
     return d;
 }
 
@@ -417,6 +447,21 @@ __device__ __forceinline__ void phase_a(const LineArgs& a, const TileDesc& t, co
     }
 }
 
+// Bulk store of a contiguous run of `total` values staged from st (st is offset so that the run's
+// first element keeps its global 16-byte phase), by warp 0, without the commit.
+__device__ __forceinline__ void store_run(double* out, const double* st, long long g0, int total, int lane) {
+    const int head = (int)(g0 & 1);
+    const int tail = (int)((g0 + total) & 1);
+    if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (total - head - tail > 0) bulk_store(out + g0 + head, st + head, (uint32_t)(total - head - tail) * 8u);
+    } else if (lane == 1 && head) {
+        out[g0] = st[0];
+    } else if (lane == 2 && tail && total > head) {
+        out[g0 + total - 1] = st[total - 1];
+    }
+}
+
 // Bulk store of one matrix of the staged tile (tr rows from output row orow0), by warp 0,
 // without the commit: lane 0 issues the 16-byte aligned interior as one cp.async.bulk, lanes
 // 1 / 2 the peeled odd end elements; padded even ld: one bulk copy per row (lane 0) and the
@@ -449,7 +494,7 @@ __device__ __forceinline__ void store_mat(const LineArgs& a, double* out, const 
     }
 }
 
-template <int P, int MODE>
+template <int P, int MODE, bool CSR>
 __global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const __grid_constant__ LineArgs a) {
     using C = Cfg<P>;
     constexpr int S = C::S, S2 = C::S2, S3 = C::S3, V = C::V, RING = C::RING;
@@ -510,8 +555,9 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const __grid_const
         const TileDesc d = desc[k & 7];
         if (d.line < 0) break;
         const TileDesc dA = desc[(k + 1) & 7];
-        double* stM = stage + d.pad;
-        double* stK = stage + C::STAGE + d.pad;
+        const int pad = CSR ? (int)(d.cs0 & 1) : d.pad;
+        double* stM = stage + pad;
+        double* stK = stage + C::STAGE + pad;
         // ---- S1: phase B of tile k ---------------------------------------------------------
         if (tid < C::ITEMS && 2 * q < d.tr && !(a.dbg & 1)) {
             const int j = 2 * q, r = d.t0 + j;
@@ -525,30 +571,73 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const __grid_const
             }
             const bool second = j + 1 < d.tr;
             const bool shift = r + 1 - P > 0;          // row r+1's window starts one plane later
-            double* dM = stM + j * SRr + S * o23;
-            double* dK = stK + j * SRr + S * o23;
-            if (r >= 2 * P && r + 1 <= n - 1 - P) {   // both rows class I (the common case)
-                finish_pair_interior<P, MODE>(hm, hk, dM, dK, SRr, second, a);
-            } else {
-                if (r >= 2 * P && r <= n - 1 - P) finish_interior<P, MODE>(hm, hk, dM, dK, a);
-                else finish_general<P, MODE>(xb_row(r), hm, hk, dM, dK);
-                if (second) {
-                    double hm1[V], hk1[V];
+            if (!CSR) {
+                double* dM = stM + j * SRr + S * o23;
+                double* dK = stK + j * SRr + S * o23;
+                if (r >= 2 * P && r + 1 <= n - 1 - P) {   // both rows class I (the common case)
+                    finish_pair_interior<P, MODE>(hm, hk, dM, dK, SRr, second, a);
+                } else {
+                    if (r >= 2 * P && r <= n - 1 - P) finish_interior<P, MODE>(hm, hk, dM, dK, a);
+                    else finish_general<P, MODE>(xb_row(r), hm, hk, dM, dK);
+                    if (second) {
+                        double hm1[V], hk1[V];
 #pragma unroll
-                    for (int v = 0; v < V; ++v) {
-                        hm1[v] = shift ? hm[v + 1] : hm[v];
-                        hk1[v] = shift ? hk[v + 1] : hk[v];
+                        for (int v = 0; v < V; ++v) {
+                            hm1[v] = shift ? hm[v + 1] : hm[v];
+                            hk1[v] = shift ? hk[v + 1] : hk[v];
+                        }
+                        if (r + 1 >= 2 * P && r + 1 <= n - 1 - P) finish_interior<P, MODE>(hm1, hk1, dM + SRr, dK + SRr, a);
+                        else finish_general<P, MODE>(xb_row(r + 1), hm1, hk1, dM + SRr, dK + SRr);
                     }
-                    if (r + 1 >= 2 * P && r + 1 <= n - 1 - P) finish_interior<P, MODE>(hm1, hk1, dM + SRr, dK + SRr, a);
-                    else finish_general<P, MODE>(xb_row(r + 1), hm1, hk1, dM + SRr, dK + SRr);
+                }
+            } else {
+                // CSR: row r's entries start at w23 (A(r) - A(t0)) in the tile; the thread's (o2, o3)
+                // group sits at pos23 = (o2 - lo2) + a2 (o3 - lo3) if inside the mesh, its o1 at o1 - lo1(r)
+                const int o2 = o23 % S, o3 = o23 / S;
+                if (o2 >= d.lo2 && o2 <= d.hi2 && o3 >= d.lo3 && o3 <= d.hi3) {
+                    const int pos23 = (o2 - d.lo2) + d.a2 * (o3 - d.lo3);
+                    const long long At0 = csr_A(d.t0, P, a.N);
+                    const int off0 = (int)(d.w23 * (csr_A(r, P, a.N) - At0));
+                    const int ar0 = (int)csr_a(r, P, a.N);
+                    if (r >= 2 * P && r + 1 <= n - 1 - P) {   // both rows class I: a(r) = 2p+1, lo1 = 0
+                        finish_pair_interior<P, MODE>(hm, hk, stM + off0 + S * pos23, stK + off0 + S * pos23, S * d.w23,
+                                                      second, a);
+                    } else {
+                        const int lo1 = max(0, P - r), hi1 = min(2 * P, a.N - 1 - r + P);
+                        double* dM = stM + off0 + ar0 * pos23 - lo1;
+                        double* dK = stK + off0 + ar0 * pos23 - lo1;
+                        if (r >= 2 * P && r <= n - 1 - P) finish_interior<P, MODE>(hm, hk, dM, dK, a);
+                        else finish_general<P, MODE>(xb_row(r), hm, hk, dM, dK, lo1, hi1);
+                        if (second) {
+                            const int r1 = r + 1;
+                            double hm1[V], hk1[V];
+#pragma unroll
+                            for (int v = 0; v < V; ++v) {
+                                hm1[v] = shift ? hm[v + 1] : hm[v];
+                                hk1[v] = shift ? hk[v + 1] : hk[v];
+                            }
+                            const int off1 = (int)(d.w23 * (csr_A(r1, P, a.N) - At0));
+                            const int lo1b = max(0, P - r1), hi1b = min(2 * P, a.N - 1 - r1 + P);
+                            double* dM1 = stM + off1 + (int)csr_a(r1, P, a.N) * pos23 - lo1b;
+                            double* dK1 = stK + off1 + (int)csr_a(r1, P, a.N) * pos23 - lo1b;
+                            if (r1 >= 2 * P && r1 <= n - 1 - P) finish_interior<P, MODE>(hm1, hk1, dM1, dK1, a);
+                            else finish_general<P, MODE>(xb_row(r1), hm1, hk1, dM1, dK1, lo1b, hi1b);
+                        }
+                    }
                 }
             }
         }
         __syncthreads();
         // ---- S2: store tile k, phase A of tile k+1, prefetch tile k+3 --------------------
         if (tid < 32 && !(a.dbg & 2)) {
-            if (MODE & 1) store_mat<P>(a, a.M, stM, d.orow0, d.tr, SRr, padded, tid);
-            if (MODE & 2) store_mat<P>(a, a.K, stK, d.orow0, d.tr, SRr, padded, tid);
+            if (CSR) {
+                const long long total = (long long)d.w23 * (csr_A(d.t0 + d.tr, P, a.N) - csr_A(d.t0, P, a.N));
+                if (MODE & 1) store_run(a.M, stM, d.cs0, (int)total, tid);
+                if (MODE & 2) store_run(a.K, stK, d.cs0, (int)total, tid);
+            } else {
+                if (MODE & 1) store_mat<P>(a, a.M, stM, d.orow0, d.tr, SRr, padded, tid);
+                if (MODE & 2) store_mat<P>(a, a.K, stK, d.orow0, d.tr, SRr, padded, tid);
+            }
             if (tid == 0) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
         if (dA.line >= 0) phase_a<P>(a, dA, patches, qbufs, Hm, Hk, tid);
@@ -760,7 +849,7 @@ template <int P, int MODE>
 int launch_line_p(const LineArgs& a, cudaStream_t st) {
     using C = Cfg<P>;
     const size_t smem = (size_t)C::SMEM * sizeof(double);
-    auto kern = k_line_grid3<P, MODE>;
+    auto kern = a.csr_base >= 0 ? k_line_grid3<P, MODE, true> : k_line_grid3<P, MODE, false>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return WGQ_ECUDA;
     cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -785,8 +874,13 @@ int launch_line_mode(const LineArgs& a, int mode, cudaStream_t st) {
 
 bool line_kernel_applies(const wgq_rules_s* R, const wgq_coeff_t* c, const wgq_out_t* M, const wgq_out_t* K) {
     const wgq_out_t* o = M ? M : K;
-    if (c->kind != WGQ_COEF_GRID || R->dim != 3 || o->layout != WGQ_ELL) return false;
+    if (c->kind != WGQ_COEF_GRID || R->dim != 3) return false;
     if (R->n < R->p + 1) return false;
+    if (o->layout == WGQ_CSR) {
+        for (const wgq_out_t* x : {M, K})
+            if (x && ((uintptr_t)x->values) % 16 != 0) return false;
+        return true;
+    }
     const int64_t S3 = (2 * R->p + 1) * (2 * R->p + 1) * (2 * R->p + 1);
     for (const wgq_out_t* x : {M, K}) {
         if (!x) continue;
@@ -811,7 +905,8 @@ int launch_line(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, 
     a.row_end = (int)o->row_end;
     a.M = M ? M->values : nullptr;
     a.K = K ? K->values : nullptr;
-    a.ld = o->ld;
+    a.ld = o->layout == WGQ_CSR ? (2 * R->p + 1) * (2 * R->p + 1) * (2 * R->p + 1) : o->ld;
+    a.csr_base = o->layout == WGQ_CSR ? csr_start(o->row_begin, R->p, R->N) : -1;
     const int mode = (M ? 1 : 0) | (K ? 2 : 0);
     a.h = 1.0 / (double)R->n;
     a.inv_h = (double)R->n;

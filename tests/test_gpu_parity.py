@@ -118,7 +118,8 @@ def test_slabs_bitwise_equal_and_padded_ld():
 
 
 @pytest.mark.parametrize("p,d,n,kind", [(2, 3, 5, "trig"), (3, 2, 9, "fourier"), (2, 2, 6, "fourier"),
-                                        (3, 1, 12, "const"), (3, 3, 4, "fourier")])
+                                        (3, 1, 12, "const"), (3, 3, 4, "fourier"), (3, 3, 9, "grid"),
+                                        (2, 3, 7, "grid"), (3, 3, 4, "grid")])
 def test_csr_matches_ell(p, d, n, kind):
     """CSR values equal the ELL values at the structural columns, for every kernel family
     (separable, 2D tensor-core FOURIER incl. its shell pass, generic)."""
@@ -128,9 +129,14 @@ def test_csr_matches_ell(p, d, n, kind):
         desc = {"kind": "trig_sep", "c0": 1.0, "amp": 0.3, "trig": ("sin",) * d, "wavenum": (1,) * d}
     elif kind == "const":
         desc = {"kind": "const", "c0": 2.5}
+    elif kind == "grid":
+        desc = {"kind": "grid", "seed": 21, "sigma": 0.5}
     else:
         desc = inputs.coefficient({"kind": "fourier_logn", "seed": 7, "n_modes": 8, "amp": 0.3}, d)
-    c = api.coefficient(desc)
+    gt = None
+    if kind == "grid":
+        gt = torch.from_numpy(np.ascontiguousarray(inputs.lognormal_grid(n, seed=21, dim=d))).cuda()
+    c = api.coefficient(desc, gt, 0)
     ell = api.assemble(rules, c)
     lo, hi = min(17, rules.n_rows // 4), rules.n_rows - min(11, rules.n_rows // 4)
     row_ptr, col_idx, vals = api.assemble_csr(rules, c, row_begin=lo, row_end=hi)

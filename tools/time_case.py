@@ -24,7 +24,7 @@ ap.add_argument("--n", type=int, default=None)
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--dbg", default="0")
 ap.add_argument("--ld", type=int, default=None)
-ap.add_argument("--op", default="assemble", choices=["assemble", "load", "apply"])
+ap.add_argument("--op", default="assemble", choices=["assemble", "load", "apply", "csr"])
 a = ap.parse_args()
 cfg = inputs.config(a.config, a.n)
 rules = wgq.Rules(cfg["p"], cfg["n"], cfg["dim"])
@@ -34,6 +34,13 @@ if cfg["coeff"]["kind"] == "grid":
 coef = api.coefficient(inputs.coefficient(cfg["coeff"], cfg["dim"]), grid, plane0)
 out = {k: api.alloc_ell(rules, 0, rules.n_rows, a.ld) for k in cfg["kinds"]} if a.op == "assemble" else None
 u = torch.randn(rules.n_rows, dtype=torch.float64, device="cuda") if a.op == "apply" else None
+if a.op == "csr":
+    nnz = wgq.wgq_nnz(rules, 0, rules.n_rows)
+    row_ptr = torch.empty(rules.n_rows + 1, dtype=torch.int64, device="cuda")
+    col_idx = torch.empty(nnz, dtype=torch.int32, device="cuda")
+    wgq.wgq_csr_structure(rules, 0, rules.n_rows, row_ptr, col_idx)
+    vals = {k: torch.empty(nnz, dtype=torch.float64, device="cuda") for k in cfg["kinds"]}
+    descs = {k: wgq.make_out(vals[k], 0, rules.n_rows, ld=0, layout=wgq.WGQ_CSR, row_ptr=row_ptr) for k in cfg["kinds"]}
 bvec = torch.empty(rules.n_rows, dtype=torch.float64, device="cuda") if a.op == "load" else None
 
 
@@ -42,10 +49,16 @@ def run():
         api.assemble(rules, coef, cfg["kinds"], out=out)
     elif a.op == "load":
         api.assemble_load(rules, coef, out=bvec)
+    elif a.op == "csr":
+        if len(cfg["kinds"]) == 2:
+            wgq.wgq_assemble_mass_stiffness(rules, coef, descs["mass"], descs["stiffness"])
+        else:
+            wgq.wgq_assemble_mass(rules, coef, descs["mass"])
     else:
         api.apply(rules, coef, u, cfg["kinds"])
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
-alg = rules.n_rows * rules.stencil * 8 * len(cfg["kinds"]) if a.op == "assemble" else rules.n_rows * 8
+alg = (rules.n_rows * rules.stencil * 8 * len(cfg["kinds"]) if a.op == "assemble" else
+       wgq.wgq_nnz(rules, 0, rules.n_rows) * 8 * len(cfg["kinds"]) if a.op == "csr" else rules.n_rows * 8)
 res = {}
 for mode in a.dbg.split(","):
     os.environ["WGQ_LINE_DBG"] = mode
