@@ -340,11 +340,31 @@ struct TileDesc {
     int pad;           // staging offset aligning the tile's first element
     long long orow0;   // output row of the tile's first row
     int Xlo, Xhi, upos;  // apply: the tile's u columns [Xlo, Xhi], ring position of Xlo
-    // CSR: slab-local position of the tile's first entry, entries per x-row unit (a2 a3), the
-    // y/z validity boxes (offset indices lo..hi of the 2p+1) and a2
+};
+
+// CSR output only: slab-local position of the tile's first entry, entries per x-row unit
+// (a2 a3), the y/z validity boxes (offset indices lo..hi of the 2p+1) and a2.  Kept apart
+// from TileDesc so the ELL and apply kernels do not carry it.
+struct TileCsr {
     long long cs0;
     int w23, lo2, hi2, lo3, hi3, a2;
 };
+
+template <int P>
+__device__ __forceinline__ TileCsr make_csr(const LineArgs& a, const TileIt& t, int last_line) {
+    TileCsr d{};
+    if (t.line <= last_line) {
+        const long long N = a.N;
+        d.cs0 = csr_start((long long)t.line * N + t.t0, P, N) - a.csr_base;
+        d.a2 = (int)csr_a(t.i2, P, N);
+        d.w23 = d.a2 * (int)csr_a(t.i3, P, N);
+        d.lo2 = max(0, P - t.i2);
+        d.hi2 = min(2 * P, (int)N - 1 - t.i2 + P);
+        d.lo3 = max(0, P - t.i3);
+        d.hi3 = min(2 * P, (int)N - 1 - t.i3 + P);
+    }
+    return d;
+}
 
 template <int P>
 __device__ __forceinline__ TileDesc make_desc(const LineArgs& a, const TileIt& t, int last_line, bool padded) {
@@ -361,16 +381,6 @@ __device__ __forceinline__ TileDesc make_desc(const LineArgs& a, const TileIt& t
     d.Xlo = max(0, t.t0 - P);
     d.Xhi = t.uhi;
     d.upos = (t.lpos + d.Xlo - t.X0) % Cfg<P>::URING;
-    if (a.csr_base >= 0 && t.line <= last_line) {
-        const long long N = a.N;
-        d.cs0 = csr_start((long long)t.line * N + t.t0, P, N) - a.csr_base;
-        d.a2 = (int)csr_a(t.i2, P, N);
-        d.w23 = d.a2 * (int)csr_a(t.i3, P, N);
-        d.lo2 = max(0, P - t.i2);
-        d.hi2 = min(2 * P, (int)N - 1 - t.i2 + P);
-        d.lo3 = max(0, P - t.i3);
-        d.hi3 = min(2 * P, (int)N - 1 - t.i3 + P);
-    }
     return d;
 }
 
@@ -507,6 +517,7 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const __grid_const
     double* xbt = patches + C::PFD * C::PATCH;            // [4P rows][PM, PK][V][S]
 
     __shared__ TileDesc desc[8];                          // tiles k .. k+PFD (ring)
+    __shared__ TileCsr cdesc[CSR ? 8 : 1];
     constexpr int PFD = C::PFD;
     const int tid = threadIdx.x;
     const int n = a.n;
@@ -540,6 +551,7 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const __grid_const
     for (int k = 0; k < PFD; ++k) {
         tile_issue<P>(a, patches, qbufs, itP, prow, last_line, tid);
         if (tid == 0) desc[k] = make_desc<P>(a, itP, last_line, padded);
+        if (CSR && tid == 0) cdesc[k & (CSR ? 7 : 0)] = make_csr<P>(a, itP, last_line);
         if (itP.line <= last_line) it_next<P>(a, itP);
     }
     cp_async_wait<PFD - 1>();                             // tile 0 landed
@@ -555,7 +567,9 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const __grid_const
         const TileDesc d = desc[k & 7];
         if (d.line < 0) break;
         const TileDesc dA = desc[(k + 1) & 7];
-        const int pad = CSR ? (int)(d.cs0 & 1) : d.pad;
+        TileCsr dc{};
+        if (CSR) dc = cdesc[k & (CSR ? 7 : 0)];
+        const int pad = CSR ? (int)(dc.cs0 & 1) : d.pad;
         double* stM = stage + pad;
         double* stK = stage + C::STAGE + pad;
         // ---- S1: phase B of tile k ---------------------------------------------------------
@@ -594,13 +608,13 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const __grid_const
                 // CSR: row r's entries start at w23 (A(r) - A(t0)) in the tile; the thread's (o2, o3)
                 // group sits at pos23 = (o2 - lo2) + a2 (o3 - lo3) if inside the mesh, its o1 at o1 - lo1(r)
                 const int o2 = o23 % S, o3 = o23 / S;
-                if (o2 >= d.lo2 && o2 <= d.hi2 && o3 >= d.lo3 && o3 <= d.hi3) {
-                    const int pos23 = (o2 - d.lo2) + d.a2 * (o3 - d.lo3);
+                if (o2 >= dc.lo2 && o2 <= dc.hi2 && o3 >= dc.lo3 && o3 <= dc.hi3) {
+                    const int pos23 = (o2 - dc.lo2) + dc.a2 * (o3 - dc.lo3);
                     const long long At0 = csr_A(d.t0, P, a.N);
-                    const int off0 = (int)(d.w23 * (csr_A(r, P, a.N) - At0));
+                    const int off0 = (int)(dc.w23 * (csr_A(r, P, a.N) - At0));
                     const int ar0 = (int)csr_a(r, P, a.N);
                     if (r >= 2 * P && r + 1 <= n - 1 - P) {   // both rows class I: a(r) = 2p+1, lo1 = 0
-                        finish_pair_interior<P, MODE>(hm, hk, stM + off0 + S * pos23, stK + off0 + S * pos23, S * d.w23,
+                        finish_pair_interior<P, MODE>(hm, hk, stM + off0 + S * pos23, stK + off0 + S * pos23, S * dc.w23,
                                                       second, a);
                     } else {
                         const int lo1 = max(0, P - r), hi1 = min(2 * P, a.N - 1 - r + P);
@@ -616,7 +630,7 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const __grid_const
                                 hm1[v] = shift ? hm[v + 1] : hm[v];
                                 hk1[v] = shift ? hk[v + 1] : hk[v];
                             }
-                            const int off1 = (int)(d.w23 * (csr_A(r1, P, a.N) - At0));
+                            const int off1 = (int)(dc.w23 * (csr_A(r1, P, a.N) - At0));
                             const int lo1b = max(0, P - r1), hi1b = min(2 * P, a.N - 1 - r1 + P);
                             double* dM1 = stM + off1 + (int)csr_a(r1, P, a.N) * pos23 - lo1b;
                             double* dK1 = stK + off1 + (int)csr_a(r1, P, a.N) * pos23 - lo1b;
@@ -631,9 +645,9 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const __grid_const
         // ---- S2: store tile k, phase A of tile k+1, prefetch tile k+3 --------------------
         if (tid < 32 && !(a.dbg & 2)) {
             if (CSR) {
-                const long long total = (long long)d.w23 * (csr_A(d.t0 + d.tr, P, a.N) - csr_A(d.t0, P, a.N));
-                if (MODE & 1) store_run(a.M, stM, d.cs0, (int)total, tid);
-                if (MODE & 2) store_run(a.K, stK, d.cs0, (int)total, tid);
+                const long long total = (long long)dc.w23 * (csr_A(d.t0 + d.tr, P, a.N) - csr_A(d.t0, P, a.N));
+                if (MODE & 1) store_run(a.M, stM, dc.cs0, (int)total, tid);
+                if (MODE & 2) store_run(a.K, stK, dc.cs0, (int)total, tid);
             } else {
                 if (MODE & 1) store_mat<P>(a, a.M, stM, d.orow0, d.tr, SRr, padded, tid);
                 if (MODE & 2) store_mat<P>(a, a.K, stK, d.orow0, d.tr, SRr, padded, tid);
@@ -644,6 +658,7 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const __grid_const
         if (a.dbg & 4) asm volatile("cp.async.commit_group;" ::: "memory");
         else tile_issue<P>(a, patches, qbufs, itP, prow, last_line, tid);    // tile k+PFD
         if (tid == 0) desc[(k + PFD) & 7] = make_desc<P>(a, itP, last_line, padded);
+        if (CSR && tid == 0) cdesc[(k + PFD) & (CSR ? 7 : 0)] = make_csr<P>(a, itP, last_line);
         if (itP.line <= last_line) it_next<P>(a, itP);
         cp_async_wait<PFD - 2>();                                  // tile k+2 landed
         if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // staging free
