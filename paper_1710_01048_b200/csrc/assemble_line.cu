@@ -402,7 +402,7 @@ template <int P, int NT = Cfg<P>::NT, int HS = Cfg<P>::S2>
 __device__ __forceinline__ void phase_a(const LineArgs& a, const TileDesc& t, const double* patches,
                                         const double* qbufs, double* Hm, double* Hk, int tid) {
     using C = Cfg<P>;
-    constexpr int V = C::V, S = C::S, S2 = C::S2, RING = C::RING;
+    constexpr int V = C::V, S = C::S, RING = C::RING;
     constexpr int KS = (V + 3) / 4;                    // k-steps of 4 (p=3: 2, p=2: 1)
     constexpr int NW = NT / 32;
     const int lane = tid & 31, warp = tid >> 5, g = lane >> 2, tq = lane & 3;
