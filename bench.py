@@ -386,6 +386,14 @@ def run_extras(rules5, coef5, peak):
     ms = _time_ms(lambda: api.apply(rules5, coef5, u), flush=flush)
     out["operators"]["apply_MK_C5"] = {"ms": round(ms, 4), "rows_per_s": n_rows / (ms / 1e3),
                                        "note": "matrix-free y_M = M u and y_K = K u, nothing stored"}
+    # the paper's own cost metric (context): basis evaluations for its 2D 100x100 test
+    # problem, weighted Gaussian (this library's rules) vs the weighted Newton-Cotes point sets
+    out["paper_eval_counts_2d_100x100_mass"] = {}
+    for pp in (2, 3):
+        g, c = wgq.wgq_eval_counts(wgq.Rules(pp, 100, 2), wgq.WGQ_MASS)
+        out["paper_eval_counts_2d_100x100_mass"][f"p{pp}"] = {
+            "gaussian": g, "newton_cotes": c, "ratio": round(c / g, 4),
+            "paper_ratio": {2: 2.08, 3: 2.44}[pp], "interior_ratio": round({2: (13 / 9) ** 2, 3: (25 / 16) ** 2}[pp], 4)}
     # peak microbenchmarks of this box, same session (tools/peaks.cu, built by build())
     exe = os.path.join(ROOT, "tools", "peaks")
     if os.path.exists(exe):
