@@ -331,7 +331,7 @@ def main():
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": cfg["name"], "p": p, "n_elems": n, "dim": d, "kinds": list(kinds),
                            "coefficient": cfg["coeff"]["kind"], "rows": rules.n_rows, "ld": ld,
-                           "layout": "ELL", "parallelism": f"z-slab x{world}",
+                           "layout": "ELL", "parallelism": f"line-granular z-slabs x{world}",
                            "l2": "flushed (512 MB write) between timed steps; outputs >> L2"},
                 "gpu_launches": args.steps * 1,
                 "roofline": roof, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu, "extras": extras,

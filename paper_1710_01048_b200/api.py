@@ -10,14 +10,17 @@ from . import wgq
 
 
 def slab_rows(N, dim, rank, world):
-    """Row range [b, e) of rank's slab: contiguous planes of the slowest row index,
-    planes split as evenly as possible (the first N % world ranks get one more)."""
-    planes = N
-    base, extra = divmod(planes, world)
-    z0 = rank * base + min(rank, extra)
-    z1 = z0 + base + (1 if rank < extra else 0)
-    plane_rows = N ** (dim - 1)
-    return z0 * plane_rows, z1 * plane_rows
+    """Row range [b, e) of rank's slab: contiguous rows along the slowest axes, split into
+    whole x-lines (N rows; single rows in 1D) as evenly as possible (the first lines % world
+    ranks get one more line).  Line granularity keeps the ranks within one line (0.01 % at C5
+    on 8 GPUs) instead of one z-plane (1.9 %) of each other; a slab may start or end inside a
+    z-plane, which every kernel and the halo logic handle."""
+    unit = N if dim >= 2 else 1
+    units = N ** dim // unit
+    base, extra = divmod(units, world)
+    u0 = rank * base + min(rank, extra)
+    u1 = u0 + base + (1 if rank < extra else 0)
+    return u0 * unit, u1 * unit
 
 
 def grid_planes_for(rules, row_begin, row_end):

@@ -1,13 +1,14 @@
 """Multi-GPU plumbing (one process per GPU, torch.distributed): row slabs, the coefficient
 halo, and the final reductions.
 
-Rows are independent: rank r owns the contiguous z-planes (3D; y-lines in 2D) of
-``api.slab_rows`` and assembles them with no data-path collective.  The only exchanges are
+Rows are independent: rank r owns the contiguous x-lines of ``api.slab_rows`` (a
+range along the slowest axes) and assembles them with no data-path collective.  The only exchanges are
 * ``exchange_halo`` -- for a user-supplied (not seeded) vertex field distributed by owned
   planes, the p planes below and the 1 plane above a rank's rows (NCCL P2P over NVLink;
   a seeded field is instead regenerated per rank by ``wgq_generate_grid``), and
-* ``exchange_u_halo`` -- for the matrix-free product (``wgq_apply``), the p row planes of u
-  below and above a rank's slab (the columns its rows touch), P2P from the neighbours, and
+* ``exchange_u_halo`` -- for the matrix-free product (``wgq_apply``), the rows of u in the
+  p planes below and above a rank's slab (the columns its rows touch), P2P from the
+  neighbours, and
 * ``reduce_checks`` / ``max_time`` -- checksum, norms and the max-over-ranks step time.
 Everything here is host logic; the arithmetic of the method stays in libwgq.
 """
@@ -71,38 +72,36 @@ def exchange_halo(owned, p, n, N, dim, group=None):
     return out, lo
 
 
-def needed_u_planes(p, N, dim, rank, world):
-    """Row planes [lo, hi) of u that the rank's rows touch: its planes +- p, clipped."""
+def needed_u_rows(p, N, dim, rank, world):
+    """Rows [lo, hi) of u that the rank's rows touch: the slowest-axis planes of its slab
+    +- p (clipped), as global row ids."""
     plane_rows = N ** (dim - 1)
     b, e = api.slab_rows(N, dim, rank, world)
     if e <= b:
         return 0, 0
+    if dim == 1:
+        return max(0, b - p), min(N, e + p)
     z0, z1 = b // plane_rows, (e - 1) // plane_rows
-    return max(0, z0 - p), min(N, z1 + p + 1)
+    return max(0, z0 - p) * plane_rows, min(N, z1 + p + 1) * plane_rows
 
 
 def exchange_u_halo(u_owned, p, N, dim, group=None):
-    """Given this rank's slab of u (its own rows, flat), return (u_ext, u_row0): u over the row
-    planes its rows touch (own planes plus p halo planes each side, from the neighbours) and the
-    global row id of u_ext[0], ready for ``wgq_apply``.  P2P sends of whole planes."""
+    """Given this rank's slab of u (its own rows, flat), return (u_ext, u_row0): u over the rows
+    its rows touch (own rows plus the halo from the neighbours) and the global row id of
+    u_ext[0], ready for ``wgq_apply``.  P2P sends of contiguous row ranges."""
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
-    plane_rows = N ** (dim - 1)
-    own = []
-    for r in range(world):
-        b, e = api.slab_rows(N, dim, r, world)
-        own.append((b // plane_rows, e // plane_rows))
-    need = [needed_u_planes(p, N, dim, r, world) for r in range(world)]
+    own = [api.slab_rows(N, dim, r, world) for r in range(world)]
+    need = [needed_u_rows(p, N, dim, r, world) for r in range(world)]
     lo, hi = need[rank]
-    planes = u_owned.reshape(-1, plane_rows)
-    out = torch.empty((max(hi - lo, 0), plane_rows), dtype=u_owned.dtype, device=u_owned.device)
+    out = torch.empty(max(hi - lo, 0), dtype=u_owned.dtype, device=u_owned.device)
     reqs = []
     for src in range(world):
         a, b = max(lo, own[src][0]), min(hi, own[src][1])
         if a >= b:
             continue
         if src == rank:
-            out[a - lo:b - lo] = planes[a - own[rank][0]:b - own[rank][0]]
+            out[a - lo:b - lo] = u_owned[a - own[rank][0]:b - own[rank][0]]
         else:
             reqs.append(dist.irecv(out[a - lo:b - lo], src=src, group=group))
     for dst in range(world):
@@ -111,10 +110,10 @@ def exchange_u_halo(u_owned, p, N, dim, group=None):
         a, b = max(need[dst][0], own[rank][0]), min(need[dst][1], own[rank][1])
         if a >= b:
             continue
-        reqs.append(dist.isend(planes[a - own[rank][0]:b - own[rank][0]].contiguous(), dst=dst, group=group))
+        reqs.append(dist.isend(u_owned[a - own[rank][0]:b - own[rank][0]].contiguous(), dst=dst, group=group))
     for r in reqs:
         r.wait()
-    return out.reshape(-1), lo * plane_rows
+    return out, lo
 
 
 def apply_distributed(rules, coeff, u_owned, kinds=("mass", "stiffness"), group=None, stream=None):

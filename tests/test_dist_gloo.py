@@ -42,8 +42,8 @@ def _worker(rank, world, port, p, n, dim, q):
         b, e = api.slab_rows(N, dim, rank, world)
         u_ext, u0 = wdist.exchange_u_halo(u_full[b:e].clone(), p, N, dim)
         plane_rows = N ** (dim - 1)
-        ulo, uhi = wdist.needed_u_planes(p, N, dim, rank, world)
-        ok_u = (u0 == ulo * plane_rows and torch.equal(u_ext, u_full[ulo * plane_rows:uhi * plane_rows])
+        ulo, uhi = wdist.needed_u_rows(p, N, dim, rank, world)
+        ok_u = (u0 == ulo and torch.equal(u_ext, u_full[ulo:uhi])
                 and (e <= b or (u0 <= max(0, b // plane_rows - p) * plane_rows
                                 and u0 + u_ext.numel() >= min(N, (e - 1) // plane_rows + p + 1) * plane_rows)))
         ok_halo = ok_halo and ok_u
@@ -76,7 +76,8 @@ def test_halo_reductions_and_slabs(world, p, n, dim):
     assert slabs[0][0] == 0 and slabs[-1][1] == N ** dim
     assert all(slabs[i][1] == slabs[i + 1][0] for i in range(world - 1))
     sizes = [e - b for b, e in slabs]
-    assert max(sizes) - min(sizes) <= N ** (dim - 1)           # plane-granular balance
+    assert max(sizes) - min(sizes) <= N                        # line-granular balance
+    assert all(b % N == 0 for b, _ in slabs)                   # whole x-lines
     for rank, ok_halo, h, s1, s2, t, _ in res:
         assert ok_halo, rank
         expect_h = ((2 ** 63 - 5) + 11 * (world - 1)) % 2 ** 64
