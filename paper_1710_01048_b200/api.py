@@ -106,3 +106,18 @@ def apply(rules, coeff, u, kinds=("mass", "stiffness"), row_begin=0, row_end=Non
     y = {k: torch.empty(rows, dtype=torch.float64, device="cuda") for k in kinds}
     wgq.wgq_apply(rules, coeff, u, u_row0, row_begin, row_end, y.get("mass"), y.get("stiffness"), stream)
     return y
+
+
+def rules_json(rules):
+    """The handle's unit-spacing rules as JSON: a list of
+    {kind, degree, class, nodes[], weights[], residual_max}, nodes / weights with 17
+    significant digits; class 0..p-1 = left boundary weight j, "interior" = the shift-invariant rule."""
+    import json
+    out = []
+    for kind, kc in (("mass", wgq.WGQ_MASS), ("stiffness", wgq.WGQ_STIFFNESS)):
+        for cls in range(rules.p + 1):
+            tau, om, res = wgq.wgq_rules_query(rules, cls, kc)
+            out.append({"kind": kind, "degree": rules.p, "class": "interior" if cls == rules.p else cls,
+                        "nodes": [float(f"{x:.17g}") for x in tau], "weights": [float(f"{w:.17g}") for w in om],
+                        "residual_max": float(res)})
+    return json.dumps(out, indent=1)

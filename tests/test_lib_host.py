@@ -137,3 +137,21 @@ def test_operator_argument_errors(L):
     assert L.wgq_apply(r.handle, ctypes.byref(c), 8, lo + N * N, hi - lo - N * N, rb, re_, 8, None, None) == wgq.WGQ_ERANGE
     assert L.wgq_apply(r.handle, ctypes.byref(c), 8, lo, hi - lo - N * N, rb, re_, 8, None, None) == wgq.WGQ_ERANGE
     assert L.wgq_apply(r.handle, ctypes.byref(c), 8, lo, hi - lo, 7, 7, 8, None, None) == wgq.WGQ_OK   # empty range
+
+
+def test_rules_json_export(L):
+    """rule tables exportable as JSON {kind, degree, nodes[], weights[], residual_max}."""
+    import json
+
+    from paper_1710_01048_b200 import api
+    for p in (2, 3):
+        r = wgq.Rules(p, 10, 1)
+        doc = json.loads(api.rules_json(r))
+        assert len(doc) == 2 * (p + 1)
+        for entry in doc:
+            assert set(entry) == {"kind", "degree", "class", "nodes", "weights", "residual_max"}
+            assert entry["degree"] == p and entry["residual_max"] < 1e-13
+            kc = wgq.WGQ_MASS if entry["kind"] == "mass" else wgq.WGQ_STIFFNESS
+            cls = p if entry["class"] == "interior" else entry["class"]
+            tau, om, _ = wgq.wgq_rules_query(r, cls, kc)
+            assert entry["nodes"] == list(tau) and entry["weights"] == list(om)   # 17 digits round-trip exactly
