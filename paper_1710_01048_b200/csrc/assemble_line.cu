@@ -737,7 +737,7 @@ __global__ void __launch_bounds__(256, 3) k_line_apply(const __grid_constant__ L
                     ubase[m] = (iy >= 0 && iy < N && iz >= 0 && iz < N) ? (long long)iz * N2 + (long long)iy * N - a.u_row0 : -1;
                 }
             }
-            const int nx = t.uhi - t.ulo + 1;
+            const int nx = (a.dbg & 16) ? 0 : t.uhi - t.ulo + 1;
             const int rpos = t.lpos - t.X0;
 #pragma unroll
             for (int m = 0; m < MU; ++m) {
@@ -795,7 +795,7 @@ __global__ void __launch_bounds__(256, 3) k_line_apply(const __grid_constant__ L
         }
         __syncthreads();
         // ---- S1b: rows of tile k (one per warp), phase A of tile k+1, prefetch tile k+PFD ----
-        if (warp == 0) {
+        if (warp == 0 && !(a.dbg & 32)) {
             // warp 0 finishes all rows of the tile: lane (j, vq) = row t0 + j, vertex planes
             // vx = vq (+4); y = sum_{vx,o1} P[vx][o1] D(b_r + vx, r - p + o1), reduced over 4 lanes
             const int j = lane >> 2, vq = lane & 3;
