@@ -47,9 +47,9 @@ def build(force=False, verbose=False):
     subprocess.run(cmd, check=True)
     # peak microbenchmarks (write-only HBM, copy, DFMA) used by bench.py's extras
     peaks_src = os.path.join(ROOT, "tools", "peaks.cu")
-    if os.path.exists(peaks_src):
+    if os.path.exists(peaks_src):                 # optional tool: a failure here never fails the build
         subprocess.run([NVCC, "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-o",
-                        os.path.join(ROOT, "tools", "peaks"), peaks_src], check=True)
+                        os.path.join(ROOT, "tools", "peaks"), peaks_src], check=False)
     return LIB
 
 
