@@ -25,8 +25,10 @@ the paper (``PAPER.md``, cited as ``P:<line>`` with the LaTeX equation label):
                      y = A u by the plain definition.
 * ``counts``      -- basis-evaluation counts of the Gaussian vs Newton-Cotes weighted
                      schemes (experiment E3).
+* ``eigen``       -- the Dirichlet eigenvalue experiments E1/E2 (SURVEY
+                     §8(f) row 4): dense K_II v = λ M_II v and the exact π² Σ k².
 
 It shares no code, tables or constants with the CUDA library.  The seeded input
 generators in ``inputs/`` are the only module both sides use.
 """
-from . import spline, quadrature, rules, coeff, assemble, elementwise, operators, counts  # noqa: F401
+from . import spline, quadrature, rules, coeff, assemble, elementwise, operators, counts, eigen  # noqa: F401

@@ -4,6 +4,7 @@
     python -m paper_1710_01048_b200 counts --degree 2 --dim 2 --mesh 100
     python -m paper_1710_01048_b200 assemble --degree 3 --dim 3 --mesh 64 [--coef grid|const|trig|fourier]
                                       [--kinds mass,stiffness] [--layout ell|csr] [--mtx out_prefix]
+    python -m paper_1710_01048_b200 eigen --degree 2 --dim 1 --mesh 1000 [--count 10]
 
 Exit codes: 0 success, 2 validation failure (a rule residual above tolerance),
 3 solver failure (WGQ_ENOCONV), 4 configuration error (bad arguments, WGQ_EINVAL /
@@ -111,6 +112,17 @@ def cmd_assemble(a):
     return EXIT_OK
 
 
+def cmd_eigen(a):
+    from . import api, eigen, wgq
+    rules = wgq.Rules(a.degree, a.mesh, a.dim)
+    lam = eigen.spectrum(rules, api.coefficient({"kind": "const", "c0": 1.0})).cpu().tolist()
+    count = min(a.count, len(lam))
+    ex = eigen.exact_eigenvalues(a.dim, count)
+    print(json.dumps({"dofs": len(lam), "exact": ex, "discrete": lam[:count],
+                      "rel_err": [float(f"{lam[k] / ex[k] - 1:.17g}") for k in range(count)]}, indent=1))
+    return EXIT_OK
+
+
 def main(argv=None):
     ap = argparse.ArgumentParser(prog="python -m paper_1710_01048_b200", description=__doc__,
                                  formatter_class=argparse.RawDescriptionHelpFormatter)
@@ -133,13 +145,18 @@ def main(argv=None):
     s.add_argument("--kinds", default="mass,stiffness")
     s.add_argument("--layout", choices=["ell", "csr"], default="ell")
     s.add_argument("--mtx", default=None, help="write MatrixMarket files <prefix>_<kind>.mtx")
+    e = sub.add_parser("eigen", help="Dirichlet Laplacian spectrum from the assembled M, K (E1/E2)")
+    e.add_argument("--degree", type=int, required=True)
+    e.add_argument("--dim", type=int, default=1)
+    e.add_argument("--mesh", type=int, required=True)
+    e.add_argument("--count", type=int, default=10)
     try:
         a = ap.parse_args(argv)
     except SystemExit as e:
         return EXIT_CONFIG if e.code else EXIT_OK
     from . import wgq
     try:
-        return {"derive-rules": cmd_derive_rules, "counts": cmd_counts, "assemble": cmd_assemble}[a.cmd](a)
+        return {"derive-rules": cmd_derive_rules, "counts": cmd_counts, "assemble": cmd_assemble, "eigen": cmd_eigen}[a.cmd](a)
     except wgq.WgqError as err:
         print(str(err), file=sys.stderr)
         return _exit_for(err)

@@ -51,3 +51,12 @@ def test_assemble_command_writes_matrix_market(tmp_path):
         A[int(i) - 1, int(j) - 1] = float(v)
     assert n == 8 and nnz == len(lines) - 2
     assert np.allclose(A, A.T, atol=1e-15) and abs(A.sum() - 1.0) < 1e-14      # c = 1: symmetric, sum = |[0,1]|
+
+
+@pytest.mark.gpu
+def test_eigen_command(capsys):
+    assert main(["eigen", "--degree", "3", "--dim", "1", "--mesh", "64", "--count", "5"]) == 0
+    doc = json.loads(capsys.readouterr().out)
+    assert doc["dofs"] == 65 and len(doc["rel_err"]) == 5
+    assert all(0 <= e < 1e-5 for e in doc["rel_err"])             # Rayleigh-Ritz: from above
+    assert abs(doc["exact"][0] - np.pi ** 2) < 1e-12
