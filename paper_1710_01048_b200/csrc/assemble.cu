@@ -220,6 +220,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32) k_assemble_generic(const Gener
     extern __shared__ double smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int warps = blockDim.x >> 5;
+    const uint64_t pol = pol_evict_first();
     double* W = smem + warp * a.sg.per_warp;
     double* T1 = W + a.sg.w;
     double* T2 = T1 + a.sg.t1;
@@ -311,8 +312,8 @@ __global__ void __launch_bounds__(kMaxWarps * 32) k_assemble_generic(const Gener
             const int slot = lane + 32 * j;
             if (slot >= NS) continue;
             if (a.M.layout == WGQ_ELL) {
-                if (a.do_mass) a.M.values[orow * a.M.ld + slot] = accM[j] + 0.0;
-                if (a.do_stiff) a.K.values[orow * a.K.ld + slot] = accK[j] + 0.0;
+                if (a.do_mass) st_stream(a.M.values + orow * a.M.ld + slot, accM[j] + 0.0, pol);
+                if (a.do_stiff) st_stream(a.K.values + orow * a.K.ld + slot, accK[j] + 0.0, pol);
             } else {
                 // CSR: slot -> compacted position inside the box of valid offsets
                 int o[3] = {slot % S1 - P, (slot / S1) % S2 - (D >= 2 ? P : 0), slot / (S1 * S2) - (D >= 3 ? P : 0)};
@@ -327,8 +328,8 @@ __global__ void __launch_bounds__(kMaxWarps * 32) k_assemble_generic(const Gener
                     stride *= hi - lo + 1;
                 }
                 if (!ok) continue;
-                if (a.do_mass) a.M.values[a.M.row_ptr[orow] + pos] = accM[j] + 0.0;
-                if (a.do_stiff) a.K.values[a.K.row_ptr[orow] + pos] = accK[j] + 0.0;
+                if (a.do_mass) st_stream(a.M.values + a.M.row_ptr[orow] + pos, accM[j] + 0.0, pol);
+                if (a.do_stiff) st_stream(a.K.values + a.K.row_ptr[orow] + pos, accK[j] + 0.0, pol);
             }
         }
         __syncwarp();

@@ -118,4 +118,19 @@ int launch_sep(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, c
 int launch_generate_grid(int64_t n, int dim, uint64_t seed, double sigma, int64_t plane0,
                          int64_t planes, double* grid, void* stream);
 
+
+#ifdef __CUDACC__
+// Streaming output stores of the assembled values: no L1 allocation and L2 evict-first, so the
+// write stream neither evicts the small per-row tables from L1 nor the coefficient data from L2
+// (C4: 0.45 -> 0.36 ms).
+__device__ __forceinline__ uint64_t pol_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void st_stream(double* p, double v, uint64_t pol) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+#endif
+
 }  // namespace wgq

@@ -133,6 +133,7 @@ __global__ void __launch_bounds__(256) k_sep(const SepArgs a) {
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int64_t rows = a.row_end - a.row_begin;
+    const uint64_t pol = pol_evict_first();
     for (int64_t c0row = warp * kChunkRows; c0row < rows; c0row += nwarps * kChunkRows) {
         const int64_t nrows = min((int64_t)kChunkRows, rows - c0row);
         const int64_t first = a.row_begin + c0row;
@@ -163,13 +164,13 @@ __global__ void __launch_bounds__(256) k_sep(const SepArgs a) {
             if (a.layout == WGQ_CSR) cpos = csr_pos<P_, D>(o, idx, a.N);
             if (MODE & 1) {
                 const double m = sep_mass(a.c0, a.amp, f[0][0], f[0][1], P, Q);
-                if (a.layout == WGQ_ELL) a.Mv[row * a.ldM + slot] = m;
-                else if (cpos >= 0) a.Mv[a.rpM[row] + cpos] = m;
+                if (a.layout == WGQ_ELL) st_stream(a.Mv + row * a.ldM + slot, m, pol);
+                else if (cpos >= 0) st_stream(a.Mv + a.rpM[row] + cpos, m, pol);
             }
             if (MODE & 2) {
                 const double k = sep_stiff<D>(a.c0, a.amp, f[0][0], f[0][1], f[0][2], f[0][3], P, Q, PK, QK);
-                if (a.layout == WGQ_ELL) a.Kv[row * a.ldK + slot] = k;
-                else if (cpos >= 0) a.Kv[a.rpK[row] + cpos] = k;
+                if (a.layout == WGQ_ELL) st_stream(a.Kv + row * a.ldK + slot, k, pol);
+                else if (cpos >= 0) st_stream(a.Kv + a.rpK[row] + cpos, k, pol);
             }
             // advance 32 elements: slot += 32, carrying whole rows into the row indices
             slot += 32;
@@ -192,6 +193,7 @@ __global__ void __launch_bounds__(256) k_sep(const SepArgs a) {
 // slots l + 32 j of every row (j < R); the y/z factors of those slots are line constants kept
 // in registers (P = uM2 uM3, Q = vM2 vM3 and the stiffness combinations PK, QK), so a row
 // costs each lane the four x-factors of its slots, a few FMAs and coalesced 256-byte stores.
+
 constexpr int kSepSeg = 32;
 
 template <int P, int D, int MODE>
@@ -209,6 +211,7 @@ __global__ void __launch_bounds__(256) k_sep_line(const SepArgs a) {
     int o1[R];
 #pragma unroll
     for (int j = 0; j < R; ++j) o1[j] = (lane + 32 * j) % S;
+    const uint64_t pol = pol_evict_first();
     for (int64_t it = warp; it < items; it += nwarps) {
         const int64_t line = line0 + it / segs;
         const int64_t x0 = max((it % segs) * kSepSeg, a.row_begin - line * N);
@@ -231,19 +234,40 @@ __global__ void __launch_bounds__(256) k_sep_line(const SepArgs a) {
             }
             sep_consts<D>(f2, f3, cP[j], cQ[j], cPK[j], cQK[j]);
         }
+        // the x-direction vectors of the next row are loaded while the current row is stored
+        double xu[R], xv[R], xuk[R], xvk[R];
+        auto load_x = [&](int64_t i1) {
+            const double* t1 = a.sep + i1 * 4 * kMaxS;
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+                xu[j] = __ldg(t1 + o1[j]);
+                xv[j] = __ldg(t1 + kMaxS + o1[j]);
+                if (MODE & 2) {
+                    xuk[j] = __ldg(t1 + 2 * kMaxS + o1[j]);
+                    xvk[j] = __ldg(t1 + 3 * kMaxS + o1[j]);
+                }
+            }
+        };
+        load_x(x0);
         for (int64_t i1 = x0; i1 < x1; ++i1) {
             const int64_t orow = line * N + i1 - a.row_begin;
-            const double* t1 = a.sep + i1 * 4 * kMaxS;
+            double cu[R], cv[R], cuk[R], cvk[R];
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+                cu[j] = xu[j];
+                cv[j] = xv[j];
+                cuk[j] = (MODE & 2) ? xuk[j] : 0.0;
+                cvk[j] = (MODE & 2) ? xvk[j] : 0.0;
+            }
+            if (i1 + 1 < x1) load_x(i1 + 1);
 #pragma unroll
             for (int j = 0; j < R; ++j) {
                 const int slot = lane + 32 * j;
                 if (slot >= NS) continue;
-                const double uM1 = __ldg(t1 + o1[j]), vM1 = __ldg(t1 + kMaxS + o1[j]);
-                if (MODE & 1) a.Mv[orow * a.ldM + slot] = sep_mass(a.c0, a.amp, uM1, vM1, cP[j], cQ[j]);
-                if (MODE & 2) {
-                    const double uK1 = __ldg(t1 + 2 * kMaxS + o1[j]), vK1 = __ldg(t1 + 3 * kMaxS + o1[j]);
-                    a.Kv[orow * a.ldK + slot] = sep_stiff<D>(a.c0, a.amp, uM1, vM1, uK1, vK1, cP[j], cQ[j], cPK[j], cQK[j]);
-                }
+                if (MODE & 1) st_stream(a.Mv + orow * a.ldM + slot, sep_mass(a.c0, a.amp, cu[j], cv[j], cP[j], cQ[j]), pol);
+                if (MODE & 2)
+                    st_stream(a.Kv + orow * a.ldK + slot, sep_stiff<D>(a.c0, a.amp, cu[j], cv[j], cuk[j], cvk[j], cP[j],
+                                                                       cQ[j], cPK[j], cQK[j]), pol);
             }
         }
     }
