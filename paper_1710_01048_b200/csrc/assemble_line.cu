@@ -54,7 +54,6 @@ struct Cfg {
 #endif
     static constexpr int PFD = WGQ_LINE_PFD;           // prefetch distance (tiles) = patch / Q buffers
     static constexpr int XB = 4 * P * 2 * V * S;       // x-boundary rows' vertex tables
-    static constexpr int URING = 48;                   // u columns (apply): window + prefetched columns
     static constexpr int SMEM = 2 * STAGE + RING * 2 * S2 + PFD * 4 * V * S + PFD * PATCH + XB;
     static_assert(W <= RING, "ring too small");
 };
@@ -238,6 +237,18 @@ __device__ __forceinline__ void finish_general(const double* pm, const double* h
     }
 }
 
+// The apply's tiles carry little arithmetic, so its tile period is short and the vertex-patch /
+// u-column loads need a longer lead than the assembly's: PFD tiles ahead, the u ring sized for
+// the current window (<= TR + 2p columns) plus PFD tiles of new columns (<= TR + p each).
+#ifndef WGQ_APPLY_PFD
+#define WGQ_APPLY_PFD 3
+#endif
+struct ApplyCfg {
+    static constexpr int PFD = WGQ_APPLY_PFD;
+    static constexpr int URING = 16 + 11 * PFD;
+    static_assert(PFD >= 2 && PFD <= 6, "desc ring holds tiles k .. k+PFD in 8 slots");
+};
+
 // Iterator over a CTA's tiles: lines first_line + blockIdx.x + m * gridDim.x, TR rows per
 // tile.  Per-line quantities are refreshed only when the line changes, so the per-tile cost
 // (paid by every thread of the CTA) is a few adds and compares.
@@ -280,14 +291,14 @@ __device__ __forceinline__ void it_init(const LineArgs& a, TileIt& t) {
     it_planes<P>(t, a.N);
 }
 
-template <int P>
+template <int P, int PFD_ = Cfg<P>::PFD, int URING_ = ApplyCfg::URING>
 __device__ __forceinline__ void it_next(const LineArgs& a, TileIt& t) {
     t.t0 += Cfg<P>::TR;
-    t.ps = t.ps == Cfg<P>::PFD - 1 ? 0 : t.ps + 1;
+    t.ps = t.ps == PFD_ - 1 ? 0 : t.ps + 1;
     if (t.t0 >= t.x1) {
-        t.lpos = (t.lpos + min(a.N - 1, t.x1 - 1 + P) - t.X0 + 1) % Cfg<P>::URING;   // finished line's columns
+        t.lpos = (t.lpos + min(a.N - 1, t.x1 - 1 + P) - t.X0 + 1) % URING_;   // finished line's columns
         t.line += gridDim.x;
-        t.qs = t.qs == Cfg<P>::PFD - 1 ? 0 : t.qs + 1;
+        t.qs = t.qs == PFD_ - 1 ? 0 : t.qs + 1;
         it_line<P>(a, t);
     }
     it_planes<P>(t, a.N);
@@ -366,7 +377,7 @@ __device__ __forceinline__ TileCsr make_csr(const LineArgs& a, const TileIt& t, 
     return d;
 }
 
-template <int P>
+template <int P, int URING_ = ApplyCfg::URING>
 __device__ __forceinline__ TileDesc make_desc(const LineArgs& a, const TileIt& t, int last_line, bool padded) {
     TileDesc d;
     d.line = t.line <= last_line ? t.line : -1;
@@ -380,7 +391,7 @@ __device__ __forceinline__ TileDesc make_desc(const LineArgs& a, const TileIt& t
     d.pad = padded ? 0 : (int)((d.orow0 * a.ld) & 1);
     d.Xlo = max(0, t.t0 - P);
     d.Xhi = t.uhi;
-    d.upos = (t.lpos + d.Xlo - t.X0) % Cfg<P>::URING;
+    d.upos = (t.lpos + d.Xlo - t.X0) % URING_;
     return d;
 }
 
@@ -682,7 +693,7 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const __grid_const
 template <int P, int MODE>
 __global__ void __launch_bounds__(256, 3) k_line_apply(const __grid_constant__ LineArgs a) {
     using C = Cfg<P>;
-    constexpr int S = C::S, S2 = C::S2, V = C::V, RING = C::RING, URING = C::URING, PFD = C::PFD;
+    constexpr int S = C::S, S2 = C::S2, V = C::V, RING = C::RING, URING = ApplyCfg::URING, PFD = ApplyCfg::PFD;
     // 8 warps: one D item, one phase-A plane and one output row each per tile
     constexpr int NT = 256;
     constexpr int HS = (S2 + 3) / 4 * 4 + ((S2 + 3) / 4 % 2 == 0 ? 4 : 0);   // row stride = 4 (mod 8): conflict-free fragments
@@ -757,8 +768,8 @@ __global__ void __launch_bounds__(256, 3) k_line_apply(const __grid_constant__ L
     it_init<P>(a, itP);
     for (int k = 0; k < PFD; ++k) {
         issue(itP, prow);
-        if (tid == 0) desc[k] = make_desc<P>(a, itP, last_line, false);
-        if (itP.line <= last_line) it_next<P>(a, itP);
+        if (tid == 0) desc[k] = make_desc<P, URING>(a, itP, last_line, false);
+        if (itP.line <= last_line) it_next<P, PFD, URING>(a, itP);
     }
     cp_async_wait<PFD - 1>();
     __syncthreads();
@@ -795,46 +806,40 @@ __global__ void __launch_bounds__(256, 3) k_line_apply(const __grid_constant__ L
         }
         __syncthreads();
         // ---- S1b: rows of tile k (one per warp), phase A of tile k+1, prefetch tile k+PFD ----
-        if (warp == 0 && !(a.dbg & 32)) {
-            // warp 0 finishes all rows of the tile: lane (j, vq) = row t0 + j, vertex planes
-            // vx = vq (+4); y = sum_{vx,o1} P[vx][o1] D(b_r + vx, r - p + o1), reduced over 4 lanes
-            const int j = lane >> 2, vq = lane & 3;
+        if (warp < d.tr && !(a.dbg & 32)) {
+            // warp j finishes row t0 + j: lane = (vx, o1) pair (vx < 4; lanes < S also take vx = 4),
+            // y = sum_{vx,o1} P[vx][o1] D(b_r + vx, r - p + o1), reduced over the warp
+            const int r = d.t0 + warp, br = max(0, r - P);
+            const bool interior = r >= 2 * P && r <= n - 1 - P;
+            const double* pm = interior ? pint : xbt + (r < 2 * P ? r : 2 * P + (r - (n - P))) * (2 * V * S);
+            const double* pk = pm + V * S;
             double ym = 0.0, yk = 0.0;
-            if (j < d.tr) {
-                const int r = d.t0 + j, br = max(0, r - P);
-                const bool interior = r >= 2 * P && r <= n - 1 - P;
-                const double* pm = interior ? pint : xbt + (r < 2 * P ? r : 2 * P + (r - (n - P))) * (2 * V * S);
-                const double* pk = pm + V * S;
 #pragma unroll
-                for (int vv = 0; vv < 2; ++vv) {
-                    const int vx = vq + 4 * vv;
-                    if (vx >= V) break;
-                    const double* dmr = Dm + (br + vx - b0) * 16 - d.Xlo;
-                    const double* dkr = Dk + (br + vx - b0) * 16 - d.Xlo;
-#pragma unroll
-                    for (int o1 = 0; o1 < S; ++o1) {
-                        const int X = r - P + o1;
-                        if (X < 0 || X >= N) continue;
-                        const double dm = dmr[X], cm = pm[vx * S + o1];
-                        ym = fma(cm, dm, ym);
-                        yk = fma(pk[vx * S + o1], dm, yk);
-                        yk = fma(cm, dkr[X], yk);
-                    }
-                }
+            for (int pass = 0; pass < 2; ++pass) {
+                const int vx = pass ? 4 : lane / S, o1 = pass ? lane : lane % S;
+                if (vx >= V || o1 >= S || (!pass && lane >= 4 * S)) continue;
+                const int X = r - P + o1;
+                if (X < 0 || X >= N) continue;
+                const int di = (br + vx - b0) * 16 + X - d.Xlo;
+                const double dm = Dm[di], cm = pm[vx * S + o1];
+                ym = fma(cm, dm, ym);
+                yk = fma(pk[vx * S + o1], dm, yk);
+                yk = fma(cm, Dk[di], yk);
             }
-            ym += __shfl_xor_sync(0xffffffffu, ym, 1);
-            yk += __shfl_xor_sync(0xffffffffu, yk, 1);
-            ym += __shfl_xor_sync(0xffffffffu, ym, 2);
-            yk += __shfl_xor_sync(0xffffffffu, yk, 2);
-            if (vq == 0 && j < d.tr) {
-                if (MODE & 1) a.yM[d.orow0 + j] = ym;
-                if (MODE & 2) a.yK[d.orow0 + j] = yk;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                ym += __shfl_xor_sync(0xffffffffu, ym, off);
+                yk += __shfl_xor_sync(0xffffffffu, yk, off);
+            }
+            if (lane == 0) {
+                if (MODE & 1) a.yM[d.orow0 + warp] = ym;
+                if (MODE & 2) a.yK[d.orow0 + warp] = yk;
             }
         }
         if (dA.line >= 0) phase_a<P, NT, HS>(a, dA, patches, qbufs, Hm, Hk, tid);
         issue(itP, prow);                                            // tile k+PFD
-        if (tid == 0) desc[(k + PFD) & 7] = make_desc<P>(a, itP, last_line, false);
-        if (itP.line <= last_line) it_next<P>(a, itP);
+        if (tid == 0) desc[(k + PFD) & 7] = make_desc<P, URING>(a, itP, last_line, false);
+        if (itP.line <= last_line) it_next<P, PFD, URING>(a, itP);
         cp_async_wait<PFD - 2>();                                    // tile k+2 landed
         __syncthreads();
     }
@@ -845,8 +850,8 @@ template <int P, int MODE>
 int launch_apply_p(const LineArgs& a, cudaStream_t st) {
     using C = Cfg<P>;
     constexpr int HS = (C::S2 + 3) / 4 * 4 + ((C::S2 + 3) / 4 % 2 == 0 ? 4 : 0);
-    const size_t smem = (size_t)(2 * C::RING * HS + C::PFD * 4 * C::V * C::S + C::PFD * C::PATCH + C::XB +
-                                 C::URING * HS + 512 + 2 * C::V * C::S + HS) * sizeof(double);
+    const size_t smem = (size_t)(2 * C::RING * HS + ApplyCfg::PFD * 4 * C::V * C::S + ApplyCfg::PFD * C::PATCH +
+                                 C::XB + ApplyCfg::URING * HS + 512 + 2 * C::V * C::S + HS) * sizeof(double);
     auto kern = k_line_apply<P, MODE>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return WGQ_ECUDA;
