@@ -694,7 +694,7 @@ template <int P, int MODE>
 __global__ void __launch_bounds__(256, 3) k_line_apply(const __grid_constant__ LineArgs a) {
     using C = Cfg<P>;
     constexpr int S = C::S, S2 = C::S2, V = C::V, RING = C::RING, URING = ApplyCfg::URING, PFD = ApplyCfg::PFD;
-    // 8 warps: one D item, one phase-A plane and one output row each per tile
+    // 8 warps: one D item and one phase-A plane each per tile; warp 0 finishes the tile's rows
     constexpr int NT = 256;
     constexpr int HS = (S2 + 3) / 4 * 4 + ((S2 + 3) / 4 % 2 == 0 ? 4 : 0);   // row stride = 4 (mod 8): conflict-free fragments
     extern __shared__ __align__(128) double sm[];
@@ -749,14 +749,14 @@ __global__ void __launch_bounds__(256, 3) k_line_apply(const __grid_constant__ L
                 }
             }
             const int nx = (a.dbg & 16) ? 0 : t.uhi - t.ulo + 1;
-            const int rpos = t.lpos - t.X0;
+            const int p0 = (t.lpos + t.ulo - t.X0) % URING;            // ring position of column ulo
 #pragma unroll
             for (int m = 0; m < MU; ++m) {
                 if (uxo[m] >= nx || uxo[m] >= 16) continue;
                 const int X = t.ulo + uxo[m];
                 const bool ok = ubase[m] >= 0;
-                int pos = rpos + X;
-                pos = pos >= URING ? pos % URING : pos;
+                int pos = p0 + uxo[m];
+                pos = pos >= URING ? pos - URING : pos;
                 cp_async8(U + pos * HS + uo23[m], a.u + (ok ? ubase[m] + X : 0), ok);
             }
         }
@@ -793,7 +793,9 @@ __global__ void __launch_bounds__(256, 3) k_line_apply(const __grid_constant__ L
             const int c = b0 + 8 * mt + g, X = d.Xlo + 8 * nt + g;
             const bool cv = c <= hi_plane, xv = X <= d.Xhi;
             const double* hrow = (cv ? H + (c & (RING - 1)) * HS : zrow) + t4;
-            const double* urow = (xv ? U + ((d.upos + 8 * nt + g) % URING) * HS : zrow) + t4;
+            int upos = d.upos + 8 * nt + g;
+            upos = upos >= URING ? upos - URING : upos;
+            const double* urow = (xv ? U + upos * HS : zrow) + t4;
             double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;     // two chains: even / odd k-steps
 #pragma unroll
             for (int s = 0; s < ((a.dbg & 8) ? 0 : (S2 + 3) / 4); ++s) {      // padding columns are zero: no masks
@@ -806,34 +808,40 @@ __global__ void __launch_bounds__(256, 3) k_line_apply(const __grid_constant__ L
         }
         __syncthreads();
         // ---- S1b: rows of tile k (one per warp), phase A of tile k+1, prefetch tile k+PFD ----
-        if (warp < d.tr && !(a.dbg & 32)) {
-            // warp j finishes row t0 + j: lane = (vx, o1) pair (vx < 4; lanes < S also take vx = 4),
-            // y = sum_{vx,o1} P[vx][o1] D(b_r + vx, r - p + o1), reduced over the warp
-            const int r = d.t0 + warp, br = max(0, r - P);
-            const bool interior = r >= 2 * P && r <= n - 1 - P;
-            const double* pm = interior ? pint : xbt + (r < 2 * P ? r : 2 * P + (r - (n - P))) * (2 * V * S);
-            const double* pk = pm + V * S;
+        if (warp == 0 && !(a.dbg & 32)) {
+            // warp 0 finishes all rows of the tile: lane (j, vq) = row t0 + j, vertex planes
+            // vx = vq (+4); y = sum_{vx,o1} P[vx][o1] D(b_r + vx, r - p + o1), reduced over 4 lanes
+            const int j = lane >> 2, vq = lane & 3;
             double ym = 0.0, yk = 0.0;
+            if (j < d.tr) {
+                const int r = d.t0 + j, br = max(0, r - P);
+                const bool interior = r >= 2 * P && r <= n - 1 - P;
+                const double* pm = interior ? pint : xbt + (r < 2 * P ? r : 2 * P + (r - (n - P))) * (2 * V * S);
+                const double* pk = pm + V * S;
 #pragma unroll
-            for (int pass = 0; pass < 2; ++pass) {
-                const int vx = pass ? 4 : lane / S, o1 = pass ? lane : lane % S;
-                if (vx >= V || o1 >= S || (!pass && lane >= 4 * S)) continue;
-                const int X = r - P + o1;
-                if (X < 0 || X >= N) continue;
-                const int di = (br + vx - b0) * 16 + X - d.Xlo;
-                const double dm = Dm[di], cm = pm[vx * S + o1];
-                ym = fma(cm, dm, ym);
-                yk = fma(pk[vx * S + o1], dm, yk);
-                yk = fma(cm, Dk[di], yk);
-            }
+                for (int vv = 0; vv < 2; ++vv) {
+                    const int vx = vq + 4 * vv;
+                    if (vx >= V) break;
+                    const double* dmr = Dm + (br + vx - b0) * 16 - d.Xlo;
+                    const double* dkr = Dk + (br + vx - b0) * 16 - d.Xlo;
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                ym += __shfl_xor_sync(0xffffffffu, ym, off);
-                yk += __shfl_xor_sync(0xffffffffu, yk, off);
+                    for (int o1 = 0; o1 < S; ++o1) {
+                        const int X = r - P + o1;
+                        if (X < 0 || X >= N) continue;
+                        const double dm = dmr[X], cm = pm[vx * S + o1];
+                        ym = fma(cm, dm, ym);
+                        yk = fma(pk[vx * S + o1], dm, yk);
+                        yk = fma(cm, dkr[X], yk);
+                    }
+                }
             }
-            if (lane == 0) {
-                if (MODE & 1) a.yM[d.orow0 + warp] = ym;
-                if (MODE & 2) a.yK[d.orow0 + warp] = yk;
+            ym += __shfl_xor_sync(0xffffffffu, ym, 1);
+            yk += __shfl_xor_sync(0xffffffffu, yk, 1);
+            ym += __shfl_xor_sync(0xffffffffu, ym, 2);
+            yk += __shfl_xor_sync(0xffffffffu, yk, 2);
+            if (vq == 0 && j < d.tr) {
+                if (MODE & 1) a.yM[d.orow0 + j] = ym;
+                if (MODE & 2) a.yK[d.orow0 + j] = yk;
             }
         }
         if (dA.line >= 0) phase_a<P, NT, HS>(a, dA, patches, qbufs, Hm, Hk, tid);
