@@ -199,6 +199,16 @@ def traffic_from_profiles(cfg_name):
 
 
 # ------------------------------------------------------------------------------------------
+def arm_config(cfg, world, ld=None):
+    """The workload description, identical for this arm and the reference (oracle) arm."""
+    p, n, d = cfg["p"], cfg["n"], cfg["dim"]
+    s = 2 * p + 1
+    return {"workload": cfg["name"], "p": p, "n_elems": n, "dim": d, "kinds": list(cfg["kinds"]),
+            "coefficient": cfg["coeff"]["kind"], "rows": (n + p) ** d, "ld": ld or s ** d,
+            "layout": "ELL", "parallelism": f"line-granular z-slabs x{world}",
+            "l2": "flushed (512 MB write) between timed steps; outputs >> L2"}
+
+
 def main():
     args = parse()
     cfg = inputs.config(args.config, args.n)
@@ -222,7 +232,7 @@ def main():
         line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
                 "dtype": "f64", "data": "synthetic",
-                "config": {"workload": cfg["name"], "p": p, "n_elems": n, "dim": d, "kinds": list(kinds)},
+                "config": arm_config(cfg, world),
                 "cpu_baseline": {"value": value, "unit": UNIT, "cores": info[1], "kind": "oracle", "sample": info[0]},
                 "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
                 "vs_baseline": None}
@@ -329,10 +339,7 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": total_ms_max / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": cfg["name"], "p": p, "n_elems": n, "dim": d, "kinds": list(kinds),
-                           "coefficient": cfg["coeff"]["kind"], "rows": rules.n_rows, "ld": ld,
-                           "layout": "ELL", "parallelism": f"line-granular z-slabs x{world}",
-                           "l2": "flushed (512 MB write) between timed steps; outputs >> L2"},
+                "config": arm_config(cfg, world, ld),
                 "gpu_launches": args.steps * 1,
                 "roofline": roof, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu, "extras": extras,
                 "setup": setup}
