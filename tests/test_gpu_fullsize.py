@@ -118,3 +118,44 @@ def test_c5_slabs_reproduce_one_gpu_checksum():
             acc[k] = (acc[k] + int(h[0].item())) % 2 ** 64
     for k in cfg["kinds"]:
         assert acc[k] == full[k], k
+
+
+def test_c5_csr_full_size_sampled_rows():
+    """C5 in CSR layout at full size (117 GB: values of both matrices, int32 columns, int64
+    row pointers): sampled rows' pointers, columns and values against the oracle."""
+    from paper_1710_01048_b200 import api, wgq
+    cfg = inputs.config("C5")
+    p, n, d = cfg["p"], cfg["n"], cfg["dim"]
+    rules = wgq.Rules(p, n, d)
+    desc = inputs.coefficient(cfg["coeff"], d)
+    grid, plane0 = api.make_grid(rules, desc["seed"], desc["sigma"], 0, rules.n_rows)
+    row_ptr, col_idx, vals = api.assemble_csr(rules, api.coefficient(desc, grid, plane0), cfg["kinds"])
+    torch.cuda.synchronize()
+    try:
+        N = n + p
+        a1 = np.array([min(i + p, N - 1) - max(i - p, 0) + 1 for i in range(N)], dtype=np.int64)
+        total = int(a1.sum()) ** 3
+        assert int(row_ptr[-1].item()) == total == wgq.wgq_nnz(rules, 0, rules.n_rows)
+        rows = sample_rows(p, n, d, 300, seed=5)
+        host_grid = inputs.lognormal_grid(n, seed=desc["seed"], sigma=desc["sigma"])
+        ref = oasm.assemble_rows(p, n, d, rows, desc, cfg["kinds"], grid=host_grid)
+        sc = oasm.assemble_rows(p, n, d, rows, desc, cfg["kinds"], grid=host_grid, absolute=True)
+        # row pointers by brute force over the lexicographic rows before r: planes, lines, rows
+        A1 = np.concatenate([[0], np.cumsum(a1)])
+        S = int(A1[-1])
+        rp = row_ptr.index_select(0, torch.from_numpy(np.concatenate([rows, rows + 1])).cuda()).cpu().numpy()
+        got = {k: np.zeros((len(rows), rules.stencil)) for k in cfg["kinds"]}
+        for t, r in enumerate(rows):
+            i1, i2, i3 = r % N, (r // N) % N, r // (N * N)
+            start = A1[i3] * S * S + a1[i3] * (A1[i2] * S + a1[i2] * A1[i1])
+            assert rp[t] == start and rp[len(rows) + t] - rp[t] == a1[i1] * a1[i2] * a1[i3]
+            cols = oasm.ell_columns(p, n, d, int(r))
+            ok = cols >= 0
+            assert np.array_equal(col_idx[rp[t]:rp[len(rows) + t]].cpu().numpy(), cols[ok])
+            for k in cfg["kinds"]:
+                got[k][t, ok] = vals[k][rp[t]:rp[len(rows) + t]].cpu().numpy()
+        for k in cfg["kinds"]:
+            check_rows(got[k], ref[k], sc[k], ("C5 csr", k))
+    finally:
+        del row_ptr, col_idx, vals
+        torch.cuda.empty_cache()
