@@ -337,9 +337,12 @@ __host__ __device__ __forceinline__ long long csr_A(long long r, int p, long lon
     const long long m = r < p ? r : p, q = r - (N - p) > 0 ? r - (N - p) : 0;
     return (2 * p + 1) * r - (m * p - m * (m - 1) / 2) - q * (q + 1) / 2;
 }
-__host__ __device__ __forceinline__ long long csr_start(long long row, int p, long long N) {
-    const long long i1 = row % N, i2 = (row / N) % N, i3 = row / (N * N), S = csr_A(N, p, N);
+__host__ __device__ __forceinline__ long long csr_start3(long long i1, long long i2, long long i3, int p, long long N) {
+    const long long S = csr_A(N, p, N);
     return csr_A(i3, p, N) * S * S + csr_a(i3, p, N) * (csr_A(i2, p, N) * S + csr_a(i2, p, N) * csr_A(i1, p, N));
+}
+__host__ __device__ __forceinline__ long long csr_start(long long row, int p, long long N) {
+    return csr_start3(row % N, (row / N) % N, row / (N * N), p, N);
 }
 
 // What every warp needs to know about a tile; written by thread 0 when the tile is prefetched.
@@ -366,7 +369,7 @@ __device__ __forceinline__ TileCsr make_csr(const LineArgs& a, const TileIt& t, 
     TileCsr d{};
     if (t.line <= last_line) {
         const long long N = a.N;
-        d.cs0 = csr_start((long long)t.line * N + t.t0, P, N) - a.csr_base;
+        d.cs0 = csr_start3(t.t0, t.i2, t.i3, P, N) - a.csr_base;     // no divisions on thread 0's path
         d.a2 = (int)csr_a(t.i2, P, N);
         d.w23 = d.a2 * (int)csr_a(t.i3, P, N);
         d.lo2 = max(0, P - t.i2);
@@ -846,7 +849,7 @@ __global__ void __launch_bounds__(256, 3) k_line_apply(const __grid_constant__ L
         }
         if (dA.line >= 0) phase_a<P, NT, HS>(a, dA, patches, qbufs, Hm, Hk, tid);
         issue(itP, prow);                                            // tile k+PFD
-        if (tid == 0) desc[(k + PFD) & 7] = make_desc<P, URING>(a, itP, last_line, false);
+        if (tid == NT - 1) desc[(k + PFD) & 7] = make_desc<P, URING>(a, itP, last_line, false);   // warp 0 finishes rows
         if (itP.line <= last_line) it_next<P, PFD, URING>(a, itP);
         cp_async_wait<PFD - 2>();                                    // tile k+2 landed
         __syncthreads();
