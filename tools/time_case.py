@@ -25,14 +25,19 @@ ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--dbg", default="0")
 ap.add_argument("--ld", type=int, default=None)
 ap.add_argument("--op", default="assemble", choices=["assemble", "load", "apply", "csr"])
+ap.add_argument("--slab", default=None, help="r/W: only rank r's rows of a W-way line-granular split (assemble)")
 a = ap.parse_args()
 cfg = inputs.config(a.config, a.n)
 rules = wgq.Rules(cfg["p"], cfg["n"], cfg["dim"])
+rb, re_ = 0, rules.n_rows
+if a.slab:
+    r_, w_ = map(int, a.slab.split("/"))
+    rb, re_ = api.slab_rows(rules.N, rules.dim, r_, w_)
 grid, plane0 = (None, 0)
 if cfg["coeff"]["kind"] == "grid":
-    grid, plane0 = api.make_grid(rules, cfg["coeff"]["seed"], cfg["coeff"]["sigma"], 0, rules.n_rows)
+    grid, plane0 = api.make_grid(rules, cfg["coeff"]["seed"], cfg["coeff"]["sigma"], rb, re_)
 coef = api.coefficient(inputs.coefficient(cfg["coeff"], cfg["dim"]), grid, plane0)
-out = {k: api.alloc_ell(rules, 0, rules.n_rows, a.ld) for k in cfg["kinds"]} if a.op == "assemble" else None
+out = {k: api.alloc_ell(rules, rb, re_, a.ld) for k in cfg["kinds"]} if a.op == "assemble" else None
 u = torch.randn(rules.n_rows, dtype=torch.float64, device="cuda") if a.op == "apply" else None
 if a.op == "csr":
     nnz = wgq.wgq_nnz(rules, 0, rules.n_rows)
@@ -46,7 +51,7 @@ bvec = torch.empty(rules.n_rows, dtype=torch.float64, device="cuda") if a.op == 
 
 def run():
     if a.op == "assemble":
-        api.assemble(rules, coef, cfg["kinds"], out=out)
+        api.assemble(rules, coef, cfg["kinds"], rb, re_, out=out)
     elif a.op == "load":
         api.assemble_load(rules, coef, out=bvec)
     elif a.op == "csr":
@@ -57,7 +62,7 @@ def run():
     else:
         api.apply(rules, coef, u, cfg["kinds"])
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
-alg = (rules.n_rows * rules.stencil * 8 * len(cfg["kinds"]) if a.op == "assemble" else
+alg = ((re_ - rb) * rules.stencil * 8 * len(cfg["kinds"]) if a.op == "assemble" else
        wgq.wgq_nnz(rules, 0, rules.n_rows) * 8 * len(cfg["kinds"]) if a.op == "csr" else rules.n_rows * 8)
 res = {}
 for mode in a.dbg.split(","):
@@ -75,4 +80,4 @@ for mode in a.dbg.split(","):
     ts.sort()
     res[mode] = {"best_ms": round(ts[0], 4), "median_ms": round(ts[len(ts) // 2], 4),
                  "GBs": round(alg / ts[0] / 1e6, 1), "all": [round(x, 3) for x in ts]}
-print(json.dumps({"config": cfg["name"], "op": a.op, "n": cfg["n"], "rows": rules.n_rows, "modes": res}))
+print(json.dumps({"config": cfg["name"], "op": a.op, "n": cfg["n"], "rows": re_ - rb, "slab": a.slab, "modes": res}))
