@@ -14,10 +14,10 @@
 //   HK[v][o2,o3]  = sum_{vy,vz} g[..][..][v] (PKy PMz + PMy PKz)
 // are computed once per line (phase A, ~1 plane per row) and each row finishes with
 //   M[o1,o23] = sum_vx PMx[vx][o1] HM[bx+vx][o23],  K = sum_vx PKx HM + PMx HK     (phase B)
-// Interior x-rows (class I) share one table P^ (times h resp. 1/h) that lives in __constant__
-// memory; its zero pattern is structural (a node in element k touches planes k, k+1 and
-// columns k..k+p), so phase B issues only the structurally nonzero FP64 FMAs, with constant
-// operands.  A CTA (3 per SM) owns a line, walks it in tiles of TR = 8 rows (each thread
+// Interior x-rows (class I) share one table P^ (times h resp. 1/h), passed as kernel
+// parameters (constant bank, read through uniform registers); its zero pattern is structural
+// (a node in element k touches planes k, k+1 and columns k..k+p), so phase B issues only the
+// structurally nonzero FP64 FMAs.  A CTA (3 per SM) owns a line, walks it in tiles of TR = 8 rows (each thread
 // finishes two consecutive rows of one (o2,o3) group from a 6-plane window, so the constant
 // tables and index arithmetic are shared by both rows), prefetches the next tile's vertex
 // patch with cp.async, stages the tile's M and K rows in shared memory and writes each tile
