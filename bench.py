@@ -140,7 +140,8 @@ class ClockSampler:
                0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting"}
 
     def __init__(self, device):
-        self.samples, self.reasons, self.ok = [], 0, False
+        self.samples, self.power, self.reasons, self.ok = [], [], 0, False
+        self.limit_w = None
         try:
             import pynvml
             pynvml.nvmlInit()
@@ -148,6 +149,10 @@ class ClockSampler:
             self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
             self.ok = True
+            try:
+                self.limit_w = pynvml.nvmlDeviceGetEnforcedPowerLimit(self.h) / 1e3
+            except Exception:
+                pass
         except Exception:
             self.max_mhz = None
         self._stop = threading.Event()
@@ -157,6 +162,7 @@ class ClockSampler:
             try:
                 self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
                 self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.power.append(self.nv.nvmlDeviceGetPowerUsage(self.h) / 1e3)
             except Exception:
                 pass
             time.sleep(0.005)
@@ -176,7 +182,9 @@ class ClockSampler:
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
         return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
-                "reasons": [v for k, v in self.REASONS.items() if self.reasons & k], "samples": len(self.samples)}
+                "reasons": [v for k, v in self.REASONS.items() if self.reasons & k], "samples": len(self.samples),
+                "power_w": round(float(np.median(self.power)), 1) if self.power else None,
+                "power_limit_w": self.limit_w}
 
 
 def peaks():
@@ -316,7 +324,9 @@ def main():
             "frac": round(achieved / peak, 4), "peak_source": peak_src,
             "traffic": traffic_from_profiles(cfg["name"]),
             "kernel": "wgq assembly (M+K fused)", "algorithmic_bytes_per_launch": int(alg_bytes),
-            "kernel_ms": round(kernel_s * 1e3, 4)}
+            "kernel_ms": round(kernel_s * 1e3, 4),
+            "step_ms": {"min": round(float(np.min(step_ms)), 4), "median": round(float(np.median(step_ms)), 4),
+                        "max": round(float(np.max(step_ms)), 4)}}
 
     # end to end through the public API with HOST buffers (H2D of the coefficient slab, D2H of M, K)
     e2e = None
