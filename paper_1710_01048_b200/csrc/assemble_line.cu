@@ -71,7 +71,8 @@ struct LineArgs {
     // interior (class I) x-row vertex tables P^ in physical units: PMh = h * PM, PKi = PK / h
     // (kernel parameters: constant-bank operands, no global state shared between handles)
     double PMh[kMaxV][kMaxS], PKi[kMaxV][kMaxS];
-    int dbg;   // profiling only (WGQ_LINE_DBG bits): 1 = skip compute, 2 = skip stores, 4 = skip loads
+    int dbg;   // profiling only (WGQ_LINE_DBG bits): 1 = skip compute, 2 = skip stores, 4 = skip loads,
+               // 64 = skip phase A, 128 = skip phase B, 256 = random staging values (assembly)
     long long csr_base;   // CSR: global position of row_begin's first entry (closed form)
     // matrix-free application (k_line_apply): y = A u over the rows, u from global row u_row0
     const double* u;
@@ -435,7 +436,7 @@ __device__ __forceinline__ void phase_a(const LineArgs& a, const TileDesc& t, co
     const double* patch = patches + t.ps * C::PATCH;
     const int nnew = t.nnew;
     const int vzp = (g >> 1) + 4 * (g & 1);            // B column g of A1 <-> vz = pi(g)
-    for (int j = NW - 1 - warp; j < ((a.dbg & 1) ? 0 : nnew); j += NW) {
+    for (int j = NW - 1 - warp; j < ((a.dbg & 65) ? 0 : nnew); j += NW) {
         double tM0 = 0.0, tM1 = 0.0, tK0 = 0.0, tK1 = 0.0;
 #pragma unroll
         for (int s = 0; s < KS; ++s) {
@@ -555,6 +556,14 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const __grid_const
         const int r = i < 2 * P ? i : n - P + (i - 2 * P);
         xbt[e] = (kind ? a.T.PK : a.T.PM)[((size_t)r * kMaxV + v) * kMaxS + o];
     }
+    if (a.dbg & 256) {      // profiling: staging holds fixed high-entropy values (with bit 1: stores only)
+        for (int e = tid; e < 2 * C::STAGE; e += C::NT) {
+            unsigned long long z = (unsigned long long)(e + 1) * 0x9E3779B97F4A7C15ull;
+            z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+            z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+            stage[e] = 1.0 + (double)(z >> 11) * 0x1.0p-53;
+        }
+    }
     auto xb_row = [&](int r) -> const double* {
         return xbt + (r < 2 * P ? r : 2 * P + (r - (n - P))) * (2 * V * S);
     };
@@ -587,7 +596,7 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const __grid_const
         double* stM = stage + pad;
         double* stK = stage + C::STAGE + pad;
         // ---- S1: phase B of tile k ---------------------------------------------------------
-        if (tid < C::ITEMS && 2 * q < d.tr && !(a.dbg & 1)) {
+        if (tid < C::ITEMS && 2 * q < d.tr && !(a.dbg & 129)) {
             const int j = 2 * q, r = d.t0 + j;
             const int b0 = max(0, r - P);
             double hm[V + 1], hk[V + 1];
