@@ -38,7 +38,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C5")
-    ap.add_argument("--n", type=int, default=None, help="override elements per direction")
+    ap.add_argument("--n", "--elems", dest="n", type=int, default=None,
+                    help="override elements per direction (--elems under torchrun: its parser claims --n)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
@@ -252,9 +253,17 @@ def main():
 
     from paper_1710_01048_b200 import api, wgq
 
-    torch.cuda.set_device(local)
+    # WGQ_BENCH_FUNCTIONAL=1: functional check of the N>1 code path on ONE GPU (every rank on
+    # cuda:0, gloo on CPU tensors); its timings are not measurements (the ranks share a GPU)
+    functional = os.environ.get("WGQ_BENCH_FUNCTIONAL") == "1"
+    dev = 0 if functional else local
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if functional:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    red_dev = "cpu" if functional else "cuda"
     stream = torch.cuda.current_stream()
 
     # setup, reported separately: host rule build, device tables, grid generation
@@ -294,7 +303,7 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev) as clk:
         for i in range(args.steps):
             flush.zero_()
             ev[i][0].record(stream)
@@ -306,8 +315,8 @@ def main():
     torch.cuda.synchronize()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = float(np.sum(step_ms))
-    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-    nz = torch.tensor([float(nnz_rank)], dtype=torch.float64, device="cuda")
+    t = torch.tensor([total_ms], dtype=torch.float64, device=red_dev)
+    nz = torch.tensor([float(nnz_rank)], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(nz, op=dist.ReduceOp.SUM)
@@ -331,7 +340,7 @@ def main():
     # end to end through the public API with HOST buffers (H2D of the coefficient slab, D2H of M, K)
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, cfg, rules, row_begin, row_end, ld, world, rank, local, nnz_all)
+        e2e = run_e2e(args, cfg, rules, row_begin, row_end, ld, world, rank, local, nnz_all, red_dev)
 
     extras = None
     if rank == 0 and world == 1 and not args.no_extras:
@@ -353,6 +362,8 @@ def main():
                 "gpu_launches": args.steps * 1,
                 "roofline": roof, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu, "extras": extras,
                 "setup": setup}
+        if functional:
+            line["functional_check"] = "WGQ_BENCH_FUNCTIONAL=1: all ranks on one GPU over gloo; not a measurement"
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -422,7 +433,7 @@ def run_extras(rules5, coef5, peak):
     return out
 
 
-def run_e2e(args, cfg, rules, row_begin, row_end, ld, world, rank, local, nnz_all):
+def run_e2e(args, cfg, rules, row_begin, row_end, ld, world, rank, local, nnz_all, red_dev="cuda"):
     import torch
     import torch.distributed as dist
 
@@ -453,7 +464,7 @@ def run_e2e(args, cfg, rules, row_begin, row_end, ld, world, rank, local, nnz_al
         t0 = time.perf_counter()
         wgq.wgq_assemble_host(rules, coef, row_begin, row_end, M, K, ld)
         times.append(time.perf_counter() - t0)
-    t = torch.tensor([float(np.sum(times))], dtype=torch.float64, device="cuda")
+    t = torch.tensor([float(np.sum(times))], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     value = nnz_all * args.e2e_steps / float(t.item())
