@@ -720,92 +720,124 @@ __global__ void __launch_bounds__(256) k_load_grid_line(const GenericArgs a, con
     }
 }
 
-// 3D GRID load vector, y-sliding variant: a warp owns (i3, a 32-row x segment, a chunk of
-// consecutive y-lines).  Lane l first reduces over z for its vertex plane c = c0 + l:
-// Hz[y] = sum_vz PWz[vz] g[bz+vz][y][c] (5 loads, reused by the 5 lines whose window holds y),
-// slides a 5-deep window of Hz over y, forms G = sum_vy PWy[vy] Hz[by+vy] per line and finishes
-// the row i1 = x0 + l with warp shuffles as in k_load_grid_line.
-constexpr int kLoadYChunk = 32;
+// 3D GRID load vector, z-sliding: a block owns a T x T tile of (i1, i2) and a
+// run of kLZC planes i3; b = sum_{vz,vy,vx} PW_z PW_y PW_x g is contracted z -> y -> x in
+// shared memory from a ring of the tile's vertex planes (T + p + 1 square, loaded once per
+// plane with cp.async one step ahead), so every vertex value is read from global memory about
+// once per tile instead of once per (row, vz) — the same sum as k_load, reordered.
+#ifndef WGQ_LZT
+#define WGQ_LZT 16
+#endif
+#ifndef WGQ_LZA
+#define WGQ_LZA 3
+#endif
+constexpr int kLZT = WGQ_LZT;   // output tile edge (rows i1, i2)
+constexpr int kLZA = WGQ_LZA;   // vertex planes loaded ahead of the window
+static_assert(kLZA >= 1 && kLZA <= 7, "cp.async groups ahead of the window");
+constexpr int kLZC = 32;        // planes i3 per block
+constexpr int kLZThreads = kLZT >= 32 ? 256 : 128;
 
 template <int P>
-__global__ void __launch_bounds__(256) k_load_grid_yslide(const GenericArgs a, const double* PW, double* b) {
-    constexpr int V = P + 2;
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const int64_t N = a.N, nv = a.n + 1, n = a.n;
-    const int64_t xsegs = (N + 31) / 32, ychunks = (N + kLoadYChunk - 1) / kLoadYChunk;
-    const int64_t plane_rows = N * N;
-    const int64_t z0 = a.row_begin / plane_rows, z1 = (a.row_end - 1) / plane_rows;
-    const int64_t items = (z1 - z0 + 1) * xsegs * ychunks;
-    for (int64_t it = warp; it < items; it += nwarps) {
-        const int64_t i3 = z0 + it / (xsegs * ychunks);
-        const int64_t rem = it % (xsegs * ychunks);
-        const int64_t x0 = (rem / ychunks) * 32, ya = (rem % ychunks) * kLoadYChunk;
-        const int64_t yb = min(N, ya + kLoadYChunk);
+__global__ void __launch_bounds__(kLZThreads) k_load_grid_zslide(const GenericArgs a, const double* PW, double* b) {
+    constexpr int V = P + 2, T = kLZT, E = T + V - 1, RZ = V + kLZA;   // ring: window + kLZA ahead
+    extern __shared__ __align__(16) double zs[];
+    double* ring = zs;                      // [RZ][E][E] vertex planes (slot = plane % RZ)
+    double* hz = ring + RZ * E * E;         // [E][E]  z-contracted
+    double* gy = hz + E * E;                // [T][E]  y-contracted
+    double* pwx = gy + T * E;               // [T][V]  the tile's x rows' vertex weights
+    double* pwy = pwx + T * V;              // [T][V]
+    const int tid = threadIdx.x;
+    const int64_t N = a.N, n = a.n, nv = n + 1;
+    const int64_t x0 = (int64_t)blockIdx.x * T, y0 = (int64_t)blockIdx.y * T;
+    const int64_t c0 = max((int64_t)0, x0 - P), r0 = max((int64_t)0, y0 - P);
+    const int64_t pr = N * N;
+    const int64_t zlo_all = a.row_begin / pr, zhi_all = (a.row_end - 1) / pr;
+    const int64_t z_lo = zlo_all + (int64_t)blockIdx.z * kLZC;
+    const int64_t z_hi = min(zhi_all + 1, z_lo + kLZC);
+    if (z_lo >= z_hi) return;
+    for (int e = tid; e < T * V; e += blockDim.x) {
+        const int j = e / V, v = e % V;
+        pwx[e] = x0 + j < N ? PW[(x0 + j) * kMaxV + v] : 0.0;
+        pwy[e] = y0 + j < N ? PW[(y0 + j) * kMaxV + v] : 0.0;
+    }
+    const int64_t zg0 = a.coef.plane0, zg1 = a.coef.plane0 + a.coef.planes;
+    auto issue_plane = [&](int64_t z) {      // one commit group per plane (empty past the mesh)
+        double* dst = ring + (int)(z % RZ) * (E * E);
+        if (z <= n) {
+            for (int e = tid; e < E * E; e += blockDim.x) {
+                const int64_t y = r0 + e / E, x = c0 + e % E;
+                const bool ok = y <= n && x <= n && z >= zg0 && z < zg1;
+                const double* src = ok ? a.coef.grid + ((z - zg0) * nv + y) * nv + x : a.coef.grid;
+                const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + e);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(src), "r"(ok ? 8 : 0)
+                             : "memory");
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    // planes needed by i3: [bz, bz + V - 1], bz = max(0, i3 - P); loaded in order, AHEAD planes early
+    int64_t next = max((int64_t)0, z_lo - P);
+    const int64_t first = next;
+    while (next < first + RZ) issue_plane(next++);            // the window plus AHEAD planes
+    for (int64_t i3 = z_lo; i3 < z_hi; ++i3) {
         const int64_t bz = max((int64_t)0, i3 - P);
-        const int64_t c0 = max((int64_t)0, x0 - P);
+        // groups still allowed in flight: the planes beyond this i3's window
+        switch ((int)min((int64_t)kLZA, next - 1 - (bz + V - 1))) {   // groups beyond the window may fly
+            case 7: asm volatile("cp.async.wait_group 7;" ::: "memory"); break;
+            case 6: asm volatile("cp.async.wait_group 6;" ::: "memory"); break;
+            case 5: asm volatile("cp.async.wait_group 5;" ::: "memory"); break;
+            case 4: asm volatile("cp.async.wait_group 4;" ::: "memory"); break;
+            case 3: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
+            case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
+            case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
+            default: asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();
+        int slot[V];
         double pwz[V];
 #pragma unroll
-        for (int v = 0; v < V; ++v) pwz[v] = PW[i3 * kMaxV + v];
-        // Hz for the lane's planes c0 + lane (h = 0) and c0 + 32 + lane (h = 1, lanes < V-1)
-        auto hz = [&](int64_t y, int h) -> double {
-            const int64_t c = c0 + lane + 32 * h;
-            if (y > n || c > n || (h == 1 && lane >= V - 1)) return 0.0;
-            double gv[V];
-#pragma unroll
-            for (int vz = 0; vz < V; ++vz) {
-                const int64_t z = bz + vz;
-                gv[vz] = z <= n ? __ldg(a.coef.grid + ((z - a.coef.plane0) * nv + y) * nv + c) : 0.0;
-            }
+        for (int v = 0; v < V; ++v) {
+            slot[v] = (int)((bz + v) % RZ);
+            pwz[v] = bz + v <= n ? PW[i3 * kMaxV + v] : 0.0;
+        }
+        for (int e = tid; e < E * E; e += blockDim.x) {
             double s = 0.0;
 #pragma unroll
-            for (int vz = 0; vz < V; ++vz) s = fma(pwz[vz], gv[vz], s);
-            return s;
-        };
-        // window W[v] = Hz[by + v] for the current line (by = max(0, i2 - P))
-        double W0[V], W1[V];
-        int64_t wby = max((int64_t)0, ya - P);
-#pragma unroll
-        for (int v = 0; v < V; ++v) {
-            W0[v] = hz(wby + v, 0);
-            W1[v] = hz(wby + v, 1);
+            for (int vz = 0; vz < V; ++vz) s = fma(pwz[vz], ring[slot[vz] * (E * E) + e], s);
+            hz[e] = s;
         }
-        for (int64_t i2 = ya; i2 < yb; ++i2) {
-            const int64_t by = max((int64_t)0, i2 - P);
-            if (by != wby) {                                   // slide by one vertex row
+        __syncthreads();
+        // once hz is formed, slots of planes below the next window are free: refill them
+        if (i3 + 1 < z_hi) {
+            const int64_t bz1 = max((int64_t)0, i3 + 1 - P);
+            while (next - RZ < bz1) issue_plane(next++);
+        }
+        for (int e = tid; e < T * E; e += blockDim.x) {
+            const int j = e / E, c = e % E;
+            const int64_t i2 = y0 + j;
+            const int yy0 = (int)(max((int64_t)0, i2 - P) - r0);
+            double s = 0.0;
 #pragma unroll
-                for (int v = 0; v + 1 < V; ++v) {
-                    W0[v] = W0[v + 1];
-                    W1[v] = W1[v + 1];
-                }
-                W0[V - 1] = hz(by + V - 1, 0);
-                W1[V - 1] = hz(by + V - 1, 1);
-                wby = by;
-            }
-            double G0 = 0.0, G1 = 0.0;
-#pragma unroll
-            for (int v = 0; v < V; ++v) {
-                const double w = PW[i2 * kMaxV + v];
-                G0 = fma(w, W0[v], G0);
-                G1 = fma(w, W1[v], G1);
-            }
-            const int64_t i1 = x0 + lane;
+            for (int vy = 0; vy < V; ++vy)
+                if (yy0 + vy < E) s = fma(pwy[j * V + vy], hz[(yy0 + vy) * E + c], s);
+            gy[e] = s;
+        }
+        __syncthreads();
+        for (int e = tid; e < T * T; e += blockDim.x) {
+            const int j = e / T, i = e % T;
+            const int64_t i1 = x0 + i, i2 = y0 + j;
+            if (i1 >= N || i2 >= N) continue;
             const int64_t row = (i3 * N + i2) * N + i1;
-            const bool mine = i1 < N && row >= a.row_begin && row < a.row_end;
-            const int64_t bx = max((int64_t)0, i1 - P);
-            double acc = 0.0;
+            if (row < a.row_begin || row >= a.row_end) continue;
+            const int cc0 = (int)(max((int64_t)0, i1 - P) - c0);
+            double s = 0.0;
 #pragma unroll
-            for (int vx = 0; vx < V; ++vx) {
-                const int src = (int)(bx + vx - c0);
-                const double g0 = __shfl_sync(0xffffffffu, G0, src & 31);
-                const double g1 = __shfl_sync(0xffffffffu, G1, src & 31);
-                const double wx = mine ? PW[i1 * kMaxV + vx] : 0.0;
-                acc = fma(wx, src < 32 ? g0 : g1, acc);
-            }
-            if (mine) b[row - a.row_begin] = acc;
+            for (int vx = 0; vx < V; ++vx)
+                if (cc0 + vx < E) s = fma(pwx[i * V + vx], gy[j * E + cc0 + vx], s);
+            b[row - a.row_begin] = s;
         }
     }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 template <int P, int D>
@@ -816,10 +848,15 @@ int launch_load_pd(const GenericArgs& a, const double* PW, double* b, cudaStream
     const int64_t rows = a.row_end - a.row_begin;
     if (D == 3 && a.coef.kind == WGQ_COEF_GRID) {
         const int64_t pr = a.N * a.N;
-        const int64_t items = ((a.row_end - 1) / pr - a.row_begin / pr + 1) * ((a.N + 31) / 32) *
-                              ((a.N + kLoadYChunk - 1) / kLoadYChunk);
-        const int64_t b3 = std::max<int64_t>(1, std::min<int64_t>((items + 7) / 8, (int64_t)sms * 16));
-        k_load_grid_yslide<P><<<(unsigned)b3, 256, 0, st>>>(a, PW, b);
+        const int64_t planes = (a.row_end - 1) / pr - a.row_begin / pr + 1;
+        constexpr int V = P + 2, E = kLZT + V - 1;
+        const size_t smem = (size_t)((V + kLZA) * E * E + E * E + kLZT * E + 2 * kLZT * V) * sizeof(double);
+        if (cudaFuncSetAttribute(k_load_grid_zslide<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess)
+            return WGQ_ECUDA;
+        const dim3 g((unsigned)((a.N + kLZT - 1) / kLZT), (unsigned)((a.N + kLZT - 1) / kLZT),
+                     (unsigned)((planes + kLZC - 1) / kLZC));
+        k_load_grid_zslide<P><<<g, kLZThreads, smem, st>>>(a, PW, b);
         return cudaGetLastError() == cudaSuccess ? WGQ_OK : WGQ_ECUDA;
     }
     if (D >= 2 && a.coef.kind == WGQ_COEF_GRID) {
