@@ -740,12 +740,12 @@ constexpr int kLZThreads = kLZT >= 32 ? 256 : 128;
 template <int P>
 __global__ void __launch_bounds__(kLZThreads) k_load_grid_zslide(const GenericArgs a, const double* PW, double* b) {
     constexpr int V = P + 2, T = kLZT, E = T + V - 1, RZ = V + kLZA;   // ring: window + kLZA ahead
+    constexpr int NT = kLZThreads;
+    constexpr int EL = (E * E + NT - 1) / NT, YL = (T * E + NT - 1) / NT, XL = (T * T + NT - 1) / NT;
     extern __shared__ __align__(16) double zs[];
     double* ring = zs;                      // [RZ][E][E] vertex planes (slot = plane % RZ)
     double* hz = ring + RZ * E * E;         // [E][E]  z-contracted
     double* gy = hz + E * E;                // [T][E]  y-contracted
-    double* pwx = gy + T * E;               // [T][V]  the tile's x rows' vertex weights
-    double* pwy = pwx + T * V;              // [T][V]
     const int tid = threadIdx.x;
     const int64_t N = a.N, n = a.n, nv = n + 1;
     const int64_t x0 = (int64_t)blockIdx.x * T, y0 = (int64_t)blockIdx.y * T;
@@ -755,33 +755,72 @@ __global__ void __launch_bounds__(kLZThreads) k_load_grid_zslide(const GenericAr
     const int64_t z_lo = zlo_all + (int64_t)blockIdx.z * kLZC;
     const int64_t z_hi = min(zhi_all + 1, z_lo + kLZC);
     if (z_lo >= z_hi) return;
-    for (int e = tid; e < T * V; e += blockDim.x) {
-        const int j = e / V, v = e % V;
-        pwx[e] = x0 + j < N ? PW[(x0 + j) * kMaxV + v] : 0.0;
-        pwy[e] = y0 + j < N ? PW[(y0 + j) * kMaxV + v] : 0.0;
+    // fixed per-thread roles (the same elements every plane step):
+    //   loads: patch elements e = tid + NT m -> in-plane offset (or -1 outside the mesh)
+    int64_t loff[EL];
+#pragma unroll
+    for (int m = 0; m < EL; ++m) {
+        const int e = tid + NT * m;
+        const int64_t y = r0 + e / E, x = c0 + e % E;
+        loff[m] = (e < E * E && y <= n && x <= n) ? y * nv + x : -1;
+    }
+    //   y pass: (j, c) -> window start row in hz and the row's vertex weights
+    int yj[YL], ystart[YL];
+    double wy[YL][V];
+#pragma unroll
+    for (int m = 0; m < YL; ++m) {
+        const int e = tid + NT * m;
+        const int j = e / E;
+        const int64_t i2 = y0 + j;
+        yj[m] = (e < T * E && i2 < N) ? 1 : 0;
+        ystart[m] = (int)(max((int64_t)0, i2 - P) - r0) * E + e % E;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            const int64_t yy = max((int64_t)0, i2 - P) - r0 + v;
+            wy[m][v] = (yj[m] && yy < E) ? PW[i2 * kMaxV + v] : 0.0;
+        }
+    }
+    //   x pass: (j, i) -> gy offset, row offset within a plane of rows, weights
+    int xg[XL];
+    int64_t xrow[XL];
+    double wx[XL][V];
+#pragma unroll
+    for (int m = 0; m < XL; ++m) {
+        const int e = tid + NT * m;
+        const int j = e / T, i = e % T;
+        const int64_t i1 = x0 + i, i2 = y0 + j;
+        const bool ok = e < T * T && i1 < N && i2 < N;
+        const int cc0 = (int)(max((int64_t)0, i1 - P) - c0);
+        xg[m] = j * E + cc0;
+        xrow[m] = ok ? i2 * N + i1 : -1;
+#pragma unroll
+        for (int v = 0; v < V; ++v) wx[m][v] = (ok && cc0 + v < E) ? PW[i1 * kMaxV + v] : 0.0;
     }
     const int64_t zg0 = a.coef.plane0, zg1 = a.coef.plane0 + a.coef.planes;
     auto issue_plane = [&](int64_t z) {      // one commit group per plane (empty past the mesh)
         double* dst = ring + (int)(z % RZ) * (E * E);
         if (z <= n) {
-            for (int e = tid; e < E * E; e += blockDim.x) {
-                const int64_t y = r0 + e / E, x = c0 + e % E;
-                const bool ok = y <= n && x <= n && z >= zg0 && z < zg1;
-                const double* src = ok ? a.coef.grid + ((z - zg0) * nv + y) * nv + x : a.coef.grid;
+            const bool zok = z >= zg0 && z < zg1;
+            const double* gz = a.coef.grid + (z - zg0) * nv * nv;
+#pragma unroll
+            for (int m = 0; m < EL; ++m) {
+                const int e = tid + NT * m;
+                if (e >= E * E) break;
+                const bool ok = zok && loff[m] >= 0;
                 const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + e);
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(src), "r"(ok ? 8 : 0)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(ok ? gz + loff[m] : a.coef.grid),
+                             "r"(ok ? 8 : 0)
                              : "memory");
             }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    // planes needed by i3: [bz, bz + V - 1], bz = max(0, i3 - P); loaded in order, AHEAD planes early
+    // planes needed by i3: [bz, bz + V - 1], bz = max(0, i3 - P); loaded in order, kLZA ahead
     int64_t next = max((int64_t)0, z_lo - P);
     const int64_t first = next;
-    while (next < first + RZ) issue_plane(next++);            // the window plus AHEAD planes
+    while (next < first + RZ) issue_plane(next++);
     for (int64_t i3 = z_lo; i3 < z_hi; ++i3) {
         const int64_t bz = max((int64_t)0, i3 - P);
-        // groups still allowed in flight: the planes beyond this i3's window
         switch ((int)min((int64_t)kLZA, next - 1 - (bz + V - 1))) {   // groups beyond the window may fly
             case 7: asm volatile("cp.async.wait_group 7;" ::: "memory"); break;
             case 6: asm volatile("cp.async.wait_group 6;" ::: "memory"); break;
@@ -793,17 +832,20 @@ __global__ void __launch_bounds__(kLZThreads) k_load_grid_zslide(const GenericAr
             default: asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
         __syncthreads();
-        int slot[V];
+        const double* rp[V];
         double pwz[V];
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-            slot[v] = (int)((bz + v) % RZ);
+            rp[v] = ring + (int)((bz + v) % RZ) * (E * E);
             pwz[v] = bz + v <= n ? PW[i3 * kMaxV + v] : 0.0;
         }
-        for (int e = tid; e < E * E; e += blockDim.x) {
+#pragma unroll
+        for (int m = 0; m < EL; ++m) {
+            const int e = tid + NT * m;
+            if (e >= E * E) break;
             double s = 0.0;
 #pragma unroll
-            for (int vz = 0; vz < V; ++vz) s = fma(pwz[vz], ring[slot[vz] * (E * E) + e], s);
+            for (int vz = 0; vz < V; ++vz) s = fma(pwz[vz], rp[vz][e], s);
             hz[e] = s;
         }
         __syncthreads();
@@ -812,29 +854,26 @@ __global__ void __launch_bounds__(kLZThreads) k_load_grid_zslide(const GenericAr
             const int64_t bz1 = max((int64_t)0, i3 + 1 - P);
             while (next - RZ < bz1) issue_plane(next++);
         }
-        for (int e = tid; e < T * E; e += blockDim.x) {
-            const int j = e / E, c = e % E;
-            const int64_t i2 = y0 + j;
-            const int yy0 = (int)(max((int64_t)0, i2 - P) - r0);
+#pragma unroll
+        for (int m = 0; m < YL; ++m) {
+            const int e = tid + NT * m;
+            if (e >= T * E) break;
             double s = 0.0;
 #pragma unroll
-            for (int vy = 0; vy < V; ++vy)
-                if (yy0 + vy < E) s = fma(pwy[j * V + vy], hz[(yy0 + vy) * E + c], s);
+            for (int vy = 0; vy < V; ++vy) s = fma(wy[m][vy], hz[min(ystart[m] + vy * E, E * E - 1)], s);
             gy[e] = s;
         }
         __syncthreads();
-        for (int e = tid; e < T * T; e += blockDim.x) {
-            const int j = e / T, i = e % T;
-            const int64_t i1 = x0 + i, i2 = y0 + j;
-            if (i1 >= N || i2 >= N) continue;
-            const int64_t row = (i3 * N + i2) * N + i1;
-            if (row < a.row_begin || row >= a.row_end) continue;
-            const int cc0 = (int)(max((int64_t)0, i1 - P) - c0);
+        const int64_t plane_row = i3 * pr - a.row_begin;
+#pragma unroll
+        for (int m = 0; m < XL; ++m) {
+            if (xrow[m] < 0) continue;
+            const int64_t r = plane_row + xrow[m];
+            if (r < 0 || r >= a.row_end - a.row_begin) continue;
             double s = 0.0;
 #pragma unroll
-            for (int vx = 0; vx < V; ++vx)
-                if (cc0 + vx < E) s = fma(pwx[i * V + vx], gy[j * E + cc0 + vx], s);
-            b[row - a.row_begin] = s;
+            for (int vx = 0; vx < V; ++vx) s = fma(wx[m][vx], gy[min(xg[m] + vx, T * E - 1)], s);
+            b[r] = s;
         }
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -850,7 +889,7 @@ int launch_load_pd(const GenericArgs& a, const double* PW, double* b, cudaStream
         const int64_t pr = a.N * a.N;
         const int64_t planes = (a.row_end - 1) / pr - a.row_begin / pr + 1;
         constexpr int V = P + 2, E = kLZT + V - 1;
-        const size_t smem = (size_t)((V + kLZA) * E * E + E * E + kLZT * E + 2 * kLZT * V) * sizeof(double);
+        const size_t smem = (size_t)((V + kLZA) * E * E + E * E + kLZT * E) * sizeof(double);
         if (cudaFuncSetAttribute(k_load_grid_zslide<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
             cudaSuccess)
             return WGQ_ECUDA;
