@@ -164,6 +164,26 @@ def wgq_nnz(rules, row_begin, row_end):
 
 
 # ---------------------------------------------------------------------------------------
+# argument checks (the C-ABI takes raw pointers: a wrong dtype, a host tensor or a
+# non-contiguous view would be read or written out of bounds, so refuse them here)
+# ---------------------------------------------------------------------------------------
+def _need(t, name, dtype="float64", numel=None, device=True):
+    import torch
+    want = {"float64": torch.float64, "int64": torch.int64, "int32": torch.int32}[dtype]
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name}: expected a torch.Tensor")
+    if t.dtype != want:
+        raise TypeError(f"{name}: expected dtype {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name}: expected a contiguous tensor")
+    if device and not t.is_cuda:
+        raise ValueError(f"{name}: expected a CUDA tensor")
+    if numel is not None and t.numel() < numel:
+        raise ValueError(f"{name}: needs at least {numel} elements, has {t.numel()}")
+    return t
+
+
+# ---------------------------------------------------------------------------------------
 # descriptors
 # ---------------------------------------------------------------------------------------
 def make_coeff(desc, grid=None, plane0=0):
@@ -192,6 +212,8 @@ def make_coeff(desc, grid=None, plane0=0):
         c.kind = WGQ_COEF_GRID
         if grid is None:
             raise ValueError("grid coefficient needs a device grid tensor")
+        if not hasattr(grid, "arr"):                   # bench's host-array adapter is checked by the library
+            _need(grid, "grid")
         c.grid = grid.data_ptr()
         keep.append(grid)                  # the descriptor holds a raw pointer: keep the tensor alive
         c.grid_plane0 = int(plane0)
@@ -206,6 +228,15 @@ def make_out(values, row_begin, row_end, ld=None, layout=WGQ_ELL, row_ptr=None):
     o = wgq_out_t()
     o.layout = layout
     o.row_begin, o.row_end = int(row_begin), int(row_end)
+    if values is not None:
+        rows = max(0, int(row_end) - int(row_begin))
+        if layout == WGQ_ELL:
+            lde = int(ld if ld is not None else (values.shape[1] if values.dim() == 2 else 0))
+            _need(values, "values", numel=rows * lde)
+        else:
+            _need(values, "values")
+    if row_ptr is not None:
+        _need(row_ptr, "row_ptr", "int64", numel=max(0, int(row_end) - int(row_begin)) + 1)
     o.values = values.data_ptr() if values is not None else None
     o.ld = int(ld if ld is not None else (values.shape[1] if values is not None and values.dim() == 2 else 0))
     o.row_ptr = row_ptr.data_ptr() if row_ptr is not None else None
@@ -232,32 +263,44 @@ def wgq_assemble_mass_stiffness(rules, coeff, M, K, stream=None):
 
 
 def wgq_csr_structure(rules, row_begin, row_end, row_ptr, col_idx, stream=None):
+    _need(row_ptr, "row_ptr", "int64", numel=max(0, row_end - row_begin) + 1)
+    if col_idx is not None:
+        _need(col_idx, "col_idx", "int32", numel=wgq_nnz(rules, row_begin, row_end))
     _check("wgq_csr_structure", lib().wgq_csr_structure(rules.handle, row_begin, row_end, row_ptr.data_ptr(),
                                                         col_idx.data_ptr() if col_idx is not None else None,
                                                         _stream(stream)))
 
 
 def wgq_assemble_load(rules, f, row_begin, row_end, b, stream=None):
+    _need(b, "b", numel=max(0, row_end - row_begin))
     _check("wgq_assemble_load", lib().wgq_assemble_load(rules.handle, ctypes.byref(f), row_begin, row_end, b.data_ptr(),
                                                         _stream(stream)))
 
 
 def wgq_apply(rules, coeff, u, u_row0, row_begin, row_end, yM=None, yK=None, stream=None):
     ptr = (lambda t: t.data_ptr() if t is not None else None)
+    _need(u, "u")
+    for name, y in (("yM", yM), ("yK", yK)):
+        if y is not None:
+            _need(y, name, numel=max(0, row_end - row_begin))
     _check("wgq_apply", lib().wgq_apply(rules.handle, ctypes.byref(coeff), u.data_ptr(), u_row0, u.numel(), row_begin,
                                         row_end, ptr(yM), ptr(yK), _stream(stream)))
 
 
 def wgq_generate_grid(n_elems, dim, seed, sigma, plane0, planes, grid, stream=None):
+    _need(grid, "grid", numel=planes * (n_elems + 1) ** (dim - 1) if dim > 1 else n_elems + 1)
     _check("wgq_generate_grid", lib().wgq_generate_grid(n_elems, dim, seed, sigma, plane0, planes, grid.data_ptr(),
                                                         _stream(stream)))
 
 
 def wgq_row_moments(rules, A, out, stream=None):
+    _need(out, "out", numel=max(0, A.row_end - A.row_begin) * (1 + rules.dim))
     _check("wgq_row_moments", lib().wgq_row_moments(rules.handle, ctypes.byref(A), out.data_ptr(), _stream(stream)))
 
 
 def wgq_checksum(rules, A, out, stream=None):
+    if out.element_size() != 8 or out.numel() < 3 or not out.is_cuda or not out.is_contiguous():
+        raise ValueError("out: expected a contiguous CUDA tensor of >= 3 8-byte elements")
     _check("wgq_checksum", lib().wgq_checksum(rules.handle, ctypes.byref(A), out.data_ptr(), _stream(stream)))
 
 
