@@ -83,3 +83,30 @@ def test_no_out_of_bounds_writes(case):
     torch.cuda.synchronize()
     check_guards(bym, rows, f"apply M {p, n, d}")
     check_guards(byk, rows, f"apply K {p, n, d}")
+
+
+@pytest.mark.parametrize("p,n,d,kind", [(3, 6, 3, "grid"), (2, 9, 2, "fourier"), (3, 5, 3, "trig"), (2, 7, 1, "const")])
+def test_empty_row_ranges_write_nothing(p, n, d, kind):
+    """row_begin == row_end (a rank with no rows) is a no-op for every entry point, at any row."""
+    from paper_1710_01048_b200 import api, wgq
+    r = wgq.Rules(p, n, d)
+    gt = None
+    if kind == "grid":
+        gt = torch.from_numpy(np.ascontiguousarray(inputs.lognormal_grid(n, seed=3, dim=d))).cuda()
+    desc = {"grid": {"kind": "grid"}, "const": {"kind": "const", "c0": 1.0},
+            "trig": {"kind": "trig_sep", "c0": 1.0, "amp": 0.4, "trig": ("sin", "cos", "sin")[:d], "wavenum": (1, 2, 1)[:d]},
+            "fourier": inputs.coefficient({"kind": "fourier_logn", "seed": 1, "n_modes": 8, "amp": 0.3}, d)}[kind]
+    c = api.coefficient(desc, gt, 0)
+    for at in (0, r.n_rows // 2, r.n_rows):
+        buf, view = guarded(0)
+        out = {"mass": view.view(0, r.stencil), "stiffness": view.view(0, r.stencil)}
+        api.assemble(r, c, ("mass", "stiffness"), at, at, out=out)
+        row_ptr = torch.full((1,), 123, dtype=torch.int64, device="cuda")
+        wgq.wgq_csr_structure(r, at, at, row_ptr, None)           # row_ptr = [0]: slab-local, from 0
+        api.assemble_load(r, c, at, at, out=view)
+        u = torch.randn(r.n_rows, dtype=torch.float64, device="cuda")
+        y = api.apply(r, c, u, ("mass", "stiffness"), at, at)
+        torch.cuda.synchronize()
+        assert all(v.numel() == 0 for v in y.values())
+        assert int(row_ptr[0].item()) == 0
+        check_guards(buf, 0, f"empty range at {at}")
