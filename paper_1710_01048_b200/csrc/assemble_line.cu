@@ -808,15 +808,15 @@ __global__ void __launch_bounds__(256, 3) k_line_apply(const __grid_constant__ L
             int upos = d.upos + 8 * nt + g;
             upos = upos >= URING ? upos - URING : upos;
             const double* urow = (xv ? U + upos * HS : zrow) + t4;
-            double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;     // two chains: even / odd k-steps
+            constexpr int KSD = (S2 + 3) / 4;                  // k-steps; padding columns are zero: no masks
+            double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};   // four independent chains
+            if (!(a.dbg & 8)) {
 #pragma unroll
-            for (int s = 0; s < ((a.dbg & 8) ? 0 : (S2 + 3) / 4); ++s) {      // padding columns are zero: no masks
-                if (s & 1) dmma(e0, e1, hrow[4 * s], urow[4 * s]);
-                else dmma(d0, d1, hrow[4 * s], urow[4 * s]);
+                for (int s = 0; s < KSD; ++s) dmma(acc[s & 3][0], acc[s & 3][1], hrow[4 * s], urow[4 * s]);
             }
             double* D = kind ? Dk : Dm;
-            D[(8 * mt + g) * 16 + 8 * nt + 2 * t4] = d0 + e0;
-            D[(8 * mt + g) * 16 + 8 * nt + 2 * t4 + 1] = d1 + e1;
+            D[(8 * mt + g) * 16 + 8 * nt + 2 * t4] = (acc[0][0] + acc[1][0]) + (acc[2][0] + acc[3][0]);
+            D[(8 * mt + g) * 16 + 8 * nt + 2 * t4 + 1] = (acc[0][1] + acc[1][1]) + (acc[2][1] + acc[3][1]);
         }
         __syncthreads();
         // ---- S1b: rows of tile k (one per warp), phase A of tile k+1, prefetch tile k+PFD ----
