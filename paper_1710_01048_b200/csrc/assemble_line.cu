@@ -263,14 +263,14 @@ struct TileIt {
     int X0, lpos, ulo, uhi;   // line's first column, its ring position, new columns [ulo, uhi]
 };
 
-template <int P>
+template <int P, int TR_ = Cfg<P>::TR>
 __device__ __forceinline__ void it_planes(TileIt& t, int N) {
     constexpr int V = P + 2;
     t.lo = t.t0 == t.x0 ? max(0, t.x0 - P) : max(0, t.t0 - 1 - P) + V;
-    t.hi = max(0, min(t.t0 + Cfg<P>::TR, t.x1) - 1 - P) + V - 1;
+    t.hi = max(0, min(t.t0 + TR_, t.x1) - 1 - P) + V - 1;
     t.X0 = max(0, t.x0 - P);
     t.ulo = t.t0 == t.x0 ? t.X0 : min(N - 1, t.t0 - 1 + P) + 1;
-    t.uhi = min(N - 1, min(t.t0 + Cfg<P>::TR, t.x1) - 1 + P);
+    t.uhi = min(N - 1, min(t.t0 + TR_, t.x1) - 1 + P);
 }
 
 template <int P>
@@ -282,19 +282,19 @@ __device__ __forceinline__ void it_line(const LineArgs& a, TileIt& t) {
     t.t0 = t.x0;
 }
 
-template <int P>
+template <int P, int TR_ = Cfg<P>::TR>
 __device__ __forceinline__ void it_init(const LineArgs& a, TileIt& t) {
     t.line = a.row_begin / a.N + blockIdx.x;
     t.qs = 0;
     t.ps = 0;
     t.lpos = 0;
     it_line<P>(a, t);
-    it_planes<P>(t, a.N);
+    it_planes<P, TR_>(t, a.N);
 }
 
-template <int P, int PFD_ = Cfg<P>::PFD, int URING_ = ApplyCfg::URING>
+template <int P, int PFD_ = Cfg<P>::PFD, int URING_ = ApplyCfg::URING, int TR_ = Cfg<P>::TR>
 __device__ __forceinline__ void it_next(const LineArgs& a, TileIt& t) {
-    t.t0 += Cfg<P>::TR;
+    t.t0 += TR_;
     t.ps = t.ps == PFD_ - 1 ? 0 : t.ps + 1;
     if (t.t0 >= t.x1) {
         t.lpos = (t.lpos + min(a.N - 1, t.x1 - 1 + P) - t.X0 + 1) % URING_;   // finished line's columns
@@ -302,14 +302,14 @@ __device__ __forceinline__ void it_next(const LineArgs& a, TileIt& t) {
         t.qs = t.qs == PFD_ - 1 ? 0 : t.qs + 1;
         it_line<P>(a, t);
     }
-    it_planes<P>(t, a.N);
+    it_planes<P, TR_>(t, a.N);
 }
 
 // Issue (cp.async, one commit group) everything tile t reads from global memory: its new
 // vertex planes into patch buffer t.ps and, for a line's first tile, the line's y/z vertex
 // tables into Q buffer t.qs (and the thread's patch row).  An exhausted iterator commits an
 // empty group.
-template <int P, int NT = Cfg<P>::NT>
+template <int P, int NT = Cfg<P>::NT, int PATCH_ = Cfg<P>::PATCH>
 __device__ __forceinline__ void tile_issue(const LineArgs& a, double* patches, double* qbufs, const TileIt& t,
                                            PatchRow& pr, int last_line, int tid) {
     using C = Cfg<P>;
@@ -324,7 +324,7 @@ __device__ __forceinline__ void tile_issue(const LineArgs& a, double* patches, d
                 cp_async8(Q + e, ((which & 1) ? a.T.PK : a.T.PM) + ((size_t)r * kMaxV + v) * kMaxS + o, true);
             }
         }
-        load_patch<P>(a, pr, patches + t.ps * C::PATCH, t.lo, t.hi - t.lo + 1, tid);
+        load_patch<P>(a, pr, patches + t.ps * PATCH_, t.lo, t.hi - t.lo + 1, tid);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
@@ -381,12 +381,12 @@ __device__ __forceinline__ TileCsr make_csr(const LineArgs& a, const TileIt& t, 
     return d;
 }
 
-template <int P, int URING_ = ApplyCfg::URING>
+template <int P, int URING_ = ApplyCfg::URING, int TR_ = Cfg<P>::TR>
 __device__ __forceinline__ TileDesc make_desc(const LineArgs& a, const TileIt& t, int last_line, bool padded) {
     TileDesc d;
     d.line = t.line <= last_line ? t.line : -1;
     d.t0 = t.t0;
-    d.tr = min(Cfg<P>::TR, t.x1 - t.t0);
+    d.tr = min(TR_, t.x1 - t.t0);
     d.lo = t.lo;
     d.nnew = t.hi - t.lo + 1;
     d.ps = t.ps;
@@ -413,11 +413,11 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // permuted, column 2t+i <-> vz = t + 4i, so each lane ends A1 holding exactly its A2 A-fragment
 // (TT[g][t], TT[g][t+4]): no shuffle or shared-memory round trip between the two products.
 // Padding rows / columns (o2, o3 >= S, vy, vz >= V) carry zero coefficients.
-template <int P, int NT = Cfg<P>::NT, int HS = Cfg<P>::S2>
+template <int P, int NT = Cfg<P>::NT, int HS = Cfg<P>::S2, int RING = Cfg<P>::RING, int PATCH_ = Cfg<P>::PATCH>
 __device__ __forceinline__ void phase_a(const LineArgs& a, const TileDesc& t, const double* patches,
                                         const double* qbufs, double* Hm, double* Hk, int tid) {
     using C = Cfg<P>;
-    constexpr int V = C::V, S = C::S, RING = C::RING;
+    constexpr int V = C::V, S = C::S;
     constexpr int KS = (V + 3) / 4;                    // k-steps of 4 (p=3: 2, p=2: 1)
     constexpr int NW = NT / 32;
     const int lane = tid & 31, warp = tid >> 5, g = lane >> 2, tq = lane & 3;
@@ -433,7 +433,7 @@ __device__ __forceinline__ void phase_a(const LineArgs& a, const TileDesc& t, co
         bZM[s] = ok ? Q[2 * V * S + e] : 0.0;
         bZK[s] = ok ? Q[3 * V * S + e] : 0.0;
     }
-    const double* patch = patches + t.ps * C::PATCH;
+    const double* patch = patches + t.ps * PATCH_;
     const int nnew = t.nnew;
     const int vzp = (g >> 1) + 4 * (g & 1);            // B column g of A1 <-> vz = pi(g)
     for (int j = NW - 1 - warp; j < ((a.dbg & 65) ? 0 : nnew); j += NW) {
@@ -697,28 +697,56 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const __grid_const
 // Row i of M is sum_vx PMx[vx][o1] HM[bx+vx][o2,o3] (the assembly's phase B), so
 //   y^M_i = sum_{vx,o1} PMx[vx][o1] D_M(bx+vx, i1-p+o1),   D_X(c, X) = sum_{o2,o3} H_X[c][o2,o3] u[X][i2-p+o2][i3-p+o3]
 //   y^K_i = sum_{vx,o1} PKx[vx][o1] D_M(..) + PMx[vx][o1] D_K(..)
-// — the definition y_i = sum_j A_ij u_j with the sums reordered.  Per tile of TR rows the D
-// values for all (vertex plane c, column X) of the tile's window are one (16 x 49) x (49 x 16)
-// product per matrix on the FP64 tensor cores (8 DMMA m8n8k4 items of 13 k-steps, one or two
-// per warp); the H planes come from the assembly's phase A, the u columns X (49 values each)
-// are prefetched with the vertex patches into a ring.  Nothing is stored but y.
-template <int P, int MODE>
-__global__ void __launch_bounds__(256, 3) k_line_apply(const __grid_constant__ LineArgs a) {
+// — the definition y_i = sum_j A_ij u_j with the sums reordered.  Per tile of TRA rows (24:
+// the per-tile iterator / descriptor / barrier cost is spread over three times the rows of the
+// assembly's tiles, at 2 CTAs per SM) the D values for the (vertex plane c, column X) pairs of
+// the tile's window are a banded (32 x 49) x (49 x 32) product per matrix on the FP64 tensor
+// cores (the 10 of 16 8x8 blocks with |X - c| <= 1 block, DMMA m8n8k4 items of 13 k-steps);
+// the H planes come from the assembly's phase A, the u columns X (49 values each) are
+// prefetched with the vertex patches into a ring.  Nothing is stored but y.
+// Tile geometry of the apply for TRA rows per tile: the vertex-plane window (TRA + p + 1 planes,
+// H ring RING_A >= that), the D product's plane x column blocks of 8 (only blocks within the band
+// |column - plane| <= 1 block carry nonzero P^ weights), the u ring (the next tile's window of
+// TRA + 2p columns plus PFD - 1 further tiles of up to TRA + p new columns).
+template <int P, int TRA>
+struct ApplyGeom {
+    static constexpr int V = P + 2, S = 2 * P + 1, S2 = S * S;
+    static constexpr int W = TRA + V - 1;                              // planes of a tile's window
+    static constexpr int RING = W <= 16 ? 16 : (W <= 32 ? 32 : 64);   // power of two >= W
+    static constexpr int PATCH = W * V * V;
+    static constexpr int PFD = ApplyCfg::PFD;
+    static constexpr int DB = (W + 7) / 8;                             // plane blocks of D
+    static constexpr int XBK = (TRA + 2 * P + 7) / 8;                  // column blocks of D
+    static constexpr int DR = DB * 8, DC = XBK * 8;                    // D extents
+    static constexpr int UXMAX = (TRA + P + 7) / 8 * 8;                // new columns per tile (bound)
+    // live columns when tile k+PFD is issued: tile k+1's window and the new columns of k+2..k+PFD
+    static constexpr int URING = TRA == 8 ? ApplyCfg::URING : (TRA + 2 * P) + (PFD - 1) * (TRA + P) + 1;
+    static constexpr int HS = (S2 + 3) / 4 * 4 + ((S2 + 3) / 4 % 2 == 0 ? 4 : 0);   // row stride = 4 (mod 8)
+    // band blocks (mt, nt) with |nt - mt| <= 1, in order
+    static constexpr int NB = DB * XBK - ((DB > 2 ? (DB - 2) * (DB - 1) / 2 : 0) + (XBK > 2 ? (XBK - 2) * (XBK - 1) / 2 : 0));
+    static constexpr size_t smem_doubles() {
+        return (size_t)2 * RING * HS + PFD * 4 * V * S + PFD * PATCH + 4 * P * 2 * V * S + (size_t)URING * HS +
+               2 * DR * DC + 2 * V * S + HS;
+    }
+};
+
+template <int P, int MODE, int TRA>
+__global__ void __launch_bounds__(256, TRA == 8 ? 3 : 2) k_line_apply(const __grid_constant__ LineArgs a) {
     using C = Cfg<P>;
-    constexpr int S = C::S, S2 = C::S2, V = C::V, RING = C::RING, URING = ApplyCfg::URING, PFD = ApplyCfg::PFD;
-    // 8 warps: one D item and one phase-A plane each per tile; warp 0 finishes the tile's rows
+    using G = ApplyGeom<P, TRA>;
+    constexpr int S = C::S, S2 = C::S2, V = C::V, RING = G::RING, URING = G::URING, PFD = G::PFD;
     constexpr int NT = 256;
-    constexpr int HS = (S2 + 3) / 4 * 4 + ((S2 + 3) / 4 % 2 == 0 ? 4 : 0);   // row stride = 4 (mod 8): conflict-free fragments
+    constexpr int HS = G::HS, DC = G::DC;
     extern __shared__ __align__(128) double sm[];
     double* Hm = sm;                                      // [RING][HS]
     double* Hk = Hm + RING * HS;
     double* qbufs = Hk + RING * HS;                       // [PFD][4][V][S]
     double* patches = qbufs + PFD * 4 * V * S;            // [PFD][W][V][V]
-    double* xbt = patches + PFD * C::PATCH;               // [4P][2][V][S]
+    double* xbt = patches + PFD * G::PATCH;               // [4P][2][V][S]
     double* U = xbt + C::XB;                              // [URING][HS]
-    double* Dm = U + URING * HS;                          // [16][16]  D_M(c - b0, X - Xlo)
-    double* Dk = Dm + 256;
-    double* pint = Dk + 256;                              // [2][V][S]: interior P^ (h, 1/h folded)
+    double* Dm = U + URING * HS;                          // [DR][DC]  D_M(c - b0, X - Xlo)
+    double* Dk = Dm + G::DR * DC;
+    double* pint = Dk + G::DR * DC;                       // [2][V][S]: interior P^ (h, 1/h folded)
     double* zrow = pint + 2 * V * S;                      // [HS] zeros: operand row of invalid planes / columns
     __shared__ TileDesc desc[8];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -739,7 +767,7 @@ __global__ void __launch_bounds__(256, 3) k_line_apply(const __grid_constant__ L
     // u loads: thread tid owns elements e = tid + NT m (m < MU) of a tile's new columns, laid
     // out as [x-offset block][o23][x-offset & 7] so a warp reads contiguous runs along X; the
     // (o23, x-offset) of each element is fixed, its global row offset changes once per line
-    constexpr int MU = (16 * S2 + NT - 1) / NT;
+    constexpr int MU = (G::UXMAX * S2 + NT - 1) / NT;
     int uxo[MU], uo23[MU];
     long long ubase[MU];
 #pragma unroll
@@ -764,7 +792,7 @@ __global__ void __launch_bounds__(256, 3) k_line_apply(const __grid_constant__ L
             const int p0 = (t.lpos + t.ulo - t.X0) % URING;            // ring position of column ulo
 #pragma unroll
             for (int m = 0; m < MU; ++m) {
-                if (uxo[m] >= nx || uxo[m] >= 16) continue;
+                if (uxo[m] >= nx || uxo[m] >= G::UXMAX) continue;
                 const int X = t.ulo + uxo[m];
                 const bool ok = ubase[m] >= 0;
                 int pos = p0 + uxo[m];
@@ -772,22 +800,22 @@ __global__ void __launch_bounds__(256, 3) k_line_apply(const __grid_constant__ L
                 cp_async8(U + pos * HS + uo23[m], a.u + (ok ? ubase[m] + X : 0), ok);
             }
         }
-        tile_issue<P, NT>(a, patches, qbufs, t, pr, last_line, tid);     // commits the group
+        tile_issue<P, NT, G::PATCH>(a, patches, qbufs, t, pr, last_line, tid);     // commits the group
     };
     TileIt itP;
     PatchRow prow;
     prow.base = nullptr;
-    it_init<P>(a, itP);
+    it_init<P, TRA>(a, itP);
     for (int k = 0; k < PFD; ++k) {
         issue(itP, prow);
-        if (tid == 0) desc[k] = make_desc<P, URING>(a, itP, last_line, false);
-        if (itP.line <= last_line) it_next<P, PFD, URING>(a, itP);
+        if (tid == 0) desc[k] = make_desc<P, URING, TRA>(a, itP, last_line, false);
+        if (itP.line <= last_line) it_next<P, PFD, URING, TRA>(a, itP);
     }
     cp_async_wait<PFD - 1>();
     __syncthreads();
     {
         const TileDesc d0 = desc[0];
-        if (d0.line >= 0) phase_a<P, NT, HS>(a, d0, patches, qbufs, Hm, Hk, tid);
+        if (d0.line >= 0) phase_a<P, NT, HS, RING, G::PATCH>(a, d0, patches, qbufs, Hm, Hk, tid);
     }
     cp_async_wait<PFD - 2>();
     __syncthreads();
@@ -799,8 +827,20 @@ __global__ void __launch_bounds__(256, 3) k_line_apply(const __grid_constant__ L
         const int b0 = max(0, d.t0 - P);
         const int hi_plane = max(0, d.t0 + d.tr - 1 - P) + V - 1;
         // ---- S1a: D_X = H_X (planes b0..) x U (columns Xlo..) on the tensor cores ----------
-        {
-            const int kind = warp >> 2, mt = (warp >> 1) & 1, nt = warp & 1;
+        // items: (matrix, band block); block b enumerates (mt, nt) with |nt - mt| <= 1
+#pragma unroll
+        for (int it = warp; it < 2 * G::NB; it += 8) {
+            const int kind = it / G::NB;
+            int b = it % G::NB, mt = 0, nt = 0;
+            for (int q = 0, cnt = 0; q < G::DB * G::XBK; ++q) {
+                const int qm = q / G::XBK, qn = q % G::XBK;
+                if (qn - qm > 1 || qm - qn > 1) continue;
+                if (cnt++ == b) {
+                    mt = qm;
+                    nt = qn;
+                    break;
+                }
+            }
             const double* H = kind ? Hk : Hm;
             const int c = b0 + 8 * mt + g, X = d.Xlo + 8 * nt + g;
             const bool cv = c <= hi_plane, xv = X <= d.Xhi;
@@ -815,15 +855,15 @@ __global__ void __launch_bounds__(256, 3) k_line_apply(const __grid_constant__ L
                 for (int s = 0; s < KSD; ++s) dmma(acc[s & 3][0], acc[s & 3][1], hrow[4 * s], urow[4 * s]);
             }
             double* D = kind ? Dk : Dm;
-            D[(8 * mt + g) * 16 + 8 * nt + 2 * t4] = (acc[0][0] + acc[1][0]) + (acc[2][0] + acc[3][0]);
-            D[(8 * mt + g) * 16 + 8 * nt + 2 * t4 + 1] = (acc[0][1] + acc[1][1]) + (acc[2][1] + acc[3][1]);
+            D[(8 * mt + g) * DC + 8 * nt + 2 * t4] = (acc[0][0] + acc[1][0]) + (acc[2][0] + acc[3][0]);
+            D[(8 * mt + g) * DC + 8 * nt + 2 * t4 + 1] = (acc[0][1] + acc[1][1]) + (acc[2][1] + acc[3][1]);
         }
         __syncthreads();
-        // ---- S1b: rows of tile k (one per warp), phase A of tile k+1, prefetch tile k+PFD ----
-        if (warp == 0 && !(a.dbg & 32)) {
-            // warp 0 finishes all rows of the tile: lane (j, vq) = row t0 + j, vertex planes
-            // vx = vq (+4); y = sum_{vx,o1} P[vx][o1] D(b_r + vx, r - p + o1), reduced over 4 lanes
-            const int j = lane >> 2, vq = lane & 3;
+        // ---- S1b: rows of tile k, phase A of tile k+1, prefetch tile k+PFD ------------------
+        if (warp < TRA / 8 && !(a.dbg & 32)) {
+            // warp w finishes rows 8w..8w+7 of the tile: lane (j, vq) = row t0 + 8w + j, vertex
+            // planes vx = vq (+4); y = sum_{vx,o1} P[vx][o1] D(b_r + vx, r - p + o1), over 4 lanes
+            const int j = 8 * warp + (lane >> 2), vq = lane & 3;
             double ym = 0.0, yk = 0.0;
             if (j < d.tr) {
                 const int r = d.t0 + j, br = max(0, r - P);
@@ -834,8 +874,8 @@ __global__ void __launch_bounds__(256, 3) k_line_apply(const __grid_constant__ L
                 for (int vv = 0; vv < 2; ++vv) {
                     const int vx = vq + 4 * vv;
                     if (vx >= V) break;
-                    const double* dmr = Dm + (br + vx - b0) * 16 - d.Xlo;
-                    const double* dkr = Dk + (br + vx - b0) * 16 - d.Xlo;
+                    const double* dmr = Dm + (br + vx - b0) * DC - d.Xlo;
+                    const double* dkr = Dk + (br + vx - b0) * DC - d.Xlo;
 #pragma unroll
                     for (int o1 = 0; o1 < S; ++o1) {
                         const int X = r - P + o1;
@@ -856,23 +896,26 @@ __global__ void __launch_bounds__(256, 3) k_line_apply(const __grid_constant__ L
                 if (MODE & 2) a.yK[d.orow0 + j] = yk;
             }
         }
-        if (dA.line >= 0) phase_a<P, NT, HS>(a, dA, patches, qbufs, Hm, Hk, tid);
+        if (dA.line >= 0) phase_a<P, NT, HS, RING, G::PATCH>(a, dA, patches, qbufs, Hm, Hk, tid);
         issue(itP, prow);                                            // tile k+PFD
-        if (tid == NT - 1) desc[(k + PFD) & 7] = make_desc<P, URING>(a, itP, last_line, false);   // warp 0 finishes rows
-        if (itP.line <= last_line) it_next<P, PFD, URING>(a, itP);
+        if (tid == NT - 1) desc[(k + PFD) & 7] = make_desc<P, URING, TRA>(a, itP, last_line, false);
+        if (itP.line <= last_line) it_next<P, PFD, URING, TRA>(a, itP);
         cp_async_wait<PFD - 2>();                                    // tile k+2 landed
         __syncthreads();
     }
     cp_async_wait<0>();
 }
 
+#ifndef WGQ_APPLY_TR
+#define WGQ_APPLY_TR 24
+#endif
+
 template <int P, int MODE>
 int launch_apply_p(const LineArgs& a, cudaStream_t st) {
-    using C = Cfg<P>;
-    constexpr int HS = (C::S2 + 3) / 4 * 4 + ((C::S2 + 3) / 4 % 2 == 0 ? 4 : 0);
-    const size_t smem = (size_t)(2 * C::RING * HS + ApplyCfg::PFD * 4 * C::V * C::S + ApplyCfg::PFD * C::PATCH +
-                                 C::XB + ApplyCfg::URING * HS + 512 + 2 * C::V * C::S + HS) * sizeof(double);
-    auto kern = k_line_apply<P, MODE>;
+    constexpr int TRA = WGQ_APPLY_TR;
+    using G = ApplyGeom<P, TRA>;
+    const size_t smem = G::smem_doubles() * sizeof(double);
+    auto kern = k_line_apply<P, MODE, TRA>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return WGQ_ECUDA;
     int dev = 0, sms = 148, per_sm = 1;
