@@ -36,24 +36,30 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // exp(x) for |x| < 700 in ~20 FP64 instructions: x = k ln2 + r (Cody-Waite, |r| <= ln2/2),
 // e^r by its degree-13 Taylor polynomial (truncation < 2e-16 relative), times 2^k.  Within
 // ~2 ulp of the correctly rounded value (the FOURIER_LOGN exponents are O(1), R13).
+__constant__ double kExpTaylor[14] = {1.0,
+                                      1.0,
+                                      0.5,
+                                      1.0 / 6.0,
+                                      1.0 / 24.0,
+                                      1.0 / 120.0,
+                                      1.0 / 720.0,
+                                      1.0 / 5040.0,
+                                      1.0 / 40320.0,
+                                      1.0 / 362880.0,
+                                      1.0 / 3628800.0,
+                                      1.0 / 39916800.0,
+                                      1.0 / 479001600.0,
+                                      1.0 / 6227020800.0};
+
 __device__ __forceinline__ double exp_fast(double x) {
+    // the Taylor coefficients come from the constant bank (DFMA operands), not 64-bit immediates
+    // that the compiler would rebuild in uniform registers on every call
     const double k = rint(x * 1.4426950408889634);
     double r = fma(-k, 6.93147180369123816490e-01, x);
     r = fma(-k, 1.90821492927058770002e-10, r);
-    double q = 1.0 / 6227020800.0;
-    q = fma(q, r, 1.0 / 479001600.0);
-    q = fma(q, r, 1.0 / 39916800.0);
-    q = fma(q, r, 1.0 / 3628800.0);
-    q = fma(q, r, 1.0 / 362880.0);
-    q = fma(q, r, 1.0 / 40320.0);
-    q = fma(q, r, 1.0 / 5040.0);
-    q = fma(q, r, 1.0 / 720.0);
-    q = fma(q, r, 1.0 / 120.0);
-    q = fma(q, r, 1.0 / 24.0);
-    q = fma(q, r, 1.0 / 6.0);
-    q = fma(q, r, 0.5);
-    q = fma(q, r, 1.0);
-    q = fma(q, r, 1.0);
+    double q = kExpTaylor[13];
+#pragma unroll
+    for (int i = 12; i >= 0; --i) q = fma(q, r, kExpTaylor[i]);
     return q * __longlong_as_double((long long)(1023 + (int)k) << 52);
 }
 
