@@ -633,13 +633,20 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const __grid_const
                 const int o2 = o23 % S, o3 = o23 / S;
                 if (o2 >= dc.lo2 && o2 <= dc.hi2 && o3 >= dc.lo3 && o3 <= dc.hi3) {
                     const int pos23 = (o2 - dc.lo2) + dc.a2 * (o3 - dc.lo3);
-                    const long long At0 = csr_A(d.t0, P, a.N);
-                    const int off0 = (int)(dc.w23 * (csr_A(r, P, a.N) - At0));
-                    const int ar0 = (int)csr_a(r, P, a.N);
-                    if (r >= 2 * P && r + 1 <= n - 1 - P) {   // both rows class I: a(r) = 2p+1, lo1 = 0
+                    if (r >= 2 * P && r + 1 <= n - 1 - P && d.t0 >= P) {
+                        // both rows class I and every row from t0 on has a(.) = 2p+1 columns:
+                        // A(r) - A(t0) = (2p+1)(r - t0), lo1 = 0
+                        const int off0 = dc.w23 * S * (r - d.t0);
+                        finish_pair_interior<P, MODE>(hm, hk, stM + off0 + S * pos23, stK + off0 + S * pos23, S * dc.w23,
+                                                      second, a);
+                    } else if (r >= 2 * P && r + 1 <= n - 1 - P) {
+                        const int off0 = (int)(dc.w23 * (csr_A(r, P, a.N) - csr_A(d.t0, P, a.N)));
                         finish_pair_interior<P, MODE>(hm, hk, stM + off0 + S * pos23, stK + off0 + S * pos23, S * dc.w23,
                                                       second, a);
                     } else {
+                        const long long At0 = csr_A(d.t0, P, a.N);
+                        const int off0 = (int)(dc.w23 * (csr_A(r, P, a.N) - At0));
+                        const int ar0 = (int)csr_a(r, P, a.N);
                         const int lo1 = max(0, P - r), hi1 = min(2 * P, a.N - 1 - r + P);
                         double* dM = stM + off0 + ar0 * pos23 - lo1;
                         double* dK = stK + off0 + ar0 * pos23 - lo1;
