@@ -40,7 +40,7 @@ struct Cfg {
     static constexpr int S2 = S * S;
     static constexpr int S3 = S2 * S;
     static constexpr int V = P + 2;
-    static constexpr int TR = 8;                       // rows per tile
+    static constexpr int TR = 12;                      // rows per tile
     static constexpr int RPT = 2;                      // consecutive rows per thread in phase B
     static constexpr int ITEMS = TR / RPT * S2;        // (row pair, o2 o3) items per tile
     static constexpr int NT = (ITEMS + 31) / 32 * 32;  // threads
@@ -520,7 +520,7 @@ __device__ __forceinline__ void store_mat(const LineArgs& a, double* out, const 
 }
 
 template <int P, int MODE, bool CSR>
-__global__ void __launch_bounds__(Cfg<P>::NT, 3) k_line_grid3(const __grid_constant__ LineArgs a) {
+__global__ void __launch_bounds__(Cfg<P>::NT, 2) k_line_grid3(const __grid_constant__ LineArgs a) {
     using C = Cfg<P>;
     constexpr int S = C::S, S2 = C::S2, S3 = C::S3, V = C::V, RING = C::RING;
     extern __shared__ __align__(128) double sm[];
