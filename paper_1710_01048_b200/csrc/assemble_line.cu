@@ -17,7 +17,7 @@
 // Interior x-rows (class I) share one table P^ (times h resp. 1/h), passed as kernel
 // parameters (constant bank, read through uniform registers); its zero pattern is structural
 // (a node in element k touches planes k, k+1 and columns k..k+p), so phase B issues only the
-// structurally nonzero FP64 FMAs.  A CTA (3 per SM) owns a line, walks it in tiles of TR = 8 rows (each thread
+// structurally nonzero FP64 FMAs.  A CTA (2 per SM) owns a line, walks it in tiles of TR = 12 rows (each thread
 // finishes two consecutive rows of one (o2,o3) group from a 6-plane window, so the constant
 // tables and index arithmetic are shared by both rows), prefetches the next tile's vertex
 // patch with cp.async, stages the tile's M and K rows in shared memory and writes each tile
