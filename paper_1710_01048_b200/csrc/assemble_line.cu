@@ -45,7 +45,7 @@ struct Cfg {
     static constexpr int ITEMS = TR / RPT * S2;        // (row pair, o2 o3) items per tile
     static constexpr int NT = (ITEMS + 31) / 32 * 32;  // threads
     static constexpr int W = TR + V - 1;               // vertex planes of a tile's window
-    static constexpr int RING = 16;                    // H ring (>= W), power of two
+    static constexpr int RING = TR + P + 1 <= 16 ? 16 : TR + P + 1;   // H ring (>= W planes)
     static constexpr int SR = S3 + 1;                  // staging row stride for padded ld
     static constexpr int STAGE = TR * SR + 2;          // doubles per staging buffer per matrix
     static constexpr int PATCH = W * V * V;
@@ -57,6 +57,12 @@ struct Cfg {
     static constexpr int SMEM = 2 * STAGE + RING * 2 * S2 + PFD * 4 * V * S + PFD * PATCH + XB;
     static_assert(W <= RING, "ring too small");
 };
+
+// slot of vertex plane c in an H ring of RING planes (a mask when RING is a power of two)
+template <int RING>
+__device__ __forceinline__ int ring_slot(int c) {
+    return (RING & (RING - 1)) == 0 ? (c & (RING - 1)) : c % RING;
+}
 
 struct LineArgs {
     RowTables T;
@@ -455,7 +461,7 @@ __device__ __forceinline__ void phase_a(const LineArgs& a, const TileDesc& t, co
             dmma(hK0, hK1, tK1, bZM[KS - 1]);
             dmma(hK0, hK1, tM1, bZK[KS - 1]);
         }
-        const int slot = (t.lo + j) & (RING - 1);
+        const int slot = ring_slot<RING>(t.lo + j);
         const int o3 = 2 * tq;
         if (g < S) {
             double* hm = Hm + slot * HS + g;
@@ -602,7 +608,7 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 2) k_line_grid3(const __grid_const
             double hm[V + 1], hk[V + 1];
 #pragma unroll
             for (int v = 0; v <= V; ++v) {             // planes b0 .. b0+V (the pair's union)
-                const int slot = (b0 + v) & (RING - 1);
+                const int slot = ring_slot<RING>(b0 + v);
                 hm[v] = Hm[slot * S2 + o23];
                 hk[v] = Hk[slot * S2 + o23];
             }
@@ -851,7 +857,7 @@ __global__ void __launch_bounds__(256, TRA == 8 ? 3 : 2) k_line_apply(const __gr
             const double* H = kind ? Hk : Hm;
             const int c = b0 + 8 * mt + g, X = d.Xlo + 8 * nt + g;
             const bool cv = c <= hi_plane, xv = X <= d.Xhi;
-            const double* hrow = (cv ? H + (c & (RING - 1)) * HS : zrow) + t4;
+            const double* hrow = (cv ? H + ring_slot<RING>(c) * HS : zrow) + t4;
             int upos = d.upos + 8 * nt + g;
             upos = upos >= URING ? upos - URING : upos;
             const double* urow = (xv ? U + upos * HS : zrow) + t4;
