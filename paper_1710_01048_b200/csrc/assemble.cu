@@ -729,8 +729,11 @@ __global__ void __launch_bounds__(256) k_load_grid_line(const GenericArgs a, con
 // 3D GRID load vector, z-sliding: a block owns a T x T tile of (i1, i2) and a
 // run of kLZC planes i3; b = sum_{vz,vy,vx} PW_z PW_y PW_x g is contracted z -> y -> x in
 // shared memory from a ring of the tile's vertex planes (T + p + 1 square, loaded once per
-// plane with cp.async one step ahead), so every vertex value is read from global memory about
-// once per tile instead of once per (row, vz) — the same sum as k_load, reordered.
+// plane with cp.async kLZA planes ahead of the window), so every vertex value is read from
+// global memory about once per tile instead of once per (row, vz) — the same sum as k_load,
+// reordered.  Each thread's roles (in-plane load offsets, y- and x-pass weights) are fixed per
+// block and kept in registers (T = 16: 128 threads, 128 registers, 4 blocks per SM; forcing 5-6
+// blocks spills and is slower).
 #ifndef WGQ_LZT
 #define WGQ_LZT 16
 #endif
