@@ -159,3 +159,28 @@ def test_c5_csr_full_size_sampled_rows():
     finally:
         del row_ptr, col_idx, vals
         torch.cuda.empty_cache()
+
+
+def test_c5_whole_lines_every_class():
+    """SURVEY §8(c) P10 at C5, line-wise: whole x-lines (all 259 x-positions, so every x row
+    class and every tile position of the line kernel) on the boundary / near-boundary y and z
+    classes and a few seeded interior ones, against the oracle row by row."""
+    cfg, rules, desc, out = assemble_config("C5")
+    p, n, d = cfg["p"], cfg["n"], cfg["dim"]
+    N = n + p
+    rng = np.random.default_rng(10)
+    ys = [0, 1, 2, 3, 5, 6, N - 7, N - 4, N - 2, N - 1] + [int(v) for v in rng.integers(2 * p + 2, N - 2 * p - 2, 3)]
+    zs = [0, 1, 3, 6, N - 5, N - 1] + [int(v) for v in rng.integers(2 * p + 2, N - 2 * p - 2, 2)]
+    lines = [(int(ys[k % len(ys)]), int(zs[k % len(zs)])) for k in range(max(len(ys), len(zs)) * 2)]
+    lines = sorted(set(lines))[:24]
+    rows = np.concatenate([(z * N + y) * N + np.arange(N) for y, z in lines])
+    host_grid = inputs.lognormal_grid(n, seed=desc["seed"], sigma=desc["sigma"])
+    try:
+        ref = oasm.assemble_rows(p, n, d, rows, desc, cfg["kinds"], grid=host_grid)
+        sc = oasm.assemble_rows(p, n, d, rows, desc, cfg["kinds"], grid=host_grid, absolute=True)
+        idx = torch.from_numpy(rows).cuda()
+        for k in cfg["kinds"]:
+            check_rows(out[k].index_select(0, idx).cpu().numpy(), ref[k], sc[k], ("C5 lines", k))
+    finally:
+        out.clear()
+        torch.cuda.empty_cache()
