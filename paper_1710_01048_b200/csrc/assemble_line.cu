@@ -743,12 +743,17 @@ struct ApplyGeom {
     }
 };
 
+#ifndef WGQ_APPLY_THREADS
+#define WGQ_APPLY_THREADS 320
+#endif
+constexpr int kApplyThreads = WGQ_APPLY_THREADS;
+
 template <int P, int MODE, int TRA>
-__global__ void __launch_bounds__(256, TRA == 8 ? 3 : 2) k_line_apply(const __grid_constant__ LineArgs a) {
+__global__ void __launch_bounds__(kApplyThreads, TRA == 8 ? 3 : 2) k_line_apply(const __grid_constant__ LineArgs a) {
     using C = Cfg<P>;
     using G = ApplyGeom<P, TRA>;
     constexpr int S = C::S, S2 = C::S2, V = C::V, RING = G::RING, URING = G::URING, PFD = G::PFD;
-    constexpr int NT = 256;
+    constexpr int NT = kApplyThreads, NW = NT / 32;
     constexpr int HS = G::HS, DC = G::DC;
     extern __shared__ __align__(128) double sm[];
     double* Hm = sm;                                      // [RING][HS]
@@ -842,7 +847,7 @@ __global__ void __launch_bounds__(256, TRA == 8 ? 3 : 2) k_line_apply(const __gr
         // ---- S1a: D_X = H_X (planes b0..) x U (columns Xlo..) on the tensor cores ----------
         // items: (matrix, band block); block b enumerates (mt, nt) with |nt - mt| <= 1
 #pragma unroll
-        for (int it = warp; it < 2 * G::NB; it += 8) {
+        for (int it = warp; it < 2 * G::NB; it += NW) {
             const int kind = it / G::NB;
             int b = it % G::NB, mt = 0, nt = 0;
             for (int q = 0, cnt = 0; q < G::DB * G::XBK; ++q) {
@@ -934,10 +939,10 @@ int launch_apply_p(const LineArgs& a, cudaStream_t st) {
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kApplyThreads, smem);
     const int64_t lines = (a.row_end - 1) / a.N - a.row_begin / a.N + 1;
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(lines, (int64_t)sms * std::max(per_sm, 1)));
-    kern<<<(unsigned)blocks, 256, smem, st>>>(a);
+    kern<<<(unsigned)blocks, kApplyThreads, smem, st>>>(a);
     return cudaGetLastError() == cudaSuccess ? WGQ_OK : WGQ_ECUDA;
 }
 
