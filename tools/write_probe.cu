@@ -69,6 +69,28 @@ __global__ void k_bulk(char* __restrict__ out, size_t chunks, int chunk, int dep
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// the same, but CTA b writes its own contiguous range of chunks (b*per .. (b+1)*per-1), like the
+// line kernel whose CTAs own whole lines, instead of a grid-stride front sweeping the buffer
+__global__ void k_bulk_blocked(char* __restrict__ out, size_t chunks, int chunk) {
+    extern __shared__ __align__(128) double sm[];
+    for (int i = threadIdx.x; i < chunk / 8; i += blockDim.x) sm[i] = 1.0;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    const uint64_t pol = pol_first();
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(sm);
+    const size_t per = (chunks + gridDim.x - 1) / gridDim.x;
+    const size_t c0 = blockIdx.x * per, c1 = c0 + per < chunks ? c0 + per : chunks;
+    for (size_t c = c0; c < c1; ++c) {
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(out + c * chunk),
+                     "r"(s), "r"(chunk), "l"(pol)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 int main() {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -123,6 +145,26 @@ int main() {
                 const double g1 = timeit([&] { k_bulk<true><<<sms * per, 64, chunk>>>((char*)buf, nch, chunk, depth); });
                 printf("bulk chunk_kb %2d ctas/SM %d depth %d  GB/s %.1f  (evict_first %.1f)\n", ck, per, depth, g0, g1);
             }
+    // the line kernel's pattern: per tile one chunk into each of two regions (M, K), 2 or 3 CTAs/SM,
+    // and large single chunks at 1 CTA/SM
+    for (int ck : {22, 33, 44, 66, 96, 128, 192})
+        for (int per : {1, 2, 3})
+            for (int depth : {1, 2}) {
+                const int chunk = ck * 1024;
+                if ((size_t)per * chunk > 200 * 1024 || (per == 1 && ck < 66)) continue;
+                const size_t nch = bytes / chunk;
+                const double g1 = timeit([&] { k_bulk<true><<<sms * per, 64, chunk>>>((char*)buf, nch, chunk, depth); });
+                printf("bulk-ef chunk_kb %3d ctas/SM %d depth %d  GB/s %.1f\n", ck, per, depth, g1);
+            }
+    cudaFuncSetAttribute(k_bulk_blocked, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    for (int ck : {22, 33, 44, 66})
+        for (int per : {2, 3}) {
+            const int chunk = ck * 1024;
+            if ((size_t)per * chunk > 200 * 1024) continue;
+            const size_t nch = bytes / chunk;
+            const double g = timeit([&] { k_bulk_blocked<<<sms * per, 64, chunk>>>((char*)buf, nch, chunk); });
+            printf("bulk-blocked chunk_kb %3d ctas/SM %d  GB/s %.1f\n", ck, per, g);
+        }
     cudaError_t e = cudaGetLastError();
     printf("status %s\n", cudaGetErrorString(e));
     return 0;
