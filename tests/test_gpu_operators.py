@@ -157,3 +157,31 @@ def test_apply_full_size_sampled_rows(name):
             ref.append(A[kind][i][ok] @ u[cols[ok]])
             scale.append(absA[kind][i][ok] @ np.abs(u[cols[ok]]))
         check(y[kind].cpu().numpy()[rows], np.array(ref), np.array(scale), (name, kind))
+
+
+def test_load_and_apply_ragged_ranges_bitwise():
+    """Row ranges that start / end inside a z-plane and straddle the load kernel's 32-plane
+    chunks and 16-row tiles (N = 39) give exactly the full-range rows (per-row arithmetic does
+    not depend on the launch), for the load vector and the matrix-free product."""
+    from paper_1710_01048_b200 import api, wgq
+    p, n, d = 3, 36, 3
+    rules = wgq.Rules(p, n, d)
+    N = rules.N
+    grid = torch.from_numpy(np.ascontiguousarray(inputs.lognormal_grid(n, seed=21, dim=d))).cuda()
+    c = api.coefficient({"kind": "grid"}, grid, 0)
+    u = torch.randn(rules.n_rows, dtype=torch.float64, device="cuda")
+    b_full = api.assemble_load(rules, c)
+    y_full = api.apply(rules, c, u)
+    cuts = [0, 5 * N * N + 17, 31 * N * N + 3 * N + 1, 33 * N * N, rules.n_rows]
+    for lo, hi in zip(cuts[:-1], cuts[1:]):
+        b = api.assemble_load(rules, c, lo, hi)
+        y = api.apply(rules, c, u, ("mass", "stiffness"), lo, hi)
+        torch.cuda.synchronize()
+        assert torch.equal(b, b_full[lo:hi]), (lo, hi)
+        for k in ("mass", "stiffness"):
+            assert torch.equal(y[k], y_full[k][lo:hi]), (lo, hi, k)
+    rows = np.array([0, 5 * N * N + 17, 31 * N * N + 3 * N, 33 * N * N - 1, rules.n_rows - 1])
+    ref = oops.load_rows(p, n, d, rows, {"kind": "grid", "seed": 21, "sigma": 0.5},
+                         grid=inputs.lognormal_grid(n, seed=21, dim=d))
+    got = b_full.cpu().numpy()[rows]
+    check(got, ref, np.abs(ref), "load ragged sample")
