@@ -189,7 +189,8 @@ int wgq_apply(wgq_rules_t rules, const wgq_coeff_t* c, const double* u, int64_t 
  * [c->grid_plane0, +grid_planes), which must cover the rows as for the device call),
  * assembles rows [row_begin, row_end) in chunks of `chunk_rows` (0 = automatic) on the
  * current device and streams each finished chunk into the HOST ELL arrays M_host / K_host
- * (row stride ld >= s^d; either may be NULL to skip that matrix) while the next chunk is
+ * (row stride ld >= s^d, slots [s^d, ld) of each host row are not written; either array may
+ * be NULL to skip that matrix) while the next chunk is
  * computed (two CUDA streams, double-buffered device staging that the call allocates and
  * frees).  Use page-locked host memory (wgq_host_alloc) for full PCIe bandwidth.  Returns
  * after all copies have completed. */

@@ -1,7 +1,8 @@
 // End-to-end assembly from/to host memory (wgq_assemble_host): the coefficient slab is
 // uploaded once, rows are assembled in chunks into double-buffered device staging on a
 // compute stream, and each finished chunk is copied to the caller's host arrays on a copy
-// stream while the next chunk is computed.  One cudaMemcpyAsync per copy.
+// stream while the next chunk is computed.  One cudaMemcpyAsync per copy (cudaMemcpy2DAsync
+// into a padded host row stride: only the s^d structural slots of each host row are written).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -66,9 +67,11 @@ extern "C" int wgq_assemble_host(wgq_rules_t R, const wgq_coeff_t* c, int64_t ro
         dc.grid = (const double*)cl.dev[0];
     }
     const int64_t rows = row_end - row_begin;
-    if (chunk_rows <= 0) chunk_rows = std::max<int64_t>(1, ((int64_t)1 << 27) / ld);   // ~1 GiB per matrix
+    // device staging holds compact rows (stride s^d); a padded host stride is written with 2D
+    // copies, so the host slots [s^d, ld) are never written (as for the device ELL output)
+    if (chunk_rows <= 0) chunk_rows = std::max<int64_t>(1, ((int64_t)1 << 27) / stencil);   // ~1 GiB per matrix
     chunk_rows = std::min(chunk_rows, rows);
-    const size_t chunk_bytes = (size_t)chunk_rows * ld * sizeof(double);
+    const size_t chunk_bytes = (size_t)chunk_rows * stencil * sizeof(double);
     const bool doM = M_host != nullptr, doK = K_host != nullptr;
     for (int b = 0; b < 2; ++b) {
         if (doM && cudaMalloc(&cl.dev[1 + b], chunk_bytes) != cudaSuccess) return WGQ_ECUDA;
@@ -81,21 +84,27 @@ extern "C" int wgq_assemble_host(wgq_rules_t R, const wgq_coeff_t* c, int64_t ro
         const int64_t hi = std::min(row_end, lo + chunk_rows);
         const int b = (int)(it & 1);
         if (it >= 2) cudaStreamWaitEvent(comp, copied[b], 0);     // staging buffer b is free again
-        wgq_out_t M{WGQ_ELL, lo, hi, (double*)cl.dev[1 + b], ld, nullptr, nullptr};
-        wgq_out_t K{WGQ_ELL, lo, hi, (double*)cl.dev[3 + b], ld, nullptr, nullptr};
+        wgq_out_t M{WGQ_ELL, lo, hi, (double*)cl.dev[1 + b], stencil, nullptr, nullptr};
+        wgq_out_t K{WGQ_ELL, lo, hi, (double*)cl.dev[3 + b], stencil, nullptr, nullptr};
         if (doM && doK) rc = wgq_assemble_mass_stiffness(R, &dc, &M, &K, comp);
         else if (doM) rc = wgq_assemble_mass(R, &dc, &M, comp);
         else rc = wgq_assemble_stiffness(R, &dc, &K, comp);
         if (rc != WGQ_OK) break;
         cudaEventRecord(computed[b], comp);
         cudaStreamWaitEvent(copy, computed[b], 0);
-        const size_t bytes = (size_t)(hi - lo) * ld * sizeof(double);
         const size_t off = (size_t)(lo - row_begin) * ld;
-        if (doM && cudaMemcpyAsync(M_host + off, cl.dev[1 + b], bytes, cudaMemcpyDeviceToHost, copy) != cudaSuccess) {
+        auto d2h = [&](double* dst, const void* src) {
+            if (ld == stencil)
+                return cudaMemcpyAsync(dst, src, (size_t)(hi - lo) * stencil * sizeof(double), cudaMemcpyDeviceToHost,
+                                       copy);
+            return cudaMemcpy2DAsync(dst, (size_t)ld * sizeof(double), src, (size_t)stencil * sizeof(double),
+                                     (size_t)stencil * sizeof(double), (size_t)(hi - lo), cudaMemcpyDeviceToHost, copy);
+        };
+        if (doM && d2h(M_host + off, cl.dev[1 + b]) != cudaSuccess) {
             rc = WGQ_ECUDA;
             break;
         }
-        if (doK && cudaMemcpyAsync(K_host + off, cl.dev[3 + b], bytes, cudaMemcpyDeviceToHost, copy) != cudaSuccess) {
+        if (doK && d2h(K_host + off, cl.dev[3 + b]) != cudaSuccess) {
             rc = WGQ_ECUDA;
             break;
         }
