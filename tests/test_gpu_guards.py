@@ -32,10 +32,12 @@ def cases():
     for p in (2, 3):
         out += [(p, 7, 3, {"kind": "grid"}), (p, 4, 3, {"kind": "grid"}), (p, 9, 2, four(2)), (p, 6, 3, trig(3)),
                 (p, 8, 2, trig(2)), (p, 5, 3, four(3)), (p, 11, 1, {"kind": "const", "c0": 1.0})]
+    # lines of several tiles (assembly: 12 rows, apply: 24, load: 16 x 16 tiles, 32-plane chunks)
+    out += [(3, 30, 3, {"kind": "grid"}), (2, 35, 3, {"kind": "grid"})]
     return out
 
 
-@pytest.mark.parametrize("case", range(14))
+@pytest.mark.parametrize("case", range(16))
 def test_no_out_of_bounds_writes(case):
     from paper_1710_01048_b200 import api, wgq
     p, n, d, desc = cases()[case]
