@@ -1085,6 +1085,8 @@ int launch_apply(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c,
     }();
     if (!force_generic && line_apply_applies(R, c))
         return launch_line_apply(R, T, c, u, u_row0, row_begin, row_end, yM, yK, stream);
+    if (!force_generic && sep_applies(c))
+        return launch_sep_apply(R, T, c, u, u_row0, row_begin, row_end, yM, yK, stream);
     cudaStream_t st = (cudaStream_t)stream;
     GenericArgs a = base_args(R, T, c, row_begin, row_end);
     a.apply = 1;

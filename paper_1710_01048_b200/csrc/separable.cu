@@ -305,14 +305,11 @@ int launch_sep_pd(const SepArgs& a, int mode, cudaStream_t st) {
 
 bool sep_applies(const wgq_coeff_t* c) { return c->kind == WGQ_COEF_CONST || c->kind == WGQ_COEF_TRIG_SEP; }
 
-int launch_sep(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, const wgq_out_t* M,
-               const wgq_out_t* K, void* stream) {
-    const wgq_out_t* any = M ? M : K;
-    if (any->row_end <= any->row_begin) return WGQ_OK;
-    cudaStream_t st = (cudaStream_t)stream;
+// The 4 x s per-direction vectors of every 1D row (uM, vM, uK, vK); they depend on the rules and
+// the factors f_a only (c0, amp enter the value formulas): built once per (device, kind, trig,
+// wavenum) and cached in the rules handle.
+int sep_vectors_for(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, cudaStream_t st, double** out) {
     const int S = 2 * R->p + 1;
-    // the 4 x s vectors depend on the rules and the factors f_a only (c0, amp enter the value
-    // formulas): built once per (device, kind, trig, wavenum) and cached in the rules handle
     double* sep = nullptr;
     {
         int dev = 0;
@@ -336,6 +333,20 @@ int launch_sep(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, c
         } else {
             sep = it->second;
         }
+    }
+    *out = sep;
+    return WGQ_OK;
+}
+
+int launch_sep(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, const wgq_out_t* M,
+               const wgq_out_t* K, void* stream) {
+    const wgq_out_t* any = M ? M : K;
+    if (any->row_end <= any->row_begin) return WGQ_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    double* sep = nullptr;
+    {
+        const int rc = sep_vectors_for(R, T, c, st, &sep);
+        if (rc != WGQ_OK) return rc;
     }
     SepArgs a{};
     a.sep = sep;
@@ -366,6 +377,103 @@ int launch_sep(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, c
         case 33: rc = launch_sep_pd<3, 3>(a, mode, st); break;
     }
     return rc;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Matrix-free y = M u, K u for the separable coefficients: with the row's
+// per-direction vectors (uM, vM, uK, vK)_a, A_ij = c0 prod_a uM_a[o_a] + amp prod_a vM_a[o_a]
+// (mass; stiffness as in sep_stiff), so y_i = sum_j A_ij u_j is contracted x -> y -> z per row:
+// the same sum as the definition, reordered.  One thread per row; the x-direction vectors of the
+// row live in registers, neighbouring threads read overlapping u windows (coalesced).
+namespace {
+template <int P, int D>
+__global__ void __launch_bounds__(256) k_sep_apply(const double* sep, int64_t N, int64_t row_begin, int64_t row_end,
+                                                   double c0, double amp, const double* u, int64_t u_row0, double* yM,
+                                                   double* yK) {
+    constexpr int S = 2 * P + 1;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t row = row_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < row_end; row += stride) {
+        const int64_t i1 = row % N, i2 = D >= 2 ? (row / N) % N : 0, i3 = D >= 3 ? row / (N * N) : 0;
+        const int lo1 = (int)max((int64_t)0, P - i1), hi1 = (int)min((int64_t)(2 * P), N - 1 - i1 + P);
+        const int lo2 = D >= 2 ? (int)max((int64_t)0, P - i2) : 0, hi2 = D >= 2 ? (int)min((int64_t)(2 * P), N - 1 - i2 + P) : 0;
+        const int lo3 = D >= 3 ? (int)max((int64_t)0, P - i3) : 0, hi3 = D >= 3 ? (int)min((int64_t)(2 * P), N - 1 - i3 + P) : 0;
+        const double* t1 = sep + i1 * 4 * kMaxS;
+        const double* t2 = sep + (N + i2) * 4 * kMaxS;
+        const double* t3 = sep + (2 * N + i3) * 4 * kMaxS;
+        double w1[4][S];
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int o = 0; o < S; ++o) w1[c][o] = __ldg(t1 + c * kMaxS + o);
+        double Mu = 0.0, Mv = 0.0, Ku = 0.0, Kv = 0.0;
+        for (int o3 = lo3; o3 <= hi3; ++o3) {
+            double Auu = 0.0, Avv = 0.0, Xu = 0.0, Xv = 0.0;    // Auu = sum uM2 (uM1 . u); X = K_x + K_y parts
+            for (int o2 = lo2; o2 <= hi2; ++o2) {
+                const int64_t base = D == 3 ? ((i3 - P + o3) * N + (i2 - P + o2)) * N : (D == 2 ? (i2 - P + o2) * N : 0);
+                const double* ur = u + base + (i1 - P) - u_row0;
+                double suM = 0.0, svM = 0.0, suK = 0.0, svK = 0.0;
+#pragma unroll
+                for (int o1 = 0; o1 < S; ++o1) {
+                    if (o1 < lo1 || o1 > hi1) continue;
+                    const double uv = __ldg(ur + o1);
+                    suM = fma(w1[0][o1], uv, suM);
+                    svM = fma(w1[1][o1], uv, svM);
+                    suK = fma(w1[2][o1], uv, suK);
+                    svK = fma(w1[3][o1], uv, svK);
+                }
+                if (D == 1) {
+                    Mu = suM, Mv = svM, Ku = suK, Kv = svK;
+                    continue;
+                }
+                const double uM2 = __ldg(t2 + o2), vM2 = __ldg(t2 + kMaxS + o2);
+                const double uK2 = __ldg(t2 + 2 * kMaxS + o2), vK2 = __ldg(t2 + 3 * kMaxS + o2);
+                Auu = fma(uM2, suM, Auu);
+                Avv = fma(vM2, svM, Avv);
+                Xu = fma(uM2, suK, fma(uK2, suM, Xu));             // uK1 uM2 + uM1 uK2
+                Xv = fma(vM2, svK, fma(vK2, svM, Xv));
+            }
+            if (D == 1) break;
+            if (D == 2) {
+                Mu = Auu, Mv = Avv, Ku = Xu, Kv = Xv;
+                break;
+            }
+            const double uM3 = __ldg(t3 + o3), vM3 = __ldg(t3 + kMaxS + o3);
+            const double uK3 = __ldg(t3 + 2 * kMaxS + o3), vK3 = __ldg(t3 + 3 * kMaxS + o3);
+            Mu = fma(uM3, Auu, Mu);
+            Mv = fma(vM3, Avv, Mv);
+            Ku = fma(uM3, Xu, fma(uK3, Auu, Ku));                  // (K_x + K_y) uM3 + uM1 uM2 uK3
+            Kv = fma(vM3, Xv, fma(vK3, Avv, Kv));
+        }
+        const int64_t o = row - row_begin;
+        if (yM) yM[o] = fma(amp, Mv, c0 * Mu);
+        if (yK) yK[o] = fma(amp, Kv, c0 * Ku);
+    }
+}
+}  // namespace
+
+int launch_sep_apply(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, const double* u, int64_t u_row0,
+                     int64_t row_begin, int64_t row_end, double* yM, double* yK, void* stream) {
+    if (row_end <= row_begin) return WGQ_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    double* sep = nullptr;
+    int rc = sep_vectors_for(R, T, c, st, &sep);
+    if (rc != WGQ_OK) return rc;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t rows = row_end - row_begin;
+    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((rows + 255) / 256, (int64_t)sms * 16));
+    const double amp = c->kind == WGQ_COEF_TRIG_SEP ? c->amp : 0.0;
+    switch (R->p * 10 + R->dim) {
+        case 21: k_sep_apply<2, 1><<<blocks, 256, 0, st>>>(sep, R->N, row_begin, row_end, c->c0, amp, u, u_row0, yM, yK); break;
+        case 22: k_sep_apply<2, 2><<<blocks, 256, 0, st>>>(sep, R->N, row_begin, row_end, c->c0, amp, u, u_row0, yM, yK); break;
+        case 23: k_sep_apply<2, 3><<<blocks, 256, 0, st>>>(sep, R->N, row_begin, row_end, c->c0, amp, u, u_row0, yM, yK); break;
+        case 31: k_sep_apply<3, 1><<<blocks, 256, 0, st>>>(sep, R->N, row_begin, row_end, c->c0, amp, u, u_row0, yM, yK); break;
+        case 32: k_sep_apply<3, 2><<<blocks, 256, 0, st>>>(sep, R->N, row_begin, row_end, c->c0, amp, u, u_row0, yM, yK); break;
+        case 33: k_sep_apply<3, 3><<<blocks, 256, 0, st>>>(sep, R->N, row_begin, row_end, c->c0, amp, u, u_row0, yM, yK); break;
+        default: return WGQ_EUNSUPPORTED;
+    }
+    return cudaGetLastError() == cudaSuccess ? WGQ_OK : WGQ_ECUDA;
 }
 
 }  // namespace wgq
