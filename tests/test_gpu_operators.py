@@ -124,9 +124,10 @@ def test_load_full_size_c5_sampled_rows():
     assert len(zs) > 3
 
 
-@pytest.mark.parametrize("name", ["C5", "C3"])
+@pytest.mark.parametrize("name", ["C5", "C3", "C4", "C2"])
 def test_apply_full_size_sampled_rows(name):
-    """y = M u, K u at the BASELINE sizes (C5: GRID line kernel, C3: 2D tensor-core kernel) on a
+    """y = M u, K u at the BASELINE sizes (C5: GRID line kernel, C3: 2D tensor-core kernel, C4 / C2:
+    separable kernel) on a
     sample of rows covering every boundary class; u is a seeded random vector."""
     from paper_1710_01048_b200 import api, wgq
     cfg = inputs.config(name)
