@@ -88,6 +88,9 @@ struct GenericArgs {
     int64_t u_row0;
     double* yM;
     double* yK;
+    // load-vector mode (wgq_assemble_load through k_fourier2d): b[i] = sum of the row's weighted mass samples
+    int load;
+    double* b;
     int64_t n, N;
     int64_t row_begin, row_end;
     OutDev M, K;
@@ -429,6 +432,14 @@ __global__ void __launch_bounds__(256) k_fourier2d(const GenericArgs a) {
                 if (4 * s >= J) break;
                 dmma(e0, e1, cx.xa[s], yb[s]);
             }
+            if (a.load) {
+                // load vector (eq:Load): the row's mass x mass samples, summed over the warp
+                double v = (!gs && xv && t < nym) ? exp_fast(e0) * cx.wx * wym : 0.0;
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+                if (lane == 0) a.b[orow0 + i1] = v;
+                continue;
+            }
             // ---- weighted samples (lane (g, t): x-node g, y-nodes mass t / stiffness t) ----
             const double s0 = (xv && t < nym) ? exp_fast(e0) * cx.wx * wym : 0.0;
             const double s1 = (!gs && xv && t < nyk) ? exp_fast(e1) * cx.wx * wyk : 0.0;
@@ -592,9 +603,9 @@ __global__ void k_vertex_weights(RowTables T, int p, double* PW) {
 template <int P, int D>
 __global__ void __launch_bounds__(256) k_load(const GenericArgs a, const double* PW, double* b) {
     constexpr int V = P + 2;
-    const int64_t rows = a.row_end - a.row_begin;
+    const int64_t rows = a.rows_list ? a.nlist : a.row_end - a.row_begin;   // rows_list: a shell pass
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < rows; t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t row = a.row_begin + t;
+        const int64_t row = a.rows_list ? a.rows_list[t] : a.row_begin + t;
         int64_t idx[3] = {0, 0, 0};
         int64_t rem = row;
 #pragma unroll
@@ -655,7 +666,7 @@ __global__ void __launch_bounds__(256) k_load(const GenericArgs a, const double*
                 }
             }
         }
-        b[t] = acc;
+        b[row - a.row_begin] = acc;
     }
 }
 
@@ -1061,6 +1072,29 @@ int launch_load(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, 
     if (c->kind == WGQ_COEF_GRID) {
         if (cudaMallocAsync((void**)&PW, (size_t)R->N * kMaxV * sizeof(double), st) != cudaSuccess) return WGQ_ENOMEM;
         k_vertex_weights<<<(unsigned)((R->N * kMaxV + 255) / 256), 256, 0, st>>>(T, R->p, PW);
+    }
+    static const bool force_generic = [] {
+        const char* e = getenv("WGQ_FORCE_GENERIC");
+        return e && e[0] == '1';
+    }();
+    if (!force_generic && R->dim == 2 && c->kind == WGQ_COEF_FOURIER_LOGN && a.coef.n_modes > 0) {
+        // the 2D tensor-core kernel in load mode (its exponent product and exp, no y / x stages),
+        // then the generic per-row kernel over the shell rows (GL-fallback boundary classes)
+        GenericArgs f = a;
+        f.load = 1;
+        f.b = b;
+        f.do_mass = 1;
+        f.do_stiff = 0;
+        rc = R->p == 3 ? launch_fourier2d_p<3>(f, st) : launch_fourier2d_p<2>(f, st);
+        const int64_t* shell = nullptr;
+        int64_t nshell = 0;
+        if (rc == WGQ_OK) rc = shell_rows_2d(const_cast<wgq_rules_s*>(R), row_begin, row_end, &shell, &nshell);
+        if (rc != WGQ_OK || nshell == 0) {
+            if (tab) cudaFreeAsync(tab, st);
+            return rc;
+        }
+        a.rows_list = shell;
+        a.nlist = nshell;
     }
     rc = WGQ_EUNSUPPORTED;
     switch (R->p * 10 + R->dim) {

@@ -186,3 +186,22 @@ def test_load_and_apply_ragged_ranges_bitwise():
                          grid=inputs.lognormal_grid(n, seed=21, dim=d))
     got = b_full.cpu().numpy()[rows]
     check(got, ref, np.abs(ref), "load ragged sample")
+
+
+def test_load_full_size_c3_sampled_rows():
+    """C3's mesh and Fourier-lognormal coefficient (the 2D tensor-core kernel in load mode plus the
+    generic shell pass): every boundary row class plus random rows against the oracle."""
+    from paper_1710_01048_b200 import api, wgq
+    cfg = inputs.config("C3")
+    p, n, d = cfg["p"], cfg["n"], cfg["dim"]
+    rules = wgq.Rules(p, n, d)
+    desc = inputs.coefficient(cfg["coeff"], d)
+    b = api.assemble_load(rules, api.coefficient(desc))
+    torch.cuda.synchronize()
+    N = rules.N
+    rng = np.random.default_rng(6)
+    edge = list(range(0, 2 * p + 2)) + list(range(N - 2 * p - 2, N))
+    rows = np.array(sorted({sum(int(rng.choice(edge) if rng.random() < 0.5 else rng.integers(0, N)) * N ** a
+                                for a in range(d)) for _ in range(400)}))
+    ref = oops.load_rows(p, n, d, rows, desc)
+    check(b.cpu().numpy()[rows], ref, np.abs(ref), "C3 load")
