@@ -1063,6 +1063,10 @@ int launch_assemble(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t*
 int launch_load(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, int64_t row_begin, int64_t row_end,
                 double* b, void* stream) {
     if (row_end <= row_begin) return WGQ_OK;
+    {
+        const char* e = getenv("WGQ_FORCE_GENERIC");
+        if (!(e && e[0] == '1') && sep_applies(c)) return launch_sep_load(R, T, c, row_begin, row_end, b, stream);
+    }
     cudaStream_t st = (cudaStream_t)stream;
     GenericArgs a = base_args(R, T, c, row_begin, row_end);
     double* tab = nullptr;

@@ -106,6 +106,8 @@ bool line_kernel_applies(const wgq_rules_s* R, const wgq_coeff_t* c, const wgq_o
 int launch_line(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, const wgq_out_t* M,
                 const wgq_out_t* K, void* stream);
 bool line_apply_applies(const wgq_rules_s* R, const wgq_coeff_t* c);
+int launch_sep_load(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, int64_t row_begin, int64_t row_end,
+                    double* b, void* stream);
 int launch_sep_apply(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, const double* u, int64_t u_row0,
                      int64_t row_begin, int64_t row_end, double* yM, double* yK, void* stream);
 int launch_line_apply(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, const double* u,

@@ -476,4 +476,51 @@ int launch_sep_apply(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t
     return cudaGetLastError() == cudaSuccess ? WGQ_OK : WGQ_ECUDA;
 }
 
+// Load vector for the separable coefficients: b_i = sum_k prod_a wM_a f(x_k)
+// with f = c0 + amp prod_a f_a, and sum_o uM_a[o] = sum_k wM_k (partition of unity over the
+// functions nonzero at each node; likewise vM with f_a), so b_i = c0 prod_a U_a + amp prod_a V_a.
+namespace {
+template <int D>
+__global__ void __launch_bounds__(256) k_sep_load(const double* sep, int64_t N, int S, int64_t row_begin,
+                                                  int64_t row_end, double c0, double amp, double* b) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t row = row_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < row_end; row += stride) {
+        int64_t idx[3] = {row % N, D >= 2 ? (row / N) % N : 0, D >= 3 ? row / (N * N) : 0};
+        double pu = 1.0, pv = 1.0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            const double* t = sep + ((int64_t)a * N + idx[a]) * 4 * kMaxS;
+            double su = 0.0, sv = 0.0;
+            for (int o = 0; o < S; ++o) {
+                su += __ldg(t + o);
+                sv += __ldg(t + kMaxS + o);
+            }
+            pu *= su;
+            pv *= sv;
+        }
+        b[row - row_begin] = fma(amp, pv, c0 * pu);
+    }
+}
+}  // namespace
+
+int launch_sep_load(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, int64_t row_begin, int64_t row_end,
+                    double* b, void* stream) {
+    if (row_end <= row_begin) return WGQ_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    double* sep = nullptr;
+    int rc = sep_vectors_for(R, T, c, st, &sep);
+    if (rc != WGQ_OK) return rc;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t rows = row_end - row_begin;
+    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((rows + 255) / 256, (int64_t)sms * 16));
+    const double amp = c->kind == WGQ_COEF_TRIG_SEP ? c->amp : 0.0;
+    const int S = 2 * R->p + 1;
+    if (R->dim == 1) k_sep_load<1><<<blocks, 256, 0, st>>>(sep, R->N, S, row_begin, row_end, c->c0, amp, b);
+    else if (R->dim == 2) k_sep_load<2><<<blocks, 256, 0, st>>>(sep, R->N, S, row_begin, row_end, c->c0, amp, b);
+    else k_sep_load<3><<<blocks, 256, 0, st>>>(sep, R->N, S, row_begin, row_end, c->c0, amp, b);
+    return cudaGetLastError() == cudaSuccess ? WGQ_OK : WGQ_ECUDA;
+}
+
 }  // namespace wgq
