@@ -720,7 +720,7 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 2) k_line_grid3(const __grid_const
 // Tile geometry of the apply for TRA rows per tile: the vertex-plane window (TRA + p + 1 planes,
 // H ring RING_A >= that), the D product's plane x column blocks of 8 (only blocks within the band
 // |column - plane| <= 1 block carry nonzero P^ weights), the u ring (the next tile's window of
-// TRA + 2p columns plus PFD - 1 further tiles of up to TRA + p new columns).
+// TRA + 2p columns plus PFD - 1 further tiles of up to TRA + 2p new columns).
 template <int P, int TRA>
 struct ApplyGeom {
     static constexpr int V = P + 2, S = 2 * P + 1, S2 = S * S;
@@ -731,9 +731,11 @@ struct ApplyGeom {
     static constexpr int DB = (W + 7) / 8;                             // plane blocks of D
     static constexpr int XBK = (TRA + 2 * P + 7) / 8;                  // column blocks of D
     static constexpr int DR = DB * 8, DC = XBK * 8;                    // D extents
-    static constexpr int UXMAX = (TRA + P + 7) / 8 * 8;                // new columns per tile (bound)
+    static constexpr int UXMAX = (TRA + 2 * P + 7) / 8 * 8;            // new columns per tile (a slab's first
+                                                                       // tile may start mid-line: TRA + 2p)
     // live columns when tile k+PFD is issued: tile k+1's window and the new columns of k+2..k+PFD
-    static constexpr int URING = TRA == 8 ? ApplyCfg::URING : (TRA + 2 * P) + (PFD - 1) * (TRA + P) + 1;
+    // (at most TRA + 2p each: a tile that starts a slab inside a line)
+    static constexpr int URING = TRA == 8 ? ApplyCfg::URING : PFD * (TRA + 2 * P) + 1;
     static constexpr int HS = (S2 + 3) / 4 * 4 + ((S2 + 3) / 4 % 2 == 0 ? 4 : 0);   // row stride = 4 (mod 8)
     // band blocks (mt, nt) with |nt - mt| <= 1, in order
     static constexpr int NB = DB * XBK - ((DB > 2 ? (DB - 2) * (DB - 1) / 2 : 0) + (XBK > 2 ? (XBK - 2) * (XBK - 1) / 2 : 0));
@@ -878,7 +880,7 @@ __global__ void __launch_bounds__(kApplyThreads, TRA == 8 ? 3 : 2) k_line_apply(
         }
         __syncthreads();
         // ---- S1b: rows of tile k, phase A of tile k+1, prefetch tile k+PFD ------------------
-        if (warp < TRA / 8 && !(a.dbg & 32)) {
+        if (warp < (TRA + 7) / 8 && !(a.dbg & 32)) {
             // warp w finishes rows 8w..8w+7 of the tile: lane (j, vq) = row t0 + 8w + j, vertex
             // planes vx = vq (+4); y = sum_{vx,o1} P[vx][o1] D(b_r + vx, r - p + o1), over 4 lanes
             const int j = 8 * warp + (lane >> 2), vq = lane & 3;

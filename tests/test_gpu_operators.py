@@ -173,7 +173,8 @@ def test_load_and_apply_ragged_ranges_bitwise():
     u = torch.randn(rules.n_rows, dtype=torch.float64, device="cuda")
     b_full = api.assemble_load(rules, c)
     y_full = api.apply(rules, c, u)
-    cuts = [0, 5 * N * N + 17, 31 * N * N + 3 * N + 1, 33 * N * N, rules.n_rows]
+    cuts = [0, 5 * N * N + 17, 7 * N * N + 4 * N + 30, 12 * N * N + 25, 31 * N * N + 3 * N + 1, 33 * N * N,
+            33 * N * N + N + 38, rules.n_rows]
     for lo, hi in zip(cuts[:-1], cuts[1:]):
         b = api.assemble_load(rules, c, lo, hi)
         y = api.apply(rules, c, u, ("mass", "stiffness"), lo, hi)
