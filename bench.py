@@ -406,6 +406,22 @@ def run_extras(rules5, coef5, peak):
         out["configs"][cfg["name"]] = {"ms": round(ms, 4), "nnz_per_s": nnz / (ms / 1e3),
                                        "hbm_gbs": round(alg / ms / 1e6, 1), "hbm_frac": round(alg / ms / 1e6 / peak, 4)}
         del o
+    # C5 in CSR layout (values of both matrices; the closed-form structure is built once, untimed)
+    nnz5 = wgq.wgq_nnz(rules5, 0, rules5.n_rows)
+    row_ptr = torch.empty(rules5.n_rows + 1, dtype=torch.int64, device="cuda")
+    col_idx = torch.empty(nnz5, dtype=torch.int32, device="cuda")
+    wgq.wgq_csr_structure(rules5, 0, rules5.n_rows, row_ptr, col_idx)
+    del col_idx
+    vals = {k: torch.empty(nnz5, dtype=torch.float64, device="cuda") for k in ("mass", "stiffness")}
+    dm = wgq.make_out(vals["mass"], 0, rules5.n_rows, ld=0, layout=wgq.WGQ_CSR, row_ptr=row_ptr)
+    dk = wgq.make_out(vals["stiffness"], 0, rules5.n_rows, ld=0, layout=wgq.WGQ_CSR, row_ptr=row_ptr)
+    ms = _time_ms(lambda: wgq.wgq_assemble_mass_stiffness(rules5, coef5, dm, dk), flush=flush)
+    csr_bytes = 2 * nnz5 * 8
+    out["configs"]["3d_p3_n256_mk_grid_csr"] = {"ms": round(ms, 4), "nnz_per_s": 2 * nnz5 / (ms / 1e3),
+                                                "hbm_gbs": round(csr_bytes / ms / 1e6, 1),
+                                                "hbm_frac": round(csr_bytes / ms / 1e6 / peak, 4)}
+    del vals, row_ptr, dm, dk
+    torch.cuda.empty_cache()
     n_rows = rules5.n_rows
     b = torch.empty(n_rows, dtype=torch.float64, device="cuda")
     ms = _time_ms(lambda: api.assemble_load(rules5, coef5, out=b), flush=flush)
