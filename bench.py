@@ -359,8 +359,9 @@ def main():
                 "warmup": args.warmup, "ms_per_step": total_ms_max / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": arm_config(cfg, world, ld),
-                # one assembly kernel per step; the 2D Fourier path adds the generic shell-row pass
-                "gpu_launches": args.steps * (2 if (d == 2 and cfg["coeff"]["kind"] == "fourier_logn") else 1),
+                # one assembly kernel per step; the 2D Fourier path adds its per-call factor tables
+                # and the generic shell-row pass
+                "gpu_launches": args.steps * (3 if (d == 2 and cfg["coeff"]["kind"] == "fourier_logn") else 1),
                 "roofline": roof, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu, "extras": extras,
                 "setup": setup}
         if functional:
