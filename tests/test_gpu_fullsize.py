@@ -15,8 +15,7 @@ from oracle import assemble as oasm
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-REL_F, REL_E = 1e-12, 1e-10
-FLOOR = 64 * np.finfo(np.float64).eps / REL_E
+from parity import compare  # noqa: E402
 
 
 def sample_rows(p, n, d, count, seed):
@@ -35,12 +34,7 @@ def sample_rows(p, n, d, count, seed):
 
 
 def check_rows(gpu_rows, ref, sc, what):
-    nrm = np.linalg.norm(ref)
-    relf = np.linalg.norm(gpu_rows - ref) / nrm
-    den = np.maximum(np.maximum(np.abs(ref), 1e-14 * np.abs(ref).max(axis=1, keepdims=True)), FLOOR * sc)
-    den = np.where(den > 0, den, 1.0)
-    rele = np.max(np.abs(gpu_rows - ref) / den)
-    assert relf <= REL_F and rele <= REL_E, (what, relf, rele)
+    compare(gpu_rows, ref, what, sc)
 
 
 def assemble_config(name):

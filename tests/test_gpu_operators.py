@@ -16,17 +16,11 @@ from oracle import operators as oops
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-REL_F, REL_E = 1e-12, 1e-10
-FLOOR = 64 * np.finfo(np.float64).eps / REL_E
+from parity import compare  # noqa: E402
 
 
 def check(g, ref, scale, what):
-    nrm = np.linalg.norm(ref)
-    relf = np.linalg.norm(g - ref) / (nrm if nrm > 0 else 1.0)
-    den = np.maximum(np.maximum(np.abs(ref), 1e-14 * np.max(np.abs(ref))), FLOOR * scale)
-    rele = np.max(np.abs(g - ref) / np.where(den > 0, den, 1.0))
-    assert relf <= REL_F, (what, relf)
-    assert rele <= REL_E, (what, rele)
+    compare(g, ref, what, scale, rowwise=False)
 
 
 def coeff_cases(d):

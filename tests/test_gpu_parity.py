@@ -15,29 +15,7 @@ from oracle import assemble as oasm
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-REL_F = 1e-12
-REL_E = 1e-10
-
-
-EPS = np.finfo(np.float64).eps
-FLOOR = 64 * EPS / REL_E
-
-
-def compare(gpu, ref, what="", scale=None):
-    gpu = np.asarray(gpu)
-    ref = np.asarray(ref)
-    assert gpu.shape == ref.shape, (what, gpu.shape, ref.shape)
-    nrm = np.linalg.norm(ref)
-    relf = np.linalg.norm(gpu - ref) / (nrm if nrm > 0 else 1.0)
-    rowmax = np.max(np.abs(ref), axis=1, keepdims=True)
-    den = np.maximum(np.abs(ref), 1e-14 * rowmax)
-    if scale is not None:
-        den = np.maximum(den, FLOOR * np.asarray(scale))
-    den = np.where(den > 0, den, 1.0)
-    rele = np.max(np.abs(gpu - ref) / den)
-    assert relf <= REL_F, (what, relf)
-    assert rele <= REL_E, (what, rele)
-    return relf, rele
+from parity import REL_E, REL_F, compare  # noqa: E402,F401
 
 
 def coeff_cases(d, n):

@@ -78,6 +78,11 @@ def test_load_linear_fields_are_exact(p, d, n):
     if d >= 2:
         fields.append((lambda *x: x[1], [I, IX] + [I] * (d - 2)))
         fields.append((lambda *x: x[0] * x[1], [IX, IX] + [I] * (d - 2)))
+    if d == 3:
+        fields.append((lambda *x: x[2], [I, I, IX]))
+        fields.append((lambda *x: x[0] * x[2], [IX, I, IX]))
+        fields.append((lambda *x: x[1] * x[2], [I, IX, IX]))
+        fields.append((lambda *x: x[0] * x[1] * x[2], [IX, IX, IX]))
     for f, factors in fields:
         grid = vertex_field(n, d, f)
         b = operators.load_rows(p, n, d, rows, {"kind": "grid"}, grid=grid)
@@ -125,3 +130,23 @@ def test_apply_full_coverage_identities(p, d, n):
         ga = np.array([g[assemble.decode(int(r), N, d)[a]] for r in range(N ** d)])
         y = operators.apply_rows(p, n, d, rows, desc, ga, "mass")
         assert np.max(np.abs(y - mx[:, a]) / np.abs(m1)) < 1e-13
+
+
+@pytest.mark.parametrize("p,n,z0,z1", [(2, 6, 3, 5), (3, 6, 4, 8), (3, 7, 0, 2), (2, 5, 5, 6)])
+def test_load_multilinear_fields_on_a_slab(p, n, z0, z1):
+    """The same exact integrals from a slab of vertex planes (plane0 != 0): rows of z-planes
+    [z0, z1] need vertex planes [max(0, z0 - p), min(n, z1 + 1)] only."""
+    d, N = 3, n + p
+    rows = np.arange(z0 * N * N, (z1 + 1) * N * N)
+    lo, hi = max(0, z0 - p), min(n, z1 + 1)
+    I, IX = int_B(p, n), int_xB(p, n)
+    for f, fac in ((lambda x, y, z: z, (I, I, IX)), (lambda x, y, z: x * y * z, (IX, IX, IX)),
+                   (lambda x, y, z: 1.0 + y * z, None)):
+        grid = vertex_field(n, d, f)[lo:hi + 1]
+        b = operators.load_rows(p, n, d, rows, {"kind": "grid"}, grid=grid, plane0=lo)
+        if fac is None:
+            ref = np.array([I[i] * I[j] * I[k] + I[i] * IX[j] * IX[k]
+                            for i, j, k in (assemble.decode(int(r), N, d) for r in rows)])
+        else:
+            ref = np.array([np.prod([fac[a][i] for a, i in enumerate(assemble.decode(int(r), N, d))]) for r in rows])
+        assert np.max(np.abs(b - ref)) < 1e-14 * np.max(np.abs(ref))
