@@ -12,7 +12,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libwgq.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["rules.cpp", "api.cpp", "host_pipeline.cpp", "tables.cu", "assemble.cu", "assemble_line.cu", "separable.cu", "grid.cu", "checks.cu"]
+SOURCES = ["rules.cpp", "api.cpp", "host_pipeline.cpp", "tables.cu", "assemble.cu", "assemble_line.cu", "fourier2d.cu", "separable.cu", "grid.cu", "checks.cu"]
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O3", "--expt-relaxed-constexpr"]
 

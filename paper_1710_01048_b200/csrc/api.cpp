@@ -32,6 +32,7 @@ int table_for(wgq_rules_s* R, RowTables* out, void* stream) {
         if (rc != WGQ_OK) return rc;
         // the cache is used from any stream afterwards: complete the one-time build now
         if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return WGQ_ECUDA;
+        if (fetch_interior_tables(R, &T) != WGQ_OK) return WGQ_ECUDA;
         // keep stream-ordered scratch (coefficient tables) in the device pool between calls
         cudaMemPool_t pool;
         if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {

@@ -93,6 +93,9 @@ struct GenericArgs {
     double* b;
     int64_t n, N;
     int64_t row_begin, row_end;
+    // k_fourier2d frame mode: skip the rows with both indices in [frame_lo, frame_hi] (done by
+    // the interior kernel of fourier2d.cu); off when frame == 0
+    int frame, frame_lo, frame_hi;
     OutDev M, K;
     int do_mass, do_stiff;
     Staging sg;
@@ -376,12 +379,31 @@ __global__ void __launch_bounds__(256) k_fourier2d(const GenericArgs a) {
     const int kg = g >> 1;
     const int segs = (N + kF2dSeg - 1) / kF2dSeg;
     const int line0 = (int)(a.row_begin / N), line1 = (int)((a.row_end - 1) / N);
-    const int64_t items = (int64_t)(line1 - line0 + 1) * segs;
+    // work items: (line, 32-row segment); in frame mode the lines with i2 in [frame_lo, frame_hi]
+    // contribute only their two frame pieces x < frame_lo and x > frame_hi
+    const int I0 = a.frame ? max(line0, a.frame_lo) : 1, I1 = a.frame ? min(line1, a.frame_hi) : 0;
+    const int nI = I1 >= I0 ? I1 - I0 + 1 : 0;
+    const int F0 = a.frame ? max(0, min(line1, a.frame_lo - 1) - line0 + 1) : line1 - line0 + 1;
+    const int nF = line1 - line0 + 1 - nI;
+    const int64_t items = (int64_t)nI * 2 + (int64_t)nF * segs;
     for (int64_t it = (int64_t)blockIdx.x * warps + warp; it < items; it += (int64_t)gridDim.x * warps) {
-        const int i2 = line0 + (int)(it / segs);
-        const int x0 = max((int)((int64_t)(it % segs) * kF2dSeg), (int)(a.row_begin - (int64_t)i2 * N));
-        const int x1 = min((int)((int64_t)(it % segs) * kF2dSeg + kF2dSeg), (int)min((int64_t)N, a.row_end - (int64_t)i2 * N));
+        int i2, x0, x1;
+        if (it < (int64_t)nI * 2) {
+            i2 = I0 + (int)(it >> 1);
+            x0 = (it & 1) ? a.frame_hi + 1 : 0;
+            x1 = (it & 1) ? N : a.frame_lo;
+        } else {
+            const int64_t f = (it - (int64_t)nI * 2) / segs;
+            const int sg = (int)((it - (int64_t)nI * 2) % segs);
+            i2 = f < F0 ? line0 + (int)f : max(line0, a.frame_hi + 1) + (int)(f - F0);
+            x0 = sg * kF2dSeg;
+            x1 = min(x0 + kF2dSeg, N);
+        }
+        x0 = max(x0, (int)(a.row_begin - (int64_t)i2 * N));
+        x1 = min(x1, (int)min((int64_t)N, a.row_end - (int64_t)i2 * N));
+        if (x0 >= x1) continue;
         // ---- y-side data of the line: counts, exponent B fragments, weights, y-stage A fragments
+        const bool i2in = a.frame && a.frame_lo <= i2 && i2 <= a.frame_hi;
         const int nym = __ldg(T.mM + i2), nyk = __ldg(T.mK + i2);
         if (nym > 4 || nyk > 4) continue;                  // whole line in the generic shell pass
         const bool yv = kg < (gs ? nyk : nym);
@@ -424,6 +446,7 @@ __global__ void __launch_bounds__(256) k_fourier2d(const GenericArgs a) {
             const XData cx = nx;
             if (i1 + 1 < x1) load_x(i1 + 1, nx);
             if (cx.nxm > 4 || cx.nxk > 4) continue;        // generic shell pass
+            if (i2in && i1 >= a.frame_lo && i1 <= a.frame_hi) continue;
             // ---- exponent GEMM: E[x-node g][y-node n] (B fragments of the line in yb) -------
             const bool xv = kg < (gs ? cx.nxk : cx.nxm);
             double e0 = 0.0, e1 = 0.0;
@@ -509,7 +532,10 @@ int launch_fourier2d_p(const GenericArgs& a, cudaStream_t st) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t segs = (a.N + kF2dSeg - 1) / kF2dSeg;
-    const int64_t items = ((a.row_end - 1) / a.N - a.row_begin / a.N + 1) * segs;
+    const int64_t lines = (a.row_end - 1) / a.N - a.row_begin / a.N + 1;
+    // (frame mode: most lines have only 2 short pieces; the grid only needs to cover the items)
+    const int64_t items = a.frame ? std::min<int64_t>(lines * segs, 2 * lines + (int64_t)(a.N - (a.frame_hi - a.frame_lo + 1)) * segs)
+                                  : lines * segs;
     int64_t blocks = std::min<int64_t>((items + 7) / 8, (int64_t)sms * 32);
     blocks = std::max<int64_t>(blocks, 1);
     const int mode = (a.do_mass ? 1 : 0) | (a.do_stiff ? 2 : 0);
@@ -1030,9 +1056,25 @@ int launch_assemble(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t*
     }
     int rc = WGQ_EUNSUPPORTED;
     const int key = R->p * 10 + R->dim;
+    a.frame = 0;
     if (!force_generic && R->dim == 2 && c->kind == WGQ_COEF_FOURIER_LOGN && a.coef.n_modes > 0) {
-        // tensor-core pass over the rows whose directions all have <= 4 nodes, then the generic
-        // kernel over the remaining shell (rows touching a GL-fallback boundary class, R1)
+        // class-I rows (both indices in [2p, N-1-2p]) in the interior kernel (fourier2d.cu), the
+        // frame in the per-row tensor-core kernel over the rows whose directions all have <= 4
+        // nodes, then the generic kernel over the remaining shell (GL-fallback classes, R1)
+        static const bool interior_on = [] {
+            const char* e = getenv("WGQ_F2D_INTERIOR");
+            return !(e && e[0] == '0');
+        }();
+        if (interior_on && f2d_interior_applies(R, T, c)) {
+            rc = launch_f2d_interior(R, T, tab, a.cw, M, K, st);
+            if (rc != WGQ_OK) {
+                cudaFreeAsync(tab, st);
+                return rc;
+            }
+            a.frame = 1;
+            a.frame_lo = 2 * R->p;
+            a.frame_hi = (int)(R->N - 1 - 2 * R->p);
+        }
         rc = R->p == 3 ? launch_fourier2d_p<3>(a, st) : launch_fourier2d_p<2>(a, st);
         if (rc != WGQ_OK) {
             cudaFreeAsync(tab, st);

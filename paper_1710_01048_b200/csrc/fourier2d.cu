@@ -1,0 +1,392 @@
+// 2D FOURIER_LOGN assembly of the interior rows (C3: p = 3, 2048^2, M + K), sm_100a.
+//
+// Row (i1, i2) samples the coefficient at three node tensors (a3): mass-x x mass-y (M),
+// stiffness-x x mass-y (K_x term) and mass-x x stiffness-y (K_y term), 48 samples for p = 3,
+// each an exp of a rank-2*n_modes exponent (R13: c = exp(sum_m a_m cos(2 pi k_m.x + theta_m)),
+// expanded with the angle-sum identity into the factor tables of k_coef_tables):
+//   E[x-node][y-node] = sum_m C^x_m C^y_m - S^x_m S^y_m.
+// Rows whose index is in the interior class I in both directions (2p <= i_a <= N-1-2p) share
+// one weighted 1D table per kind (w_k B_{i+o}(x_k), w_k B'_{i+o}(x_k); eq:GaussQuadSys P:249-252,
+// eq:GaussQuadSysStiff P:350-353), so with Aw = w * B folded
+//   M[o1][o2] = sum_{kx,ky} AwM[kx][o1] AwM[ky][o2] c(xM_kx, yM_ky)
+//   K[o1][o2] = sum AwK[kx][o1] AwM[ky][o2] c(xK_kx, yM_ky) + AwM[kx][o1] AwK[ky][o2] c(xM_kx, yK_ky)
+// which is the definition with the products regrouped, contracted y then x
+// (eq:Decompo P:194-199).
+//
+// One warp owns a block of 2 x-lines (i2 = a, a+1) and walks pairs of rows (i1, i1+1):
+//  * exponents on the FP64 tensor cores (DMMA m8n8k4): x-nodes of the pair form the 8 tile rows
+//    (x-node g = (kx = g/2, row g%2)); tile A_a / A_b take the 8 y-nodes of line a / b
+//    (y-node n = (ky = n/2, mass|stiffness)), tile B the stiffness x-nodes against the mass
+//    y-nodes of both lines (n = (ky = n/2, line a|b)).  Every product is a used sample: 12 DMMA
+//    per 4 rows, 6 samples per lane, lane-dense exp;
+//  * exp by a 64-entry table of 2^(j/64) (16 lane-private copies, conflict-free) and a degree-5
+//    polynomial on |r| <= ln2/128 (10 FP64 operations, < 1 ulp before rounding);
+//  * y stage on DMMA: the exp'd accumulator fragment is the B operand of T^T = Aw_y^T W^T as is
+//    (6 DMMA per 4 rows);
+//  * x stage on DFMA with the structural zeros of the class-I tables skipped (16 of 28 per term;
+//    coefficients from the kernel-parameter constant bank), lanes own (row, o2) columns;
+//  * the rows are staged in shared memory and written as contiguous runs with streaming stores.
+// The frame (rows with an index outside class I) goes through k_fourier2d (assemble.cu).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+
+#include "internal.h"
+
+namespace wgq {
+namespace {
+
+constexpr int kF2iWarps = 8;
+constexpr int kF2iMinBlocks = 2;
+constexpr int kF2iChunk = 8;              // row pairs per work item (the line pair's y data is loaded once)
+constexpr int kF2iRun = 100;                             // staging of one (line, matrix) run: 2 rows + shift + pad
+constexpr int kF2iWarpSmem = 4 * kF2iRun;                // output staging of 2 lines x M, K
+
+struct F2iArgs {
+    const double* ctab;  // k_coef_tables layout: ((kind * N + r) * kMaxNodes + k) * cw + j
+    int cw;
+    int64_t N, row_begin, row_end;
+    int lo, hi;          // class-I index range [lo, hi] (both directions)
+    int line0, line1;    // interior lines inside the row range
+    double* Mv;
+    double* Kv;
+    int64_t ldM, ldK;
+    const int64_t* rpM;
+    const int64_t* rpK;
+    int csr;
+    int dbg;             // profiling switches (WGQ_F2D_DBG): 1 no global stores, 2 no exponent / exp
+    double AwM[4][7], AwK[4][7];   // interior weighted tables w_k B_{i+o}(x_k), w_k B'_{i+o}(x_k)
+};
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+// Taylor coefficients of e^r (degree 5) from the constant bank
+__constant__ double kExp5[6] = {1.0, 1.0, 0.5, 1.0 / 6.0, 1.0 / 24.0, 1.0 / 120.0};
+
+// exp(x), |x| < 700: x = k ln2/64 + r with k = rint(64 x / ln2) (the 1.5*2^52 shifter leaves k
+// in the low word), |r| <= ln2/128 (Cody-Waite two-part ln2/64), e^x = 2^(k>>6) 2^((k&63)/64) e^r.
+// tbl holds 2^(j/64) at [j * 16 + copy]: the 16 lanes of a half-warp read 16 different banks.
+__device__ __forceinline__ double exp_tab(double x, const double* tbl, int copy) {
+    const double s = fma(x, 92.332482616893656877, 6755399441055744.0);   // 64/ln2, 1.5*2^52
+    const double kd = s - 6755399441055744.0;
+    const int k = __double2loint(s);
+    double r = fma(-kd, 6.93147180369123816490e-01 / 64.0, x);
+    r = fma(-kd, 1.90821492927058770002e-10 / 64.0, r);
+    double q = kExp5[5];
+#pragma unroll
+    for (int i = 4; i >= 0; --i) q = fma(q, r, kExp5[i]);
+    const double t = tbl[((k & 63) << 4) | copy];
+    return q * __hiloint2double(__double2hiint(t) + ((k >> 6) << 20), __double2loint(t));
+}
+
+__device__ __forceinline__ void st_out(double* p, double v, uint64_t pol) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+
+__device__ __forceinline__ void st_out2(double* p, double v0, double v1, uint64_t pol) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v0), "d"(v1),
+                 "l"(pol)
+                 : "memory");
+}
+
+// The general case: the two staged rows src[0..48], src[49..97] at d0, d1 (null: not stored).
+__device__ __forceinline__ void store_rows(double* d0, double* d1, const double* src, int lane, uint64_t pol) {
+    for (int e = lane; e < 98; e += 32) {
+        double* p = e < 49 ? d0 : d1;
+        if (p) st_out(p + (e < 49 ? e : e - 49), src[e], pol);
+    }
+}
+
+// EXACT: cw == 4 KS (every k-step column is a table column, no predicated loads)
+template <int KS, bool EXACT>
+__global__ void __launch_bounds__(kF2iWarps * 32, kF2iMinBlocks) k_f2d_interior(const F2iArgs a) {
+    constexpr int S = 7;
+    __shared__ double tbl[64 * 16];
+    extern __shared__ double stage[];      // per warp: T staging, output staging
+    for (int e = threadIdx.x; e < 64 * 16; e += blockDim.x) tbl[e] = exp2((double)(e >> 4) * (1.0 / 64.0));
+    __syncthreads();
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, warp = threadIdx.x >> 5;
+    const int copy = lane & 15;
+    double* ws = stage + warp * kF2iWarpSmem;
+    double* os = ws;
+    const uint64_t pol = pol_evict_first();
+    const int64_t N = a.N;
+    const int cw = EXACT ? 4 * KS : a.cw;
+    const int64_t nstride = (int64_t)kMaxNodes * cw;                 // doubles per 1D row of ctab
+    // y-stage A fragments (class-I lines): lane (g, t) = Aw^T[o2 = g][ky = t]
+    double aMy = 0.0, aKy = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+        for (int oo = 0; oo < S; ++oo)
+            if (kk == t && oo == g) {       // static parameter indices (no local-memory copy)
+                aMy = a.AwM[kk][oo];
+                aKy = a.AwK[kk][oo];
+            }
+    // the exponent tables of this lane's x-node (kx = g >> 1, row + (g & 1)) and y-nodes
+    const int jt = t;
+    const double ysg = (t & 1) ? -1.0 : 1.0;   // S components negated: E = sum C C - S S
+
+    const int nlines = a.line1 - a.line0 + 1;
+    const int lpairs = (nlines + 1) >> 1;
+    const int rpairs = (a.hi - a.lo + 2) >> 1;
+    const int chunks = (rpairs + kF2iChunk - 1) / kF2iChunk;
+    const int64_t items = (int64_t)lpairs * chunks;
+    for (int64_t it = (int64_t)blockIdx.x * kF2iWarps + warp; it < items; it += (int64_t)gridDim.x * kF2iWarps) {
+        const int lp = (int)(it / chunks), ch = (int)(it % chunks);
+        const int La = a.line0 + 2 * lp;
+        const bool bval = La + 1 <= a.line1;
+        // ---- line-pair data: exponent B fragments
+        double Ya[KS], Yb[KS], Yab[KS];
+        {
+            const int ky = g >> 1, hi = g & 1;
+            const double* pa = a.ctab + ((int64_t)(2 + hi) * N + La) * nstride + ky * cw + jt;
+            const double* pb = pa + nstride;
+            const double* pab = a.ctab + ((int64_t)2 * N + La + hi) * nstride + ky * cw + jt;
+#pragma unroll
+            for (int s = 0; s < KS; ++s) {
+                const bool in = EXACT || 4 * s + jt < cw;
+                Ya[s] = in ? ysg * __ldg(pa + 4 * s) : 0.0;
+                Yb[s] = in ? ysg * __ldg(pb + 4 * s) : 0.0;
+                Yab[s] = in ? ysg * __ldg(pab + 4 * s) : 0.0;
+            }
+        }
+        const int p0 = ch * kF2iChunk, p1 = min(rpairs, p0 + kF2iChunk);
+        // output runs: when every row of the chunk in line L is stored and consecutive rows are
+        // 49 doubles apart (ELL ld = 49, or CSR: class-I rows have full stencils), the pair's
+        // two rows are one 98-double run at base[L][mat] + 98 (pr - p0); sh[L] shifts the
+        // staging by one double when the run starts 8 bytes off a 16-byte boundary
+        bool full[2];
+        int sh[2];
+        double* base[2][2];
+#pragma unroll
+        for (int L = 0; L < 2; ++L) {
+            const int64_t g0 = (int64_t)(La + L) * N + a.lo + 2 * p0;
+            const int64_t g1 = g0 + 2 * (p1 - p0) - 1;
+            full[L] = (L == 0 || bval) && a.lo + 2 * p1 - 1 <= a.hi && g0 >= a.row_begin && g1 < a.row_end &&
+                      (a.csr || ((!a.Mv || a.ldM == 49) && (!a.Kv || a.ldK == 49)));
+#pragma unroll
+            for (int mat = 0; mat < 2; ++mat) {
+                double* dst = mat ? a.Kv : a.Mv;
+                base[L][mat] = nullptr;
+                if (full[L] && dst) {
+                    const int64_t orow = g0 - a.row_begin;
+                    base[L][mat] = dst + (a.csr ? (mat ? a.rpK : a.rpM)[orow] : orow * 49);
+                }
+            }
+            double* b0 = base[L][0] ? base[L][0] : base[L][1];
+            sh[L] = b0 && (reinterpret_cast<uintptr_t>(b0) & 15) ? 1 : 0;
+            // M and K runs must share the shift (equal alignment); else store line L per row
+            if (base[L][0] && base[L][1] &&
+                ((reinterpret_cast<uintptr_t>(base[L][0]) ^ reinterpret_cast<uintptr_t>(base[L][1])) & 15))
+                full[L] = false, sh[L] = 0;
+        }
+        double* dl[2][2];                 // per lane: its 16-byte pair of the (L, mat) run of this step
+        const double* sl[2][2];           // and of the staging
+        double* sb[2];                    // x-stage staging base of line L for lane (g, t)
+#pragma unroll
+        for (int L = 0; L < 2; ++L) {
+#pragma unroll
+            for (int mat = 0; mat < 2; ++mat) {
+                dl[L][mat] = base[L][mat] ? base[L][mat] + sh[L] + 2 * lane : nullptr;
+                sl[L][mat] = os + (L * 2 + mat) * kF2iRun + 2 * sh[L] + 2 * lane;
+            }
+            sb[L] = os + L * 2 * kF2iRun + sh[L] + g + 14 * t;
+        }
+        // x-node g of the pair = (kx = g >> 1, row i1 + (g & 1)); prefetched one pair ahead
+        const double* pxm = a.ctab + (int64_t)(a.lo + 2 * p0 + (g & 1)) * nstride + (g >> 1) * cw + jt;
+        const double* pxk = pxm + N * nstride;
+        double XM[KS], XK[KS];
+#pragma unroll
+        for (int s = 0; s < KS; ++s) {
+            const bool in = EXACT || 4 * s + jt < cw;
+            XM[s] = in && p0 < p1 ? __ldg(pxm + 4 * s) : 0.0;
+            XK[s] = in && p0 < p1 ? __ldg(pxk + 4 * s) : 0.0;
+        }
+        for (int pr = p0; pr < p1; ++pr) {
+            const int i1 = a.lo + 2 * pr;
+            // ---- exponents (a3): three 8 x 8 x 2n_modes products
+            double ea0 = 0.0, ea1 = 0.0, eb0 = 0.0, eb1 = 0.0, ek0 = 0.0, ek1 = 0.0;
+            if (a.dbg & 2) {
+                ea0 = XM[0], ea1 = XM[1], eb0 = XM[2], eb1 = XM[3], ek0 = XK[0], ek1 = XK[1];
+            } else
+#pragma unroll
+            for (int s = 0; s < KS; ++s) {
+                dmma(ea0, ea1, XM[s], Ya[s]);
+                dmma(eb0, eb1, XM[s], Yb[s]);
+                dmma(ek0, ek1, XK[s], Yab[s]);
+            }
+            pxm += 2 * nstride;
+            pxk += 2 * nstride;
+            if (pr + 1 < p1) {
+#pragma unroll
+                for (int s = 0; s < KS; ++s) {
+                    const bool in = EXACT || 4 * s + jt < cw;
+                    XM[s] = in ? __ldg(pxm + 4 * s) : 0.0;
+                    XK[s] = in ? __ldg(pxk + 4 * s) : 0.0;
+                }
+            }
+            // ---- samples c = exp(E): lane (g, t) holds x-node g against y-node (ky = t, *)
+            double wMa, wKya, wMb, wKyb, wKxa, wKxb;
+            if (a.dbg & 2) {
+                wMa = ea0, wKya = ea1, wMb = eb0, wKyb = eb1, wKxa = ek0, wKxb = ek1;
+            } else {
+                wMa = exp_tab(ea0, tbl, copy), wKya = exp_tab(ea1, tbl, copy);
+                wMb = exp_tab(eb0, tbl, copy), wKyb = exp_tab(eb1, tbl, copy);
+                wKxa = exp_tab(ek0, tbl, copy), wKxb = exp_tab(ek1, tbl, copy);
+            }
+            // ---- y stage (a5): T^T[o2][x-node] = Aw_y^T[o2][ky] W^T[ky][x-node]
+            double tM[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, tKx[2][2] = {{0.0, 0.0}, {0.0, 0.0}},
+                   tKy[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+            dmma(tM[0][0], tM[0][1], aMy, wMa);
+            dmma(tKy[0][0], tKy[0][1], aKy, wKya);
+            dmma(tKx[0][0], tKx[0][1], aMy, wKxa);
+            dmma(tM[1][0], tM[1][1], aMy, wMb);
+            dmma(tKy[1][0], tKy[1][1], aKy, wKyb);
+            dmma(tKx[1][0], tKx[1][1], aMy, wKxb);
+            // lane (g, t) now holds T[line][row i][kx = t][o2 = g] in component i: exactly the B
+            // fragment of the x stage of row i,
+            // ---- x stage (a5, a6) on DMMA: M[o1][o2] = Aw_x^T[o1][kx] T[kx][o2] (the class-I A
+            // operand Aw^T[o1 = g][kx = t] is the y stage's), K = AwK_x^T T_Kx + AwM_x^T T_Ky;
+            // lane (g, t) receives M[o1 = g][o2 = 2t + j], staged at slot o1 + 7 o2 of its row
+#pragma unroll
+            for (int L = 0; L < 2; ++L)
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    double m0 = 0.0, m1 = 0.0, k0 = 0.0, k1 = 0.0;
+                    dmma(m0, m1, aMy, tM[L][i]);
+                    dmma(k0, k1, aKy, tKx[L][i]);
+                    dmma(k0, k1, aMy, tKy[L][i]);
+                    double* b = sb[L] + i * 49;
+                    if (g < S) {
+                        b[0] = m0;
+                        b[kF2iRun] = k0;
+                        if (t < 3) {
+                            b[7] = m1;
+                            b[kF2iRun + 7] = k1;
+                        }
+                    }
+                }
+            __syncwarp();
+            // ---- a7: the two rows of each line (one 98-double run when full[L]: 16-byte streaming
+            // stores, loads from the staging first), M and K
+#pragma unroll
+            for (int L = 0; L < 2; ++L) {
+#pragma unroll
+                for (int mat = 0; mat < 2; ++mat) {
+                    double* dst = mat ? a.Kv : a.Mv;
+                    if (!dst || (a.dbg & 1)) continue;
+                    if (full[L]) {
+                        // this lane's 16-byte pair(s) of the run; with sh = 1 lanes 0 / 1 also
+                        // store the run's first / last element (offsets -1 / +94 from their pair)
+                        const double* sp = sl[L][mat];
+                        const double2 v0 = *reinterpret_cast<const double2*>(sp);
+                        double2 v1 = make_double2(0.0, 0.0);
+                        const bool two = lane + 32 < 49 - sh[L];
+                        if (two) v1 = *reinterpret_cast<const double2*>(sp + 64);
+                        const bool edge = sh[L] && lane < 2;
+                        const double ve = edge ? sp[lane ? 94 : -1] : 0.0;
+                        double* d = dl[L][mat];
+                        st_out2(d, v0.x, v0.y, pol);
+                        if (two) st_out2(d + 64, v1.x, v1.y, pol);
+                        if (edge) st_out(d + (lane ? 94 : -1), ve, pol);
+                        dl[L][mat] = d + 98;
+                        continue;
+                    }
+                    const double* src = os + (L * 2 + mat) * kF2iRun + sh[L];
+                    double* d[2];
+#pragma unroll
+                    for (int i = 0; i < 2; ++i) {
+                        const int64_t grow = (int64_t)(La + L) * N + i1 + i;
+                        const bool ok = (L == 0 || bval) && i1 + i <= a.hi && grow >= a.row_begin && grow < a.row_end;
+                        const int64_t orow = grow - a.row_begin;
+                        d[i] = !ok ? nullptr
+                                   : dst + (a.csr ? (mat ? a.rpK : a.rpM)[orow] : orow * (mat ? a.ldK : a.ldM));
+                    }
+                    store_rows(d[0], d[1], src, lane, pol);
+                }
+            }
+            __syncwarp();                         // the staging is rewritten by the next pair
+        }
+    }
+}
+
+}  // namespace
+
+bool f2d_interior_applies(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c) {
+    if (R->p != 3 || R->dim != 2 || c->kind != WGQ_COEF_FOURIER_LOGN) return false;
+    if (c->n_modes <= 0 || c->n_modes > 16 || !T.int_ok) return false;
+    if (T.imM != 4 || T.imK != 4) return false;
+    const int64_t lo = 2 * R->p, hi = R->N - 1 - 2 * R->p;
+    if (hi < lo) return false;
+    // the x stage skips the band's structural zeros: node k of a class-I row is nonzero on
+    // columns o in [k, k + p] only (it lies in the support's element k)
+    for (int kx = 0; kx < 4; ++kx)
+        for (int o = 0; o < 7; ++o)
+            if ((o < kx || o > kx + 3) && (T.iAwM[kx][o] != 0.0 || T.iAwK[kx][o] != 0.0)) return false;
+    return true;
+}
+
+int launch_f2d_interior(const wgq_rules_s* R, const RowTables& T, const double* ctab, int cw, const wgq_out_t* M,
+                        const wgq_out_t* K, cudaStream_t st) {
+    const wgq_out_t* any = M ? M : K;
+    F2iArgs a{};
+    a.ctab = ctab;
+    a.cw = cw;
+    a.N = R->N;
+    a.row_begin = any->row_begin;
+    a.row_end = any->row_end;
+    a.lo = 2 * R->p;
+    a.hi = (int)(R->N - 1 - 2 * R->p);
+    const int64_t l0 = a.row_begin / R->N, l1 = (a.row_end - 1) / R->N;
+    a.line0 = (int)std::max<int64_t>(l0, a.lo);
+    a.line1 = (int)std::min<int64_t>(l1, a.hi);
+    if (a.row_end <= a.row_begin || a.line1 < a.line0) return WGQ_OK;
+    a.Mv = M ? M->values : nullptr;
+    a.Kv = K ? K->values : nullptr;
+    a.ldM = M ? M->ld : 0;
+    a.ldK = K ? K->ld : 0;
+    a.rpM = M ? M->row_ptr : nullptr;
+    a.rpK = K ? K->row_ptr : nullptr;
+    a.csr = any->layout == WGQ_CSR;
+    static const int dbg = [] {
+        const char* e = getenv("WGQ_F2D_DBG");
+        return e ? atoi(e) : 0;
+    }();
+    a.dbg = dbg;
+    for (int kx = 0; kx < 4; ++kx)
+        for (int o = 0; o < 7; ++o) {
+            a.AwM[kx][o] = T.iAwM[kx][o];
+            a.AwK[kx][o] = T.iAwK[kx][o];
+        }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t lpairs = (a.line1 - a.line0 + 2) / 2;
+    const int64_t rpairs = (a.hi - a.lo + 2) / 2;
+    const int64_t items = lpairs * ((rpairs + kF2iChunk - 1) / kF2iChunk);
+    int64_t blocks = std::min<int64_t>((items + kF2iWarps - 1) / kF2iWarps, (int64_t)sms * kF2iMinBlocks);
+    blocks = std::max<int64_t>(blocks, 1);
+    const size_t smem = (size_t)kF2iWarps * kF2iWarpSmem * sizeof(double);
+    auto go = [&](auto kern) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return WGQ_ECUDA;
+        kern<<<(unsigned)blocks, kF2iWarps * 32, smem, st>>>(a);
+        return WGQ_OK;
+    };
+    int rc;
+    if (cw == 16) rc = go(k_f2d_interior<4, true>);
+    else if (cw < 16) rc = go(k_f2d_interior<4, false>);
+    else if (cw == 32) rc = go(k_f2d_interior<8, true>);
+    else rc = go(k_f2d_interior<8, false>);
+    if (rc != WGQ_OK) return rc;
+    return cudaGetLastError() == cudaSuccess ? WGQ_OK : WGQ_ECUDA;
+}
+
+}  // namespace wgq

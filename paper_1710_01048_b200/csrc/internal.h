@@ -48,6 +48,13 @@ struct RowTables {
     double* PM = nullptr;      // [N][kMaxV][kMaxS]
     double* PK = nullptr;      // [N][kMaxV][kMaxS]
     void* base = nullptr;      // single allocation
+    // Host copies of one class-I (interior, 2p <= r <= N-1-2p) row's weighted tables
+    // iAwM[k][o] = wM[k] VM[k][o], iAwK[k][o] = wK[k] DK[k][o] (shift-invariant up to rounding:
+    // the interior kernels take them as kernel parameters), filled after the one-time build.
+    bool int_ok = false;
+    int imM = 0, imK = 0;
+    double iAwM[kMaxP + 1][kMaxS] = {};
+    double iAwK[kMaxP + 1][kMaxS] = {};
 };
 
 }  // namespace wgq
@@ -112,6 +119,14 @@ int launch_sep_apply(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t
                      int64_t row_begin, int64_t row_end, double* yM, double* yK, void* stream);
 int launch_line_apply(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, const double* u,
                       int64_t u_row0, int64_t row_begin, int64_t row_end, double* yM, double* yK, void* stream);
+
+// fourier2d.cu (2D FOURIER_LOGN, p = 3, rows of class I in both directions; C3)
+bool f2d_interior_applies(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c);
+#ifdef __CUDACC__
+int launch_f2d_interior(const wgq_rules_s* R, const RowTables& T, const double* ctab, int cw, const wgq_out_t* M,
+                        const wgq_out_t* K, cudaStream_t st);
+#endif
+int fetch_interior_tables(const wgq_rules_s* R, RowTables* T);
 
 // separable.cu (CONST, TRIG_SEP coefficients)
 bool sep_applies(const wgq_coeff_t* c);

@@ -217,6 +217,31 @@ int build_row_tables(const wgq_rules_s* R, RowTables* T, void* stream) {
     return WGQ_OK;
 }
 
+int fetch_interior_tables(const wgq_rules_s* R, RowTables* T) {
+    T->int_ok = false;
+    const int64_t r = 2 * R->p;                  // first class-I row (class I: 2p <= r <= n-1-p)
+    if (r > R->n - 1 - R->p) return WGQ_OK;      // no class-I rows on this mesh
+    int m[2];
+    double w[2][kMaxNodes], A[2][kMaxNodes * kMaxS];
+    if (cudaMemcpy(&m[0], T->mM + r, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(&m[1], T->mK + r, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(w[0], T->wM + r * kMaxMassNodes, sizeof(w[0]), cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(w[1], T->wK + r * kMaxStiffNodes, sizeof(w[1]), cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(A[0], T->VM + r * kMaxMassNodes * kMaxS, sizeof(A[0]), cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(A[1], T->DK + r * kMaxStiffNodes * kMaxS, sizeof(A[1]), cudaMemcpyDeviceToHost) != cudaSuccess)
+        return WGQ_ECUDA;
+    if (m[0] > kMaxP + 1 || m[1] > kMaxP + 1) return WGQ_OK;
+    T->imM = m[0];
+    T->imK = m[1];
+    for (int k = 0; k <= kMaxP; ++k)
+        for (int o = 0; o < kMaxS; ++o) {
+            T->iAwM[k][o] = k < m[0] ? w[0][k] * A[0][k * kMaxS + o] : 0.0;
+            T->iAwK[k][o] = k < m[1] ? w[1][k] * A[1][k * kMaxS + o] : 0.0;
+        }
+    T->int_ok = true;
+    return WGQ_OK;
+}
+
 void free_row_tables(RowTables* T) {
     if (T->base) cudaFree(T->base);
     T->base = nullptr;

@@ -165,3 +165,35 @@ def test_row_moments_identities():
     for a in range(d):
         assert np.max(np.abs(mom["mass"][:, 1 + a] - mx[:, a]) / scaleM) < 1e-13
         assert np.max(np.abs(mom["stiffness"][:, 1 + a] - kx[:, a]) / scaleK) < 1e-13
+
+
+@pytest.mark.parametrize("n", [9, 10, 21, 40])
+def test_fourier2d_interior_kernel(n):
+    """C3's kernel pair (p = 3, 2D FOURIER): the class-I interior kernel (2 lines x row pairs,
+    chunks of 8 pairs) plus the frame kernel, over whole meshes whose interior has an odd / even
+    number of lines and rows and several chunks, and over ragged row ranges that start and end
+    inside lines (slabs), ELL with padded ld and CSR."""
+    from paper_1710_01048_b200 import api, wgq
+    p, d = 3, 2
+    N = n + p
+    desc = inputs.coefficient({"kind": "fourier_logn", "seed": 13, "n_modes": 8, "amp": 0.3}, d)
+    rows = np.arange(N ** d)
+    ref = oasm.assemble_rows(p, n, d, rows, desc)
+    sc = oasm.assemble_rows(p, n, d, rows, desc, absolute=True)
+    g, _ = gpu_assemble(p, n, d, desc)
+    for k in ("mass", "stiffness"):
+        compare(g[k], ref[k], ("f2d-int", n, k), sc[k])
+    rules = wgq.Rules(p, n, d)
+    c = api.coefficient(desc)
+    for lo, hi in ((7 * N + 3, 9 * N + 8), (N + 5, N * N - N - 2), (6 * N + 6, 6 * N + 9)):
+        out = api.assemble(rules, c, row_begin=lo, row_end=hi, ld=50)
+        rp, ci, vals = api.assemble_csr(rules, c, row_begin=lo, row_end=hi)
+        torch.cuda.synchronize()
+        rpn = rp.cpu().numpy()
+        for k in ("mass", "stiffness"):
+            e = out[k].cpu().numpy()
+            assert np.array_equal(e[:, :49], g[k][lo:hi]), (lo, hi, k)
+            v = vals[k].cpu().numpy()
+            for r in range(lo, hi):
+                cols = oasm.ell_columns(p, n, d, r)
+                assert np.array_equal(v[rpn[r - lo]:rpn[r - lo + 1]], g[k][r][cols >= 0]), (r, k)
