@@ -120,7 +120,75 @@ def run_oracle(cfg, seconds, rows_hint=None):
         nnz += stencil_nnz(p, n, d, rows) * len(kinds)
         nrows += len(rows)
     sample = f"{nrows} rows of {cfg['name']} (whole x-lines of z-planes {[int(z) for z, _ in groups]}), {'+'.join(kinds)}"
+    run_oracle.last_rows = nrows
     return nnz / elapsed, sample, 1, elapsed
+
+
+_POOL_JOBS = None
+
+
+def _oracle_job(i):
+    """One block of the all-core oracle run (fork workers; the job list is inherited)."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import assemble as oasm
+    threadpool_limits(1)
+    cfg, desc, rows, grid, plane0 = _POOL_JOBS[i]
+    t0 = time.perf_counter()
+    oasm.assemble_rows(cfg["p"], cfg["n"], cfg["dim"], rows, desc, cfg["kinds"], grid=grid, plane0=plane0)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(cfg, seconds):
+    """The oracle (as it stands: plain numpy, oracle.assemble_rows) on the host cores: a
+    1-core run on a bounded sample of the workload, and the same per-core sample on every core
+    at once (fork workers over row blocks) -- SURVEY §8(d) / BASELINE.md §4."""
+    import multiprocessing as mp
+    global _POOL_JOBS
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(1):                      # the 1-core figure is one core
+        v1, sample, _, el1 = run_oracle(cfg, seconds / 2)
+    cores = os.cpu_count() or 1
+    desc = inputs.coefficient(cfg["coeff"], cfg["dim"])
+    # every core gets about the 1-core sample's rows, in 2 blocks per core
+    per_job = max(1, run_oracle.last_rows // 2)
+    jobs = []
+    for z, rows in oracle_sample_rows(cfg, cores * run_oracle.last_rows, seed=1):
+        grid, plane0 = _oracle_grid(cfg, z)
+        for b0 in range(0, len(rows), per_job):
+            jobs.append((cfg, desc, rows[b0:b0 + per_job], grid, plane0))
+    _POOL_JOBS = jobs
+    from oracle import assemble as oasm
+    oasm.tables_1d(cfg["p"], cfg["n"])
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    with ctx.Pool(cores) as pool:
+        pool.map(_oracle_job, range(len(jobs)), chunksize=1)
+    wall = time.perf_counter() - t0
+    nnz = sum(stencil_nnz(cfg["p"], cfg["n"], cfg["dim"], r) for _, _, r, _, _ in jobs) * len(cfg["kinds"])
+    rows_all = sum(len(r) for _, _, r, _, _ in jobs)
+    return {"value": nnz / wall, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{rows_all} rows of {cfg['name']} (whole x-lines of boundary and interior z-planes, "
+                      f"{len(jobs)} row blocks over {cores} processes), {'+'.join(cfg['kinds'])}",
+            "seconds": round(wall, 2),
+            "one_core": {"value": v1, "unit": UNIT, "cores": 1, "sample": sample, "seconds": round(el1, 2)}}
+
+
+def build_info():
+    """git commit of the tree (the GPU box gets a snapshot without .git: build() records it)."""
+    info = {}
+    try:
+        with open(os.path.join(ROOT, "paper_1710_01048_b200", "build_info.json")) as f:
+            info = json.load(f)
+    except Exception:
+        pass
+    try:
+        r = subprocess.run(["git", "-C", ROOT, "rev-parse", "HEAD"], capture_output=True, text=True, timeout=5)
+        if r.returncode == 0 and r.stdout.strip():
+            info["git_sha"] = r.stdout.strip()
+    except Exception:
+        pass
+    return info
 
 
 def _oracle_grid(cfg, z):
@@ -218,6 +286,15 @@ def arm_config(cfg, world, ld=None):
             "l2": "flushed (512 MB write) between timed steps; outputs >> L2"}
 
 
+def gpu_launches_per_step(cfg):
+    """Kernels of one assembly call: one, except the 2D FOURIER path (factor tables, then for
+    p = 3 the class-I interior kernel, the frame kernel and the GL-shell pass; for p = 2 the
+    per-row kernel and the shell pass)."""
+    if cfg["dim"] == 2 and cfg["coeff"]["kind"] == "fourier_logn":
+        return 4 if cfg["p"] == 3 else 3
+    return 1
+
+
 def main():
     args = parse()
     cfg = inputs.config(args.config, args.n)
@@ -233,10 +310,10 @@ def main():
         vals = []
         info = None
         for i in range(args.warmup + args.steps):
-            v, sample, cores, el = run_oracle(cfg, min(args.cpu_seconds, 60.0 / max(1, args.steps + args.warmup)))
+            cb = cpu_baseline(cfg, min(args.cpu_seconds, 120.0 / max(1, args.steps + args.warmup)))
             if i >= args.warmup:
-                vals.append(v)
-                info = (sample, cores)
+                vals.append(cb["value"])
+                info = (cb["sample"], cb["cores"])
         value = float(np.median(vals))
         line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
@@ -252,6 +329,7 @@ def main():
     import torch.distributed as dist
 
     from paper_1710_01048_b200 import api, wgq
+    from paper_1710_01048_b200 import dist as wdist
 
     # WGQ_BENCH_FUNCTIONAL=1: functional check of the N>1 code path on ONE GPU (every rank on
     # cuda:0, gloo on CPU tensors); its timings are not measurements (the ranks share a GPU)
@@ -314,28 +392,44 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     step_ms = [a.elapsed_time(b) for a, b in ev]
-    total_ms = float(np.sum(step_ms))
-    t = torch.tensor([total_ms], dtype=torch.float64, device=red_dev)
+    # per-step max over ranks; the metric is taken at the median step
+    t = torch.tensor(step_ms, dtype=torch.float64, device=red_dev)
     nz = torch.tensor([float(nnz_rank)], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(nz, op=dist.ReduceOp.SUM)
-    total_ms_max = float(t.item())
+    step_max = [float(x) for x in t.cpu().tolist()]
+    med_ms = float(np.median(step_max))
     nnz_all = float(nz.item())
-    value = nnz_all * args.steps / (total_ms_max / 1e3)
+    value = nnz_all / (med_ms / 1e3)
+
+    # self-check of the result (every N): order-independent hash of each matrix's slab, summed
+    # over ranks -- an N-GPU line carries the same hash as the 1-GPU line (rows are independent)
+    checksum = {}
+    for k in kinds:
+        h = torch.zeros(3, dtype=torch.int64, device="cuda")
+        wgq.wgq_checksum(rules, wgq.make_out(out[k], row_begin, row_end, ld=ld), h, stream)
+        torch.cuda.synchronize()
+        local = h.to(red_dev)
+        if world > 1:
+            hv, s1, s2 = wdist.reduce_checks(local)
+        else:
+            hv, s1, s2 = int(local[0].item()) & (2 ** 64 - 1), float(local[1:].view(torch.float64)[0]), \
+                float(local[1:].view(torch.float64)[1])
+        checksum[k] = {"hash": f"{hv:016x}", "sum": s1, "sumsq": s2}
 
     # roofline of the dominant (only) kernel: algorithmic bytes = rows x s^d x 8 x matrices
     alg_bytes = rows * rules.stencil * 8 * len(kinds)
-    kernel_s = np.mean(step_ms) / 1e3
+    kernel_s = float(np.median(step_ms)) / 1e3
     peak, peak_src = peaks()
     achieved = alg_bytes / kernel_s / 1e9
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "peak_source": peak_src,
             "traffic": traffic_from_profiles(cfg["name"]),
             "kernel": "wgq assembly (M+K fused)", "algorithmic_bytes_per_launch": int(alg_bytes),
-            "kernel_ms": round(kernel_s * 1e3, 4),
+            "kernel_ms": round(kernel_s * 1e3, 4), "kernel_ms_stat": "median of the timed steps (this rank)",
             "step_ms": {"min": round(float(np.min(step_ms)), 4), "median": round(float(np.median(step_ms)), 4),
-                        "max": round(float(np.max(step_ms)), 4)}}
+                        "mean": round(float(np.mean(step_ms)), 4), "max": round(float(np.max(step_ms)), 4)}}
 
     # end to end through the public API with HOST buffers (H2D of the coefficient slab, D2H of M, K)
     e2e = None
@@ -350,25 +444,59 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        v, sample, cores, el = run_oracle(cfg, args.cpu_seconds)
-        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
-               "seconds": round(el, 2)}
+        cpu = cpu_baseline(cfg, args.cpu_seconds)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": total_ms_max / args.steps, "higher_is_better": True,
+                "warmup": args.warmup, "ms_per_step": med_ms, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": arm_config(cfg, world, ld),
                 # one assembly kernel per step; the 2D Fourier path adds its per-call factor tables
                 # and the generic shell-row pass
-                "gpu_launches": args.steps * (3 if (d == 2 and cfg["coeff"]["kind"] == "fourier_logn") else 1),
+                "gpu_launches": args.steps * gpu_launches_per_step(cfg),
                 "roofline": roof, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu, "extras": extras,
-                "setup": setup}
+                "setup": setup, "checksum": checksum, "nnz_per_step": int(nnz_all),
+                "timing": {"stat": "median over the timed steps of the per-step max over ranks",
+                           "ms_mean": float(np.mean(step_max)), "ms_min": float(np.min(step_max)),
+                           "ms_max": float(np.max(step_max))},
+                "build": build_info(), "peaks": {"hbm_gbs": peak, "source": peak_src}}
         if functional:
             line["functional_check"] = "WGQ_BENCH_FUNCTIONAL=1: all ranks on one GPU over gloo; not a measurement"
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def apply_flops_per_row(rules):
+    """Algorithmic FP64 flops per row of the matrix-free product y_M = M u, y_K = K u on the GRID
+    line structure, structural zeros skipped: with the interior vertex-projected
+    tables P^M, P^K (V = p+2 vertex planes x S = 2p+1 columns; entry (v, o) is nonzero iff some
+    node k of the row's rule lies in element f_k = floor(tau_k) with v in {f_k, f_k+1} and o in
+    [f_k, f_k+p]) of nz_M, nz_K nonzeros,
+      phase A (one vertex plane per row): TT_M = P^M_y patch (nz_M V), TT_K (nz_K V),
+              H_M = TT_M P^M_z (S nz_M), H_K = TT_K P^M_z + TT_M P^K_z (S nz_M + S nz_K);
+      D stage: D_X(c, X) = sum_{o2,o3} H_X u (S^2 per matrix) for the n_delta distinct offsets
+               X - c = o - v of the nonzeros (one (c, X) pair per offset per row);
+      finish: y_M = sum P^M D_M (nz_M), y_K = sum P^K D_M + P^M D_K (nz_K + nz_M).
+    Returns (flops per row, definition text)."""
+    from paper_1710_01048_b200 import wgq
+    p = rules.p
+    V, S = p + 2, 2 * p + 1
+    nz, offs = {}, set()
+    for kind, kc in (("M", wgq.WGQ_MASS), ("K", wgq.WGQ_STIFFNESS)):
+        tau, om, _ = wgq.wgq_rules_query(rules, p, kc)
+        pat = set()
+        for tk, wk in zip(tau, om):
+            f = int(np.floor(tk))
+            for v in (f, f + 1):
+                for o in range(f, f + p + 1):
+                    pat.add((v, o))
+        nz[kind] = len(pat)
+        offs |= {o - v for v, o in pat}
+    nzM, nzK, nd = nz["M"], nz["K"], len(offs)
+    fma = V * (nzM + nzK) + S * (2 * nzM + nzK) + 2 * S * S * nd + 2 * nzM + nzK
+    return 2 * fma, (f"2 x FMA: phase A V(nzM+nzK)+S(2nzM+nzK) + D 2 S^2 n_delta + finish 2nzM+nzK with "
+                     f"p={p}, V={V}, S={S}, nzM={nzM}, nzK={nzK}, n_delta={nd}")
 
 
 def _time_ms(fn, reps=5, flush=None):
@@ -425,22 +553,49 @@ def run_extras(rules5, coef5, peak):
     del vals, row_ptr, dm, dk
     torch.cuda.empty_cache()
     n_rows = rules5.n_rows
+    # peak microbenchmarks of this box, same session (tools/peaks.cu, built by build()): the
+    # FP64 denominator of the matrix-free product
+    exe = os.path.join(ROOT, "tools", "peaks")
+    if os.path.exists(exe):
+        try:
+            r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+            out["box_peaks"] = json.loads(r.stdout.strip().splitlines()[-1])
+        except Exception as e:          # the headline numbers do not depend on it
+            out["box_peaks"] = {"error": str(e)[:200]}
+    fp64_peak, fp64_src = out.get("box_peaks", {}).get("fp64_tflops"), "tools/peaks DFMA (this box, this run)"
+    if not fp64_peak:
+        fp64_peak, fp64_src = 34.2, "DFMA microbenchmark, round 1 (DESIGN.md §5)"
     b = torch.empty(n_rows, dtype=torch.float64, device="cuda")
     ms = _time_ms(lambda: api.assemble_load(rules5, coef5, out=b), flush=flush)
     nv = rules5.n + 1
     load_bytes = (nv ** 3 + n_rows) * 8                  # the vertex grid read once + b written
-    out["operators"]["load_vector_C5"] = {"ms": round(ms, 4), "rows_per_s": n_rows / (ms / 1e3),
-                                          "hbm_gbs": round(load_bytes / (ms / 1e3) / 1e9, 1),
-                                          "hbm_frac": round(load_bytes / (ms / 1e3) / 1e9 / peak, 4)}
+    out["operators"]["load_vector_C5"] = {
+        "ms": round(ms, 4), "rows_per_s": n_rows / (ms / 1e3),
+        "roofline": {"bound": "hbm", "achieved": round(load_bytes / (ms / 1e3) / 1e9, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(load_bytes / (ms / 1e3) / 1e9 / peak, 4),
+                     "algorithmic_bytes": int(load_bytes), "bytes_def": "257^3 vertex values read once + b written"}}
     u = torch.randn(n_rows, dtype=torch.float64, device="cuda")
     ms = _time_ms(lambda: api.apply(rules5, coef5, u), flush=flush)
+    fl_row, fl_def = apply_flops_per_row(rules5)
+    apply_bytes = (nv ** 3 + 3 * n_rows) * 8             # grid + u read once, y_M and y_K written
+    a_tf = fl_row * n_rows / (ms / 1e3) / 1e12
+    a_gbs = apply_bytes / (ms / 1e3) / 1e9
+    fp_frac, hbm_frac = a_tf / fp64_peak, a_gbs / peak
     # context: the time just to stream the assembled M and K (ELL) once at the copy peak
     stream_ms = n_rows * rules5.stencil * 8 * 2 / (peak * 1e9) * 1e3
-    out["operators"]["apply_MK_C5"] = {"ms": round(ms, 4), "rows_per_s": n_rows / (ms / 1e3),
-                                       "stream_assembled_ms": round(stream_ms, 3),
-                                       "note": "matrix-free y_M = M u and y_K = K u, nothing stored; "
-                                               "stream_assembled_ms = reading the 95 GB of assembled M, K once "
-                                               "at the copy peak (what any assembled SpMV would need)"}
+    out["operators"]["apply_MK_C5"] = {
+        "ms": round(ms, 4), "rows_per_s": n_rows / (ms / 1e3), "stream_assembled_ms": round(stream_ms, 3),
+        "roofline": {"bound": "fp64" if fp_frac >= hbm_frac else "hbm",
+                     "achieved": round(a_tf, 2) if fp_frac >= hbm_frac else round(a_gbs, 1),
+                     "peak": fp64_peak if fp_frac >= hbm_frac else peak,
+                     "unit": "TFLOP/s" if fp_frac >= hbm_frac else "GB/s",
+                     "frac": round(max(fp_frac, hbm_frac), 4),
+                     "fp64": {"achieved_tflops": round(a_tf, 2), "peak_tflops": fp64_peak, "peak_source": fp64_src,
+                              "frac": round(fp_frac, 4), "algorithmic_flops_per_row": fl_row, "flops_def": fl_def},
+                     "hbm": {"achieved_gbs": round(a_gbs, 1), "peak_gbs": peak, "frac": round(hbm_frac, 5),
+                             "algorithmic_bytes": int(apply_bytes)}},
+        "note": "matrix-free y_M = M u and y_K = K u, nothing stored; stream_assembled_ms = reading the 95 GB of "
+                "assembled M, K once at the copy peak (what any assembled SpMV would need)"}
     # the paper's own cost metric (context): basis evaluations for its 2D 100x100 test
     # problem, weighted Gaussian (this library's rules) vs the weighted Newton-Cotes point sets
     out["paper_eval_counts_2d_100x100_mass"] = {}
@@ -449,14 +604,6 @@ def run_extras(rules5, coef5, peak):
         out["paper_eval_counts_2d_100x100_mass"][f"p{pp}"] = {
             "gaussian": g, "newton_cotes": c, "ratio": round(c / g, 4),
             "paper_ratio": {2: 2.08, 3: 2.44}[pp], "interior_ratio": round({2: (13 / 9) ** 2, 3: (25 / 16) ** 2}[pp], 4)}
-    # peak microbenchmarks of this box, same session (tools/peaks.cu, built by build())
-    exe = os.path.join(ROOT, "tools", "peaks")
-    if os.path.exists(exe):
-        try:
-            r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
-            out["box_peaks"] = json.loads(r.stdout.strip().splitlines()[-1])
-        except Exception as e:          # the headline numbers do not depend on it
-            out["box_peaks"] = {"error": str(e)[:200]}
     return out
 
 
@@ -476,7 +623,7 @@ def run_e2e(args, cfg, rules, row_begin, row_end, ld, world, rank, local, nnz_al
                                   planes=hi - lo + 1)
         pin = wgq.PinnedArray(g.shape)
         pin.array[...] = g
-        coef = wgq.make_coeff({"kind": "grid"}, grid=_HostGrid(pin.array), plane0=lo)
+        coef = wgq.make_coeff({"kind": "grid"}, grid=wgq.HostGrid(pin.array), plane0=lo)
         h2d = g.nbytes
     else:
         coef = api.coefficient(inputs.coefficient(cfg["coeff"], d))
@@ -500,17 +647,6 @@ def run_e2e(args, cfg, rules, row_begin, row_end, ld, world, rank, local, nnz_al
         v.close()
     return {"value": value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "steps": args.e2e_steps, "api": "wgq_assemble_host (pinned host buffers, chunked 2-stream pipeline)"}
-
-
-class _HostGrid:
-    """Adapter so make_coeff can take a host numpy array for wgq_assemble_host."""
-
-    def __init__(self, arr):
-        self.arr = arr
-        self.shape = arr.shape
-
-    def data_ptr(self):
-        return self.arr.ctypes.data
 
 
 if __name__ == "__main__":

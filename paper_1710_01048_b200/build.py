@@ -29,8 +29,28 @@ def up_to_date():
     return all(os.path.getmtime(d) <= t for d in deps)
 
 
+def write_build_info():
+    """paper_1710_01048_b200/build_info.json: the git commit the library was built from (the GPU
+    box receives a snapshot without .git; bench.py reports it)."""
+    import json
+    import time
+    info = {"built": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime())}
+    try:
+        sha = subprocess.run(["git", "-C", ROOT, "rev-parse", "HEAD"], capture_output=True, text=True, timeout=10)
+        dirty = subprocess.run(["git", "-C", ROOT, "status", "--porcelain", "--untracked-files=no"],
+                               capture_output=True, text=True, timeout=10)
+        if sha.returncode == 0:
+            info["git_sha"] = sha.stdout.strip()
+            info["dirty"] = bool(dirty.stdout.strip())
+    except Exception:
+        pass
+    with open(os.path.join(PKG, "build_info.json"), "w") as f:
+        json.dump(info, f)
+
+
 def build(force=False, verbose=False):
     if not force and up_to_date():
+        write_build_info()
         return LIB
     objs = []
     os.makedirs(os.path.join(PKG, "build"), exist_ok=True)
@@ -45,6 +65,7 @@ def build(force=False, verbose=False):
         objs.append(obj)
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB] + objs + ["-lcudart"]
     subprocess.run(cmd, check=True)
+    write_build_info()
     # peak microbenchmarks (write-only HBM, copy, DFMA) used by bench.py's extras
     peaks_src = os.path.join(ROOT, "tools", "peaks.cu")
     if os.path.exists(peaks_src):                 # optional tool: a failure here never fails the build

@@ -27,6 +27,7 @@ int table_for(wgq_rules_s* R, RowTables* out, void* stream) {
     std::lock_guard<std::mutex> lock(R->mu);
     auto it = R->tables.find(dev);
     if (it == R->tables.end()) {
+        NvtxRange nvtx_("wgq_row_tables (one-time build)");
         RowTables T;
         int rc = build_row_tables(R, &T, stream);
         if (rc != WGQ_OK) return rc;
@@ -99,6 +100,13 @@ int assemble(wgq_rules_t R, const wgq_coeff_t* c, const wgq_out_t* M, const wgq_
 
 }  // namespace
 
+namespace wgq {
+int validate_coeff_range(const wgq_rules_s* R, const wgq_coeff_t* c, int64_t row_begin, int64_t row_end) {
+    wgq_out_t range{WGQ_ELL, row_begin, row_end, nullptr, 0, nullptr, nullptr};
+    return check_coeff(R, c, &range);
+}
+}  // namespace wgq
+
 extern "C" {
 
 const char* wgq_strerror(int code) {
@@ -117,6 +125,7 @@ const char* wgq_strerror(int code) {
 const char* wgq_version(void) { return "wgq 0.1 (sm_100a)"; }
 
 int wgq_build_rules_ex(int p, int64_t n_elems, int dim, int boundary_mode, wgq_rules_t* out) {
+    NvtxRange nvtx_("wgq_build_rules");
     if (!out) return WGQ_EINVAL;
     *out = nullptr;
     if (p != 2 && p != 3) return WGQ_EUNSUPPORTED;
@@ -195,23 +204,27 @@ int wgq_nnz(wgq_rules_t R, int64_t row_begin, int64_t row_end, int64_t* nnz) {
 }
 
 int wgq_assemble_mass(wgq_rules_t R, const wgq_coeff_t* c, const wgq_out_t* M, void* stream) {
+    NvtxRange nvtx_("wgq_assemble_mass");
     if (!M) return WGQ_EINVAL;
     return assemble(R, c, M, nullptr, stream);
 }
 
 int wgq_assemble_stiffness(wgq_rules_t R, const wgq_coeff_t* c, const wgq_out_t* K, void* stream) {
+    NvtxRange nvtx_("wgq_assemble_stiffness");
     if (!K) return WGQ_EINVAL;
     return assemble(R, c, nullptr, K, stream);
 }
 
 int wgq_assemble_mass_stiffness(wgq_rules_t R, const wgq_coeff_t* c, const wgq_out_t* M, const wgq_out_t* K,
                                 void* stream) {
+    NvtxRange nvtx_("wgq_assemble_mass_stiffness");
     if (!M || !K) return WGQ_EINVAL;
     return assemble(R, c, M, K, stream);
 }
 
 int wgq_assemble_load(wgq_rules_t R, const wgq_coeff_t* f, int64_t row_begin, int64_t row_end, double* b,
                       void* stream) {
+    NvtxRange nvtx_("wgq_assemble_load");
     if (!R || row_begin < 0 || row_end < row_begin || row_end > ipow(R->N, R->dim)) return WGQ_EINVAL;
     if (row_end > row_begin && !b) return WGQ_EINVAL;
     wgq_out_t range{};
@@ -227,6 +240,7 @@ int wgq_assemble_load(wgq_rules_t R, const wgq_coeff_t* f, int64_t row_begin, in
 
 int wgq_apply(wgq_rules_t R, const wgq_coeff_t* c, const double* u, int64_t u_row0, int64_t u_rows, int64_t row_begin,
               int64_t row_end, double* y_M, double* y_K, void* stream) {
+    NvtxRange nvtx_("wgq_apply");
     if (!R || row_begin < 0 || row_end < row_begin || row_end > ipow(R->N, R->dim)) return WGQ_EINVAL;
     if (row_end == row_begin) return WGQ_OK;
     if (!u || (!y_M && !y_K) || u_row0 < 0 || u_rows < 0) return WGQ_EINVAL;
@@ -260,6 +274,7 @@ int wgq_eval_counts(wgq_rules_t R, int kind, int64_t* gaussian, int64_t* newton_
 
 int wgq_csr_structure(wgq_rules_t R, int64_t row_begin, int64_t row_end, int64_t* row_ptr, int32_t* col_idx,
                       void* stream) {
+    NvtxRange nvtx_("wgq_csr_structure");
     if (!R || !row_ptr || row_begin < 0 || row_end < row_begin || row_end > ipow(R->N, R->dim)) return WGQ_EINVAL;
     if (row_end > row_begin && !col_idx) return WGQ_EINVAL;
     return launch_csr_structure(R, row_begin, row_end, row_ptr, col_idx, stream);
@@ -267,6 +282,7 @@ int wgq_csr_structure(wgq_rules_t R, int64_t row_begin, int64_t row_end, int64_t
 
 int wgq_generate_grid(int64_t n_elems, int dim, uint64_t seed, double sigma, int64_t plane0, int64_t planes,
                       double* grid, void* stream) {
+    NvtxRange nvtx_("wgq_generate_grid");
     if (!grid || n_elems < 1 || dim < 1 || dim > 3 || planes < 0 || plane0 < 0) return WGQ_EINVAL;
     if (dim == 1 && (plane0 != 0 || planes != n_elems + 1)) return WGQ_EINVAL;
     if (plane0 + planes > n_elems + 1) return WGQ_EINVAL;
@@ -275,6 +291,7 @@ int wgq_generate_grid(int64_t n_elems, int dim, uint64_t seed, double sigma, int
 }
 
 int wgq_row_moments(wgq_rules_t R, const wgq_out_t* A, double* out, void* stream) {
+    NvtxRange nvtx_("wgq_row_moments");
     if (!R || !out) return WGQ_EINVAL;
     int rc = check_out(R, A);
     if (rc != WGQ_OK) return rc;
@@ -283,6 +300,7 @@ int wgq_row_moments(wgq_rules_t R, const wgq_out_t* A, double* out, void* stream
 }
 
 int wgq_checksum(wgq_rules_t R, const wgq_out_t* A, unsigned long long* out_dev, void* stream) {
+    NvtxRange nvtx_("wgq_checksum");
     if (!R || !out_dev) return WGQ_EINVAL;
     int rc = check_out(R, A);
     if (rc != WGQ_OK) return rc;

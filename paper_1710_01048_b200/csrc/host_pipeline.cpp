@@ -42,11 +42,14 @@ extern "C" int wgq_host_free(void* ptr) { return cudaFreeHost(ptr) == cudaSucces
 
 extern "C" int wgq_assemble_host(wgq_rules_t R, const wgq_coeff_t* c, int64_t row_begin, int64_t row_end,
                                  double* M_host, double* K_host, int64_t ld, int64_t chunk_rows) {
+    NvtxRange nvtx_("wgq_assemble_host");
     if (!R || !c || (!M_host && !K_host) || row_begin < 0 || row_end < row_begin) return WGQ_EINVAL;
     int64_t stencil = 1;
     for (int q = 0; q < R->dim; ++q) stencil *= 2 * R->p + 1;
     if (ld < stencil) return WGQ_ERANGE;
     if (row_end == row_begin) return WGQ_OK;
+    // the descriptor must cover the whole range before anything is allocated or copied
+    if (int rc0 = validate_coeff_range(R, c, row_begin, row_end)) return rc0;
     Cleanup cl;
     if (cudaStreamCreateWithFlags(&cl.s[0], cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&cl.s[1], cudaStreamNonBlocking) != cudaSuccess)
@@ -61,7 +64,7 @@ extern "C" int wgq_assemble_host(wgq_rules_t R, const wgq_coeff_t* c, int64_t ro
         if (!c->grid) return WGQ_EINVAL;
         int64_t plane = 1;
         for (int q = 0; q < R->dim - 1; ++q) plane *= R->n + 1;
-        const size_t bytes = (size_t)(R->dim == 1 ? R->n + 1 : c->grid_planes * plane) * sizeof(double);
+        const size_t bytes = (size_t)c->grid_planes * plane * sizeof(double);   // plane = 1 in 1D
         if (cudaMalloc(&cl.dev[0], bytes) != cudaSuccess) return WGQ_ECUDA;
         if (cudaMemcpyAsync(cl.dev[0], c->grid, bytes, cudaMemcpyHostToDevice, comp) != cudaSuccess) return WGQ_ECUDA;
         dc.grid = (const double*)cl.dev[0];

@@ -10,7 +10,18 @@
 
 #include "wgq.h"
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace wgq {
+
+// NVTX range over a library call (SURVEY §5 tracing: rules, tables, grid generation, assembly,
+// operators); header-only NVTX3, a no-op unless a tool (nsys / ncu) is attached.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 constexpr int kMaxP = 3;
 constexpr int kMaxS = 2 * kMaxP + 1;   // stencil width per direction
@@ -119,6 +130,9 @@ int launch_sep_apply(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t
                      int64_t row_begin, int64_t row_end, double* yM, double* yK, void* stream);
 int launch_line_apply(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, const double* u,
                       int64_t u_row0, int64_t row_begin, int64_t row_end, double* yM, double* yK, void* stream);
+
+// api.cpp: the coefficient descriptor check of the assembly calls, for a row range
+int validate_coeff_range(const wgq_rules_s* R, const wgq_coeff_t* c, int64_t row_begin, int64_t row_end);
 
 // fourier2d.cu (2D FOURIER_LOGN, p = 3, rows of class I in both directions; C3)
 bool f2d_interior_applies(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c);

@@ -17,6 +17,45 @@ import torch.distributed as dist
 
 from . import api
 
+_p2p_ready = set()
+
+
+def _p2p(sends, recvs, group=None):
+    """Post the point-to-point transfers of one exchange together: ``sends`` / ``recvs`` are
+    lists of (tensor, peer).  One ``batch_isend_irecv`` (a ncclGroupStart/End group under
+    NCCL) so that two ranks sending to each other cannot deadlock on the per-pair NCCL stream
+    the way one-at-a-time isend/irecv can.  Under gloo (host transport) CUDA tensors are staged
+    through host memory.  The first P2P call on a group must be made by all its ranks (NCCL
+    communicator setup), so a barrier precedes it once per group."""
+    torch.cuda.nvtx.range_push("wgq halo exchange")
+    try:
+        _p2p_inner(sends, recvs, group)
+    finally:
+        torch.cuda.nvtx.range_pop()
+
+
+def _p2p_inner(sends, recvs, group):
+    key = id(group)
+    if key not in _p2p_ready:
+        dist.barrier(group=group)
+        _p2p_ready.add(key)
+    host = dist.get_backend(group) == "gloo"
+    staged = []
+    ops = []
+    for t, peer in sends:
+        src = t.cpu() if host and t.is_cuda else t.contiguous()
+        ops.append(dist.P2POp(dist.isend, src, peer, group))
+    for t, peer in recvs:
+        dst = torch.empty(t.shape, dtype=t.dtype) if host and t.is_cuda else t
+        staged.append((t, dst))
+        ops.append(dist.P2POp(dist.irecv, dst, peer, group))
+    if ops:
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+    for t, dst in staged:
+        if dst is not t:
+            t.copy_(dst)
+
 
 def owned_vertex_planes(n, N, dim, rank, world):
     """Vertex planes [v0, v1) of the slowest axis a rank owns when a user field is
@@ -48,7 +87,7 @@ def exchange_halo(owned, p, n, N, dim, group=None):
     lo, hi = need[rank]
     plane_shape = owned.shape[1:]
     out = torch.empty((max(hi - lo + 1, 0),) + tuple(plane_shape), dtype=owned.dtype, device=owned.device)
-    reqs = []
+    sends, recvs = [], []
     # receive: planes of [lo, hi] owned by other ranks
     for src in range(world):
         a, b = max(lo, own[src][0]), min(hi + 1, own[src][1])
@@ -57,7 +96,7 @@ def exchange_halo(owned, p, n, N, dim, group=None):
         if src == rank:
             out[a - lo:b - lo] = owned[a - own[rank][0]:b - own[rank][0]]
         else:
-            reqs.append(dist.irecv(out[a - lo:b - lo], src=src, group=group))
+            recvs.append((out[a - lo:b - lo], _peer(src, group)))
     # send: my owned planes other ranks need
     for dst in range(world):
         if dst == rank:
@@ -66,9 +105,8 @@ def exchange_halo(owned, p, n, N, dim, group=None):
         a, b = max(dlo, own[rank][0]), min(dhi + 1, own[rank][1])
         if a >= b:
             continue
-        reqs.append(dist.isend(owned[a - own[rank][0]:b - own[rank][0]].contiguous(), dst=dst, group=group))
-    for r in reqs:
-        r.wait()
+        sends.append((owned[a - own[rank][0]:b - own[rank][0]], _peer(dst, group)))
+    _p2p(sends, recvs, group)
     return out, lo
 
 
@@ -95,7 +133,7 @@ def exchange_u_halo(u_owned, p, N, dim, group=None):
     need = [needed_u_rows(p, N, dim, r, world) for r in range(world)]
     lo, hi = need[rank]
     out = torch.empty(max(hi - lo, 0), dtype=u_owned.dtype, device=u_owned.device)
-    reqs = []
+    sends, recvs = [], []
     for src in range(world):
         a, b = max(lo, own[src][0]), min(hi, own[src][1])
         if a >= b:
@@ -103,16 +141,15 @@ def exchange_u_halo(u_owned, p, N, dim, group=None):
         if src == rank:
             out[a - lo:b - lo] = u_owned[a - own[rank][0]:b - own[rank][0]]
         else:
-            reqs.append(dist.irecv(out[a - lo:b - lo], src=src, group=group))
+            recvs.append((out[a - lo:b - lo], _peer(src, group)))
     for dst in range(world):
         if dst == rank:
             continue
         a, b = max(need[dst][0], own[rank][0]), min(need[dst][1], own[rank][1])
         if a >= b:
             continue
-        reqs.append(dist.isend(u_owned[a - own[rank][0]:b - own[rank][0]].contiguous(), dst=dst, group=group))
-    for r in reqs:
-        r.wait()
+        sends.append((u_owned[a - own[rank][0]:b - own[rank][0]], _peer(dst, group)))
+    _p2p(sends, recvs, group)
     return out, lo
 
 
@@ -123,6 +160,11 @@ def apply_distributed(rules, coeff, u_owned, kinds=("mass", "stiffness"), group=
     b, e = api.slab_rows(rules.N, rules.dim, rank, world)
     u_ext, u0 = exchange_u_halo(u_owned, rules.p, rules.N, rules.dim, group)
     return api.apply(rules, coeff, u_ext, kinds, b, e, u_row0=u0, stream=stream)
+
+
+def _peer(r, group):
+    """Global rank of group rank r (P2POp takes global ranks)."""
+    return r if group is None else dist.get_global_rank(group, r)
 
 
 def reduce_checks(local, group=None):

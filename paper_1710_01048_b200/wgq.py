@@ -304,11 +304,43 @@ def wgq_checksum(rules, A, out, stream=None):
     _check("wgq_checksum", lib().wgq_checksum(rules.handle, ctypes.byref(A), out.data_ptr(), _stream(stream)))
 
 
+def _need_host(a, name, numel, writeable=True):
+    if a is None:
+        return
+    if not isinstance(a, np.ndarray):
+        raise TypeError(f"{name}: expected a numpy array")
+    if a.dtype != np.float64:
+        raise TypeError(f"{name}: expected dtype float64, got {a.dtype}")
+    if not a.flags["C_CONTIGUOUS"] or (writeable and not a.flags["WRITEABLE"]):
+        raise ValueError(f"{name}: expected a {'writeable ' if writeable else ''}C-contiguous array")
+    if a.size < numel:
+        raise ValueError(f"{name}: needs at least {numel} elements, has {a.size}")
+
+
 def wgq_assemble_host(rules, coeff, row_begin, row_end, M_host, K_host, ld, chunk_rows=0):
     """Blocking end-to-end call; M_host / K_host are numpy arrays (or None) [rows][ld]."""
+    rows = max(0, int(row_end) - int(row_begin))
+    _need_host(M_host, "M_host", rows * int(ld))
+    _need_host(K_host, "K_host", rows * int(ld))
+    g = coeff._keep[0] if coeff.kind == WGQ_COEF_GRID and coeff._keep else None
+    if g is not None and hasattr(g, "arr"):          # host grid slab: [grid_planes][plane]
+        plane = (rules.n + 1) ** (rules.dim - 1)
+        _need_host(g.arr, "grid", coeff.grid_planes * plane, writeable=False)
     ptr = (lambda a: a.ctypes.data if a is not None else None)
     _check("wgq_assemble_host", lib().wgq_assemble_host(rules.handle, ctypes.byref(coeff), row_begin, row_end,
                                                         ptr(M_host), ptr(K_host), ld, chunk_rows))
+
+
+class HostGrid:
+    """A host (numpy, float64, C-contiguous) GRID slab [planes][...] for wgq_assemble_host,
+    which copies it to the device itself; pass it to make_coeff in place of a device tensor."""
+
+    def __init__(self, arr):
+        self.arr = arr
+        self.shape = arr.shape
+
+    def data_ptr(self):
+        return self.arr.ctypes.data
 
 
 class PinnedArray:

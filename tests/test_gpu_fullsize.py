@@ -6,6 +6,8 @@ mesh, device-generated GRID field for C5); the oracle recomputes a sample of row
 match them (R12).  Properties that hold at any size are checked on ALL rows on the device:
 (K 1)_i = 0 (P9) and the 8-slab z-partition of C5 reproduces the one-GPU checksum exactly.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -178,3 +180,66 @@ def test_c5_whole_lines_every_class():
     finally:
         out.clear()
         torch.cuda.empty_cache()
+
+
+_P9_JOBS = None
+
+
+def _p9_job(i):
+    from threadpoolctl import threadpool_limits
+    threadpool_limits(1)
+    p, n, d, rows, desc, grid, plane0 = _P9_JOBS[i]
+    return oasm.row_weight_sums(p, n, d, rows, desc, grid=grid, plane0=plane0)
+
+
+def test_c5_full_scale_p9_identities():
+    """SURVEY §8(c) P9 at the full C5 size (every entry is integrated exactly):
+    on EVERY row of the z-planes {0, 1, 3, 6, N-1} and two seeded interior planes (all row
+    classes), the GPU matrices' row moments (M 1, M g^a, K 1, K g^a; wgq_row_moments) equal the
+    oracle's weighted sums sum_k W^M, sum_k W^M x^a, 0, sum_k W^{K,a} (oracle.assemble.row_weight_sums,
+    from the rules and c alone, on its own vertex-plane slab) to 1e-13 x the row maximum."""
+    import multiprocessing as mp
+
+    from paper_1710_01048_b200 import wgq
+    global _P9_JOBS
+    cfg, rules, desc, out = assemble_config("C5")
+    p, n, d = cfg["p"], cfg["n"], cfg["dim"]
+    N = rules.N
+    P = N * N
+    rng = np.random.default_rng(449)
+    planes = [0, 1, 3, 6, N - 1] + sorted(int(z) for z in rng.choice(np.arange(2 * p + 1, N - 2 * p - 1), 2, replace=False))
+    try:
+        gpu = {}
+        for z in planes:
+            lo, hi = z * P, (z + 1) * P
+            for k in ("mass", "stiffness"):
+                m = torch.empty((P, 1 + d), dtype=torch.float64, device="cuda")
+                wgq.wgq_row_moments(rules, wgq.make_out(out[k][lo:hi], lo, hi), m)
+                gpu[(z, k)] = (m.cpu().numpy(), out[k][lo:hi].abs().amax(dim=1).cpu().numpy())
+    finally:
+        out.clear()
+        torch.cuda.empty_cache()
+    jobs, where = [], []
+    for z in planes:
+        gl, gh = max(0, z - p), min(n, z + 1)
+        slab = inputs.lognormal_grid(n, seed=desc["seed"], sigma=desc["sigma"], plane0=gl, planes=gh - gl + 1)
+        rows = np.arange(z * P, (z + 1) * P)
+        for blk in np.array_split(rows, 24):
+            jobs.append((p, n, d, blk, desc, slab, gl))
+            where.append((z, blk[0] - z * P, len(blk)))
+    _P9_JOBS = jobs
+    oasm.tables_1d(p, n)
+    with mp.get_context("fork").Pool(os.cpu_count() or 1) as pool:
+        res = pool.map(_p9_job, range(len(jobs)), chunksize=1)
+    worst = {"M1": 0.0, "Mg": 0.0, "K1": 0.0, "Kg": 0.0}
+    for (z, off, cnt), (m1, mx, kx) in zip(where, res):
+        mm, sM = gpu[(z, "mass")]
+        km, sK = gpu[(z, "stiffness")]
+        sl = slice(off, off + cnt)
+        worst["M1"] = max(worst["M1"], float(np.max(np.abs(mm[sl, 0] - m1) / sM[sl])))
+        worst["K1"] = max(worst["K1"], float(np.max(np.abs(km[sl, 0]) / sK[sl])))
+        for a in range(d):
+            worst["Mg"] = max(worst["Mg"], float(np.max(np.abs(mm[sl, 1 + a] - mx[:, a]) / sM[sl])))
+            worst["Kg"] = max(worst["Kg"], float(np.max(np.abs(km[sl, 1 + a] - kx[:, a]) / sK[sl])))
+    print("C5 P9 worst relative to row max:", worst, "planes", planes)
+    assert worst["M1"] < 1e-13 and worst["Mg"] < 1e-13 and worst["Kg"] < 1e-13 and worst["K1"] < 1e-12, worst

@@ -197,3 +197,45 @@ def test_fourier2d_interior_kernel(n):
             for r in range(lo, hi):
                 cols = oasm.ell_columns(p, n, d, r)
                 assert np.array_equal(v[rpn[r - lo]:rpn[r - lo + 1]], g[k][r][cols >= 0]), (r, k)
+
+
+@pytest.mark.parametrize("p,n", [(2, 7), (3, 6)])
+def test_gl_boundary_mode_grid_3d(p, n):
+    """WGQ_BND_GL ("or one can use standard Gauss rules there") with the GRID
+    coefficient in 3D: the line kernel (ELL, compact and padded ld), its CSR runs, the load
+    vector and the matrix-free product against the oracle in mode "gl"."""
+    from paper_1710_01048_b200 import api, wgq
+    d = 3
+    N = n + p
+    rows = np.arange(N ** d)
+    desc = {"kind": "grid", "seed": 23, "sigma": 0.5}
+    grid = inputs.lognormal_grid(n, seed=23)
+    ref = oasm.assemble_rows(p, n, d, rows, desc, grid=grid, mode="gl")
+    sc = oasm.assemble_rows(p, n, d, rows, desc, grid=grid, mode="gl", absolute=True)
+    s3 = (2 * p + 1) ** 3
+    for ld in (None, s3 + 3):
+        g, _ = gpu_assemble(p, n, d, desc, bnd=wgq.WGQ_BND_GL, host_grid=grid, ld=ld)
+        for k in ("mass", "stiffness"):
+            compare(g[k][:, :s3], ref[k], ("gl-grid", p, n, ld, k), sc[k])
+    rules = wgq.Rules(p, n, d, wgq.WGQ_BND_GL)
+    c = api.coefficient(desc, torch.from_numpy(grid).cuda(), 0)
+    rp, ci, vals = api.assemble_csr(rules, c)
+    b = api.assemble_load(rules, c)
+    u = np.random.default_rng(3).standard_normal(N ** d)
+    y = api.apply(rules, c, torch.from_numpy(u).cuda())
+    torch.cuda.synchronize()
+    rpn = rp.cpu().numpy()
+    for k in ("mass", "stiffness"):
+        v = vals[k].cpu().numpy()
+        for r in rows:
+            cols = oasm.ell_columns(p, n, d, r)
+            assert np.array_equal(v[rpn[r]:rpn[r + 1]], g[k][r][:s3][cols >= 0]), (r, k)
+    from oracle import operators as oops
+    bref = oops.load_rows(p, n, d, rows, desc, grid=grid, mode="gl")
+    compare(b.cpu().numpy(), bref, ("gl-grid load", p, n), rowwise=False)
+    for k in ("mass", "stiffness"):
+        yref = oops.apply_rows(p, n, d, rows, desc, u, k, grid=grid, mode="gl")
+        scale = np.array([np.abs(sc[k][i][oasm.ell_columns(p, n, d, r) >= 0]) @
+                          np.abs(u[oasm.ell_columns(p, n, d, r)[oasm.ell_columns(p, n, d, r) >= 0]])
+                          for i, r in enumerate(rows)])
+        compare(y[k].cpu().numpy(), yref, ("gl-grid apply", p, n, k), scale, rowwise=False)
