@@ -763,163 +763,156 @@ __global__ void __launch_bounds__(256) k_load_grid_line(const GenericArgs a, con
     }
 }
 
-// 3D GRID load vector, z-sliding: a block owns a T x T tile of (i1, i2) and a
-// run of kLZC planes i3; b = sum_{vz,vy,vx} PW_z PW_y PW_x g is contracted z -> y -> x in
-// shared memory from a ring of the tile's vertex planes (T + p + 1 square, loaded once per
-// plane with cp.async kLZA planes ahead of the window), so every vertex value is read from
-// global memory about once per tile instead of once per (row, vz) — the same sum as k_load,
-// reordered.  Each thread's roles (in-plane load offsets, y- and x-pass weights) are fixed per
-// block and kept in registers (T = 16: 128 threads, 128 registers, 4 blocks per SM; forcing 5-6
-// blocks spills and is slower).
-#ifndef WGQ_LZT
-#define WGQ_LZT 16
-#endif
-#ifndef WGQ_LZA
-#define WGQ_LZA 3
-#endif
-constexpr int kLZT = WGQ_LZT;   // output tile edge (rows i1, i2)
-constexpr int kLZA = WGQ_LZA;   // vertex planes loaded ahead of the window
-static_assert(kLZA >= 1 && kLZA <= 7, "cp.async groups ahead of the window");
-constexpr int kLZC = 32;        // planes i3 per block
-constexpr int kLZThreads = kLZT >= 32 ? 256 : 128;
+// 3D GRID load vector: b = sum_{vz,vy,vx} PW_z PW_y PW_x g (vertex
+// projection, as k_load), contracted y -> z -> x (the same sum, reordered).  A block owns
+// kLTW x kLTLW lines i2 (kLTLW consecutive lines per warp) x W = 32 - (p + 1) rows i1 and
+// slides along i3 over kLTZ output planes.  The tile's vertex planes (lines + p + 1 rows x 32
+// columns, one column per lane) stream through a shared-memory ring, loaded with cp.async kLTA
+// planes ahead; when plane z arrives each warp contracts it over y for its lines at its column
+// (q(z), into a per-line q ring in shared memory), and every output plane whose window ends at
+// z is finished: s = sum_vz PW_z q (z) per column, then sum_vx PW_x s over each row's window by
+// shuffles (x).  One block barrier per vertex plane; each vertex value is read from global
+// memory once per tile.
+constexpr int kLTW = 8;        // warps per block
+constexpr int kLTLW = 2;       // lines per warp
+constexpr int kLTZ = 32;       // output planes per block
+constexpr int kLTA = 4;        // vertex planes in flight ahead
+constexpr int kLTR = 8;        // ring depth, a power of two >= p + 2 + kLTA - 1 (a plane's q stays while its window is open)
+static_assert(kLTR >= kMaxP + 2 + kLTA - 1 && (kLTR & (kLTR - 1)) == 0, "load ring depth");
 
 template <int P>
-__global__ void __launch_bounds__(kLZThreads) k_load_grid_zslide(const GenericArgs a, const double* PW, double* b) {
-    constexpr int V = P + 2, T = kLZT, E = T + V - 1, RZ = V + kLZA;   // ring: window + kLZA ahead
-    constexpr int NT = kLZThreads;
-    constexpr int EL = (E * E + NT - 1) / NT, YL = (T * E + NT - 1) / NT, XL = (T * T + NT - 1) / NT;
-    extern __shared__ __align__(16) double zs[];
-    double* ring = zs;                      // [RZ][E][E] vertex planes (slot = plane % RZ)
-    double* hz = ring + RZ * E * E;         // [E][E]  z-contracted
-    double* gy = hz + E * E;                // [T][E]  y-contracted
-    const int tid = threadIdx.x;
-    const int64_t N = a.N, n = a.n, nv = n + 1;
-    const int64_t x0 = (int64_t)blockIdx.x * T, y0 = (int64_t)blockIdx.y * T;
-    const int64_t c0 = max((int64_t)0, x0 - P), r0 = max((int64_t)0, y0 - P);
-    const int64_t pr = N * N;
-    const int64_t zlo_all = a.row_begin / pr, zhi_all = (a.row_end - 1) / pr;
-    const int64_t z_lo = zlo_all + (int64_t)blockIdx.z * kLZC;
-    const int64_t z_hi = min(zhi_all + 1, z_lo + kLZC);
+__global__ void __launch_bounds__(kLTW * 32) k_load_grid_tile(const GenericArgs a, const double* PW, double* b) {
+    constexpr int V = P + 2, W = 32 - V + 1, LT = kLTW * kLTLW, EY = LT + V - 1, TILE = EY * 32;
+    constexpr int NT = kLTW * 32, LPT = (TILE + NT - 1) / NT;
+    extern __shared__ __align__(16) double lt_smem[];
+    double* raw = lt_smem;                                      // [kLTR][EY][32] vertex planes
+    double* qr = raw + kLTR * TILE;                             // [LT][kLTR][32] y-contracted planes per line
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // 32-bit indices: the launcher requires N^3 < 2^31 (so (n + 1)^3 too)
+    const int N = (int)a.N, n = (int)a.n, nv = n + 1;
+    const int64_t pr = (int64_t)N * N;
+    const int x0 = blockIdx.x * W, y0 = blockIdx.y * LT;
+    const int c0 = x0 - P, by0 = max(0, y0 - P);
+    const int zlo_all = (int)(a.row_begin / pr), zhi_all = (int)((a.row_end - 1) / pr);
+    const int z_lo = zlo_all + blockIdx.z * kLTZ;
+    const int z_hi = min(zhi_all + 1, z_lo + kLTZ);
     if (z_lo >= z_hi) return;
-    // fixed per-thread roles (the same elements every plane step):
-    //   loads: patch elements e = tid + NT m -> in-plane offset (or -1 outside the mesh)
-    int64_t loff[EL];
+    // planes: [zs, ze] = the windows of the outputs [z_lo, z_hi)
+    const int zs = max(0, z_lo - P);
+    const int ze = min(n, max(V - 1, z_hi));                     // last output z_hi - 1 needs z_hi
+    const int zg0 = (int)a.coef.plane0, zg1 = (int)(a.coef.plane0 + a.coef.planes);
+    // load roles: tile element e = tid + NT m -> (row by0 + e / 32, column c0 + e % 32)
+    int goff[LPT];
+    uint32_t sdst[LPT];
 #pragma unroll
-    for (int m = 0; m < EL; ++m) {
+    for (int m = 0; m < LPT; ++m) {
         const int e = tid + NT * m;
-        const int64_t y = r0 + e / E, x = c0 + e % E;
-        loff[m] = (e < E * E && y <= n && x <= n) ? y * nv + x : -1;
+        const int y = by0 + e / 32, x = c0 + e % 32;
+        goff[m] = (e < TILE && y <= n && x >= 0 && x <= n) ? y * nv + x : -1;
+        sdst[m] = (uint32_t)__cvta_generic_to_shared(raw + (e < TILE ? e : 0));
     }
-    //   y pass: (j, c) -> window start row in hz and the row's vertex weights
-    int yj[YL], ystart[YL];
-    double wy[YL][V];
-#pragma unroll
-    for (int m = 0; m < YL; ++m) {
-        const int e = tid + NT * m;
-        const int j = e / E;
-        const int64_t i2 = y0 + j;
-        yj[m] = (e < T * E && i2 < N) ? 1 : 0;
-        ystart[m] = (int)(max((int64_t)0, i2 - P) - r0) * E + e % E;
-#pragma unroll
-        for (int v = 0; v < V; ++v) {
-            const int64_t yy = max((int64_t)0, i2 - P) - r0 + v;
-            wy[m][v] = (yj[m] && yy < E) ? PW[i2 * kMaxV + v] : 0.0;
-        }
-    }
-    //   x pass: (j, i) -> gy offset, row offset within a plane of rows, weights
-    int xg[XL];
-    int64_t xrow[XL];
-    double wx[XL][V];
-#pragma unroll
-    for (int m = 0; m < XL; ++m) {
-        const int e = tid + NT * m;
-        const int j = e / T, i = e % T;
-        const int64_t i1 = x0 + i, i2 = y0 + j;
-        const bool ok = e < T * T && i1 < N && i2 < N;
-        const int cc0 = (int)(max((int64_t)0, i1 - P) - c0);
-        xg[m] = j * E + cc0;
-        xrow[m] = ok ? i2 * N + i1 : -1;
-#pragma unroll
-        for (int v = 0; v < V; ++v) wx[m][v] = (ok && cc0 + v < E) ? PW[i1 * kMaxV + v] : 0.0;
-    }
-    const int64_t zg0 = a.coef.plane0, zg1 = a.coef.plane0 + a.coef.planes;
-    auto issue_plane = [&](int64_t z) {      // one commit group per plane (empty past the mesh)
-        double* dst = ring + (int)(z % RZ) * (E * E);
-        if (z <= n) {
+    const int plane_el = nv * nv;
+    auto issue = [&](int z) {                                    // one commit group per plane
+        if (z <= ze) {
+            const uint32_t so = (uint32_t)((z & (kLTR - 1)) * TILE * sizeof(double));
             const bool zok = z >= zg0 && z < zg1;
-            const double* gz = a.coef.grid + (z - zg0) * nv * nv;
+            const double* gz = a.coef.grid + (int64_t)(z - zg0) * plane_el;
 #pragma unroll
-            for (int m = 0; m < EL; ++m) {
-                const int e = tid + NT * m;
-                if (e >= E * E) break;
-                const bool ok = zok && loff[m] >= 0;
-                const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + e);
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(ok ? gz + loff[m] : a.coef.grid),
-                             "r"(ok ? 8 : 0)
+            for (int m = 0; m < LPT; ++m) {
+                if (tid + NT * m >= TILE) break;
+                const bool ok = zok && goff[m] >= 0;
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sdst[m] + so),
+                             "l"(ok ? gz + goff[m] : a.coef.grid), "r"(ok ? 8 : 0)
                              : "memory");
             }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    // planes needed by i3: [bz, bz + V - 1], bz = max(0, i3 - P); loaded in order, kLZA ahead
-    int64_t next = max((int64_t)0, z_lo - P);
-    const int64_t first = next;
-    while (next < first + RZ) issue_plane(next++);
-    for (int64_t i3 = z_lo; i3 < z_hi; ++i3) {
-        const int64_t bz = max((int64_t)0, i3 - P);
-        switch ((int)min((int64_t)kLZA, next - 1 - (bz + V - 1))) {   // groups beyond the window may fly
-            case 7: asm volatile("cp.async.wait_group 7;" ::: "memory"); break;
-            case 6: asm volatile("cp.async.wait_group 6;" ::: "memory"); break;
-            case 5: asm volatile("cp.async.wait_group 5;" ::: "memory"); break;
-            case 4: asm volatile("cp.async.wait_group 4;" ::: "memory"); break;
-            case 3: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
-            case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
-            case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
-            default: asm volatile("cp.async.wait_group 0;" ::: "memory");
+    // this warp's lines i2 = y0 + kLTLW warp + l: rows by_l .. by_l + V - 1 of the tile
+    // (consecutive lines: by_l = by_0 + l except near the mesh start), weights wy[l][v] at the
+    // row offset v + (by_l - by_0) of the warp's row window (zero elsewhere)
+    constexpr int YW = V + kLTLW - 1;                             // rows of the warp's window
+    const int i2w = y0 + kLTLW * warp;
+    const int byw = max(0, i2w - P);
+    double wy[kLTLW][YW];
+    bool lok[kLTLW];
+#pragma unroll
+    for (int l = 0; l < kLTLW; ++l) {
+        const int i2 = i2w + l;
+        lok[l] = i2 < N;
+        const int d = max(0, i2 - P) - byw;
+#pragma unroll
+        for (int v = 0; v < YW; ++v) {
+            const int vv = v - d;
+            wy[l][v] = (lok[l] && vv >= 0 && vv < V && byw + v <= n) ? __ldg(PW + i2 * kMaxV + vv) : 0.0;
         }
-        __syncthreads();
-        const double* rp[V];
-        double pwz[V];
+    }
+    // x: lane = vertex column c0 + lane; lanes < W also own row i1 = x0 + lane
+    const int i1 = x0 + lane;
+    const bool xok = lane < W && i1 < N;
+    const int off = xok ? max(0, i1 - P) - c0 : 0;
+    double wx[V];
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
-            rp[v] = ring + (int)((bz + v) % RZ) * (E * E);
-            pwz[v] = bz + v <= n ? PW[i3 * kMaxV + v] : 0.0;
+    for (int v = 0; v < V; ++v) wx[v] = xok ? __ldg(PW + i1 * kMaxV + v) : 0.0;
+    double* q = qr + (kLTLW * warp) * kLTR * 32 + lane;          // q[l][slot] at q[(l kLTR + slot) 32]
+    const double* rl = raw + (byw - by0) * 32 + lane;
+    double* bl = b + ((int64_t)i2w * N + i1 - a.row_begin);      // row (i3 = 0, line i2w) of this lane
+    // weights of a class-I plane (any i3 in [2p, N-1-2p]; all such rows share them) and whether
+    // every row of the block lies in the slab
+    double wzi[V];
+    const int i3i = min(2 * P, N - 1);
+#pragma unroll
+    for (int v = 0; v < V; ++v) wzi[v] = __ldg(PW + i3i * kMaxV + v);
+    const bool all_in = (int64_t)z_lo * pr >= a.row_begin && (int64_t)z_hi * pr <= a.row_end;
+    for (int k = 0; k < kLTA; ++k) issue(zs + k);
+    for (int z = zs; z <= ze; ++z) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(kLTA - 1) : "memory");
+        __syncthreads();                                         // plane z landed; slot of z - kLTR + kLTA free
+        issue(z + kLTA);
+        // y stage of plane z at this lane's column, for each line of the warp
+        const int sl = z & (kLTR - 1);
+        const double* rz = rl + sl * TILE;
+        double g[YW];
+#pragma unroll
+        for (int v = 0; v < YW; ++v) g[v] = rz[v * 32];
+#pragma unroll
+        for (int l = 0; l < kLTLW; ++l) {
+            double qz = 0.0;
+#pragma unroll
+            for (int v = 0; v < YW; ++v) qz = fma(wy[l][v], g[v], qz);
+            q[(l * kLTR + sl) * 32] = qz;
         }
+        // the outputs whose window [bz, bz + V - 1] (clipped to the mesh) ends at plane z,
+        // last(i3) = min(n, max(V - 1, i3 + 1)): i3 = z - 1 in the steady state, [0, P] at
+        // z = V - 1, and every remaining output at the last plane
+        int o0 = z - 1, o1 = z - 1;
+        if (z == ze) o0 = z <= V - 1 ? 0 : z - 1, o1 = z_hi - 1;
+        else if (z == V - 1) o0 = 0, o1 = P;
+        else if (z < V - 1) o1 = o0 - 1;                         // none yet
+        o0 = max(o0, z_lo);
+        o1 = min(o1, z_hi - 1);
+        for (int i3 = o0; i3 <= o1; ++i3) {
+            const int bz = max(0, i3 - P);
+            double wz[V];
+            const bool interior = i3 >= 2 * P && i3 <= N - 1 - 2 * P;   // class-I plane: the shared weights
 #pragma unroll
-        for (int m = 0; m < EL; ++m) {
-            const int e = tid + NT * m;
-            if (e >= E * E) break;
-            double s = 0.0;
+            for (int v = 0; v < V; ++v) wz[v] = interior ? wzi[v] : __ldg(PW + i3 * kMaxV + v);
+            const int64_t rowz = i3 * pr;
+            const bool rin = all_in || (rowz + (int64_t)i2w * N + x0 >= a.row_begin &&
+                                        rowz + (int64_t)(i2w + kLTLW - 1) * N + x0 + W <= a.row_end);
 #pragma unroll
-            for (int vz = 0; vz < V; ++vz) s = fma(pwz[vz], rp[vz][e], s);
-            hz[e] = s;
-        }
-        __syncthreads();
-        // once hz is formed, slots of planes below the next window are free: refill them
-        if (i3 + 1 < z_hi) {
-            const int64_t bz1 = max((int64_t)0, i3 + 1 - P);
-            while (next - RZ < bz1) issue_plane(next++);
-        }
+            for (int l = 0; l < kLTLW; ++l) {
+                double s = 0.0;
 #pragma unroll
-        for (int m = 0; m < YL; ++m) {
-            const int e = tid + NT * m;
-            if (e >= T * E) break;
-            double s = 0.0;
+                for (int v = 0; v < V; ++v) s = fma(wz[v], q[(l * kLTR + ((bz + v) & (kLTR - 1))) * 32], s);
+                double acc = 0.0;
 #pragma unroll
-            for (int vy = 0; vy < V; ++vy) s = fma(wy[m][vy], hz[min(ystart[m] + vy * E, E * E - 1)], s);
-            gy[e] = s;
-        }
-        __syncthreads();
-        const int64_t plane_row = i3 * pr - a.row_begin;
-#pragma unroll
-        for (int m = 0; m < XL; ++m) {
-            if (xrow[m] < 0) continue;
-            const int64_t r = plane_row + xrow[m];
-            if (r < 0 || r >= a.row_end - a.row_begin) continue;
-            double s = 0.0;
-#pragma unroll
-            for (int vx = 0; vx < V; ++vx) s = fma(wx[m][vx], gy[min(xg[m] + vx, T * E - 1)], s);
-            b[r] = s;
+                for (int v = 0; v < V; ++v) acc = fma(wx[v], __shfl_sync(0xffffffffu, s, (off + v) & 31), acc);
+                if (xok && lok[l]) {
+                    const int64_t row = rowz + (int64_t)(i2w + l) * N + i1;
+                    if (rin || (row >= a.row_begin && row < a.row_end)) bl[rowz + (int64_t)l * N] = acc;
+                }
+            }
         }
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -931,17 +924,18 @@ int launch_load_pd(const GenericArgs& a, const double* PW, double* b, cudaStream
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t rows = a.row_end - a.row_begin;
-    if (D == 3 && a.coef.kind == WGQ_COEF_GRID) {
+    if (D == 3 && a.coef.kind == WGQ_COEF_GRID && a.N * a.N * a.N < ((int64_t)1 << 31)) {
         const int64_t pr = a.N * a.N;
         const int64_t planes = (a.row_end - 1) / pr - a.row_begin / pr + 1;
-        constexpr int V = P + 2, E = kLZT + V - 1;
-        const size_t smem = (size_t)((V + kLZA) * E * E + E * E + kLZT * E) * sizeof(double);
-        if (cudaFuncSetAttribute(k_load_grid_zslide<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        constexpr int W = 32 - (P + 2) + 1;
+        constexpr int LT = kLTW * kLTLW, TILE = (LT + P + 1) * 32;
+        const size_t smem = (size_t)(kLTR * TILE + LT * kLTR * 32) * sizeof(double);
+        if (cudaFuncSetAttribute(k_load_grid_tile<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
             cudaSuccess)
             return WGQ_ECUDA;
-        const dim3 g((unsigned)((a.N + kLZT - 1) / kLZT), (unsigned)((a.N + kLZT - 1) / kLZT),
-                     (unsigned)((planes + kLZC - 1) / kLZC));
-        k_load_grid_zslide<P><<<g, kLZThreads, smem, st>>>(a, PW, b);
+        const dim3 g((unsigned)((a.N + W - 1) / W), (unsigned)((a.N + LT - 1) / LT),
+                     (unsigned)((planes + kLTZ - 1) / kLTZ));
+        k_load_grid_tile<P><<<g, kLTW * 32, smem, st>>>(a, PW, b);
         return cudaGetLastError() == cudaSuccess ? WGQ_OK : WGQ_ECUDA;
     }
     if (D >= 2 && a.coef.kind == WGQ_COEF_GRID) {
