@@ -162,10 +162,6 @@ void wgq_free_rules(wgq_rules_t R) {
         cudaSetDevice(kv.first);
         free_row_tables(&kv.second);
     }
-    for (auto& kv : R->shells) {
-        cudaSetDevice(std::get<0>(kv.first));
-        if (kv.second.first) cudaFree(kv.second.first);
-    }
     for (auto& kv : R->sep_vectors) {
         cudaSetDevice(kv.first[0]);
         cudaFree(kv.second);

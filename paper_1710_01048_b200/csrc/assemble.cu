@@ -977,43 +977,78 @@ GenericArgs base_args(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_
 
 }  // namespace
 
-int shell_rows_2d(wgq_rules_s* R, int64_t row_begin, int64_t row_end, const int64_t** rows, int64_t* count) {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return WGQ_ECUDA;
-    std::lock_guard<std::mutex> lock(R->mu);
-    const auto key = std::make_tuple(dev, row_begin, row_end);
-    auto it = R->shells.find(key);
-    if (it == R->shells.end()) {
-        // 1D rows whose rule has more than 4 nodes (the GL-fallback boundary classes, R1)
-        std::vector<int64_t> wide;
-        for (int64_t r = 0; r < R->N; ++r) {
-            const int cls = r < R->p ? (int)r : (r >= R->n ? (int)(R->n + R->p - 1 - r) : R->p);
-            if (R->rules[WGQ_MASS][cls].m > 4 || R->rules[WGQ_STIFFNESS][cls].m > 4) wide.push_back(r);
+// The 2D shell rows of [row_begin, row_end): rows whose line i2 or column i1 is a "wide" 1D row
+// (a GL-fallback boundary class with more than 4 nodes, R1), in row order.  Per line l the rows
+// are the whole line (wide l) or its wide columns; with the nw <= 2p sorted wide indices w_k the
+// count and position of every row are closed forms, so the list is generated on the device into
+// stream-ordered scratch (no per-range cache, no host copy: graph-capturable).
+struct ShellDesc {
+    int64_t N, rb, re, l0, l1;
+    int nw;
+    int64_t w[2 * kMaxP];
+};
+
+__host__ __device__ inline bool shell_is_wide(const ShellDesc& d, int64_t l) {
+    for (int k = 0; k < d.nw; ++k)
+        if (d.w[k] == l) return true;
+    return false;
+}
+// rows of line l inside the range
+__host__ __device__ inline int64_t shell_line_count(const ShellDesc& d, int64_t l) {
+    const int64_t a = l * d.N > d.rb ? l * d.N : d.rb, b = (l + 1) * d.N < d.re ? (l + 1) * d.N : d.re;
+    if (b <= a) return 0;
+    if (shell_is_wide(d, l)) return b - a;
+    int64_t c = 0;
+    for (int k = 0; k < d.nw; ++k) c += (l * d.N + d.w[k] >= a && l * d.N + d.w[k] < b);
+    return c;
+}
+// list position of line l's first row: count(l0) + full lines strictly between (N or nw rows)
+__host__ __device__ inline int64_t shell_line_start(const ShellDesc& d, int64_t l) {
+    if (l <= d.l0) return 0;
+    int64_t wide_between = 0;
+    for (int k = 0; k < d.nw; ++k) wide_between += (d.w[k] > d.l0 && d.w[k] < l);
+    return shell_line_count(d, d.l0) + (l - d.l0 - 1) * d.nw + wide_between * (d.N - d.nw);
+}
+
+__global__ void k_shell_rows(const ShellDesc d, int64_t* out) {
+    const int64_t l = d.l0 + blockIdx.y;
+    if (l > d.l1) return;
+    const int64_t a = l * d.N > d.rb ? l * d.N : d.rb, b = (l + 1) * d.N < d.re ? (l + 1) * d.N : d.re;
+    const int64_t base = shell_line_start(d, l);
+    if (shell_is_wide(d, l)) {
+        for (int64_t r = a + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < b; r += (int64_t)gridDim.x * blockDim.x)
+            out[base + (r - a)] = r;
+    } else if (blockIdx.x == 0 && threadIdx.x == 0) {
+        int64_t c = 0;
+        for (int k = 0; k < d.nw; ++k) {
+            const int64_t r = l * d.N + d.w[k];
+            if (r >= a && r < b) out[base + c++] = r;
         }
-        std::vector<int64_t> shell;
-        const int64_t N = R->N;
-        for (int64_t i2 = row_begin / N; !wide.empty() && i2 <= (row_end - 1) / N; ++i2) {
-            const bool w2 = std::find(wide.begin(), wide.end(), i2) != wide.end();
-            auto add = [&](int64_t i1) {
-                const int64_t row = i2 * N + i1;
-                if (row >= row_begin && row < row_end) shell.push_back(row);
-            };
-            if (w2)
-                for (int64_t i1 = 0; i1 < N; ++i1) add(i1);
-            else
-                for (int64_t i1 : wide) add(i1);
-        }
-        int64_t* d = nullptr;
-        if (!shell.empty()) {
-            if (cudaMalloc((void**)&d, shell.size() * sizeof(int64_t)) != cudaSuccess) return WGQ_ENOMEM;
-            if (cudaMemcpy(d, shell.data(), shell.size() * sizeof(int64_t), cudaMemcpyHostToDevice) != cudaSuccess)
-                return WGQ_ECUDA;
-        }
-        it = R->shells.emplace(key, std::make_pair(d, (int64_t)shell.size())).first;
     }
-    *rows = it->second.first;
-    *count = it->second.second;
-    return WGQ_OK;
+}
+
+int shell_rows_2d(const wgq_rules_s* R, int64_t row_begin, int64_t row_end, cudaStream_t st, int64_t** rows,
+                  int64_t* count) {
+    *rows = nullptr;
+    *count = 0;
+    ShellDesc d{};
+    d.N = R->N;
+    d.rb = row_begin;
+    d.re = row_end;
+    for (int64_t r = 0; r < R->N; ++r) {
+        const int cls = r < R->p ? (int)r : (r >= R->n ? (int)(R->n + R->p - 1 - r) : R->p);
+        if ((R->rules[WGQ_MASS][cls].m > 4 || R->rules[WGQ_STIFFNESS][cls].m > 4) && d.nw < 2 * kMaxP) d.w[d.nw++] = r;
+    }
+    if (d.nw == 0 || row_end <= row_begin) return WGQ_OK;
+    d.l0 = row_begin / R->N;
+    d.l1 = (row_end - 1) / R->N;
+    const int64_t total = d.l1 > d.l0 ? shell_line_start(d, d.l1) + shell_line_count(d, d.l1) : shell_line_count(d, d.l0);
+    if (total == 0) return WGQ_OK;
+    if (cudaMallocAsync((void**)rows, (size_t)total * sizeof(int64_t), st) != cudaSuccess) return WGQ_ENOMEM;
+    const dim3 g((unsigned)((R->N + 255) / 256), (unsigned)(d.l1 - d.l0 + 1));
+    k_shell_rows<<<g, 256, 0, st>>>(d, *rows);
+    *count = total;
+    return cudaGetLastError() == cudaSuccess ? WGQ_OK : WGQ_ECUDA;
 }
 
 int launch_assemble(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, const wgq_out_t* M,
@@ -1051,6 +1086,7 @@ int launch_assemble(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t*
     int rc = WGQ_EUNSUPPORTED;
     const int key = R->p * 10 + R->dim;
     a.frame = 0;
+    int64_t* shell = nullptr;            // 2D shell-row list (stream-ordered scratch)
     if (!force_generic && R->dim == 2 && c->kind == WGQ_COEF_FOURIER_LOGN && a.coef.n_modes > 0) {
         // class-I rows (both indices in [2p, N-1-2p]) in the interior kernel (fourier2d.cu), the
         // frame in the per-row tensor-core kernel over the rows whose directions all have <= 4
@@ -1074,15 +1110,12 @@ int launch_assemble(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t*
             cudaFreeAsync(tab, st);
             return rc;
         }
-        const int64_t* shell = nullptr;
-        int64_t nshell = 0;
-        rc = shell_rows_2d(const_cast<wgq_rules_s*>(R), a.row_begin, a.row_end, &shell, &nshell);
-        if (rc != WGQ_OK || nshell == 0) {
+        rc = shell_rows_2d(R, a.row_begin, a.row_end, st, &shell, &a.nlist);
+        if (rc != WGQ_OK || a.nlist == 0) {
             cudaFreeAsync(tab, st);
             return rc;
         }
         a.rows_list = shell;
-        a.nlist = nshell;
     }
     switch (key) {
         case 21: rc = launch_generic_pd<2, 1>(a, T.maxM, T.maxK, st); break;
@@ -1092,6 +1125,7 @@ int launch_assemble(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t*
         case 32: rc = launch_generic_pd<3, 2>(a, T.maxM, T.maxK, st); break;
         case 33: rc = launch_generic_pd<3, 3>(a, T.maxM, T.maxK, st); break;
     }
+    if (shell) cudaFreeAsync(shell, st);
     if (tab) cudaFreeAsync(tab, st);
     return rc;
 }
@@ -1117,6 +1151,7 @@ int launch_load(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, 
         const char* e = getenv("WGQ_FORCE_GENERIC");
         return e && e[0] == '1';
     }();
+    int64_t* shell = nullptr;            // 2D shell-row list (stream-ordered scratch)
     if (!force_generic && R->dim == 2 && c->kind == WGQ_COEF_FOURIER_LOGN && a.coef.n_modes > 0) {
         // the 2D tensor-core kernel in load mode (its exponent product and exp, no y / x stages),
         // then the generic per-row kernel over the shell rows (GL-fallback boundary classes)
@@ -1126,15 +1161,12 @@ int launch_load(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, 
         f.do_mass = 1;
         f.do_stiff = 0;
         rc = R->p == 3 ? launch_fourier2d_p<3>(f, st) : launch_fourier2d_p<2>(f, st);
-        const int64_t* shell = nullptr;
-        int64_t nshell = 0;
-        if (rc == WGQ_OK) rc = shell_rows_2d(const_cast<wgq_rules_s*>(R), row_begin, row_end, &shell, &nshell);
-        if (rc != WGQ_OK || nshell == 0) {
+        if (rc == WGQ_OK) rc = shell_rows_2d(R, row_begin, row_end, st, &shell, &a.nlist);
+        if (rc != WGQ_OK || a.nlist == 0) {
             if (tab) cudaFreeAsync(tab, st);
             return rc;
         }
         a.rows_list = shell;
-        a.nlist = nshell;
     }
     rc = WGQ_EUNSUPPORTED;
     switch (R->p * 10 + R->dim) {
@@ -1145,6 +1177,7 @@ int launch_load(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, 
         case 32: rc = launch_load_pd<3, 2>(a, PW, b, st); break;
         case 33: rc = launch_load_pd<3, 3>(a, PW, b, st); break;
     }
+    if (shell) cudaFreeAsync(shell, st);
     if (tab) cudaFreeAsync(tab, st);
     if (PW) cudaFreeAsync(PW, st);
     return rc;
@@ -1174,18 +1207,16 @@ int launch_apply(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c,
     double* tab = nullptr;
     int rc = coef_tables(R, T, a, c, st, &tab);
     if (rc != WGQ_OK) return rc;
+    int64_t* shell = nullptr;            // 2D shell-row list (stream-ordered scratch)
     if (!force_generic && R->dim == 2 && c->kind == WGQ_COEF_FOURIER_LOGN && a.coef.n_modes > 0) {
         // tensor-core rows, then the generic kernel over the shell rows (as for the assembly)
         rc = R->p == 3 ? launch_fourier2d_p<3>(a, st) : launch_fourier2d_p<2>(a, st);
-        const int64_t* shell = nullptr;
-        int64_t nshell = 0;
-        if (rc == WGQ_OK) rc = shell_rows_2d(const_cast<wgq_rules_s*>(R), row_begin, row_end, &shell, &nshell);
-        if (rc != WGQ_OK || nshell == 0) {
+        if (rc == WGQ_OK) rc = shell_rows_2d(R, row_begin, row_end, st, &shell, &a.nlist);
+        if (rc != WGQ_OK || a.nlist == 0) {
             cudaFreeAsync(tab, st);
             return rc;
         }
         a.rows_list = shell;
-        a.nlist = nshell;
     }
     rc = WGQ_EUNSUPPORTED;
     switch (R->p * 10 + R->dim) {
@@ -1196,6 +1227,7 @@ int launch_apply(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c,
         case 32: rc = launch_generic_pd<3, 2>(a, T.maxM, T.maxK, st); break;
         case 33: rc = launch_generic_pd<3, 3>(a, T.maxM, T.maxK, st); break;
     }
+    if (shell) cudaFreeAsync(shell, st);
     if (tab) cudaFreeAsync(tab, st);
     return rc;
 }

@@ -80,9 +80,6 @@ struct wgq_rules_s {
     wgq::ClassRule rules[2][wgq::kMaxP + 1];
     std::mutex mu;
     std::map<int, wgq::RowTables> tables;   // per CUDA device
-    // shell rows (rows touching a GL-fallback boundary class) of a row range, per device:
-    // (device, row_begin, row_end) -> device array of global row ids (built once, reused)
-    std::map<std::tuple<int, int64_t, int64_t>, std::pair<int64_t*, int64_t>> shells;
     // separable-coefficient vectors (separable.cu), per (device, kind, trig[3], wavenum[3])
     std::map<std::array<int, 8>, double*> sep_vectors;
 };
@@ -104,8 +101,12 @@ int build_row_tables(const wgq_rules_s* R, RowTables* T, void* stream);
 void free_row_tables(RowTables* T);
 
 // assemble.cu
-// Device array of the 2D shell rows of [row_begin, row_end) (cached in the rules handle).
-int shell_rows_2d(wgq_rules_s* R, int64_t row_begin, int64_t row_end, const int64_t** rows, int64_t* count);
+#ifdef __CUDACC__
+// The 2D shell rows of [row_begin, row_end) (rows touching a GL-fallback boundary class), generated
+// on the device into stream-ordered scratch the caller frees with cudaFreeAsync on the same stream.
+int shell_rows_2d(const wgq_rules_s* R, int64_t row_begin, int64_t row_end, cudaStream_t st, int64_t** rows,
+                  int64_t* count);
+#endif
 int launch_assemble(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c,
                     const wgq_out_t* M, const wgq_out_t* K, void* stream);
 int launch_csr_structure(const wgq_rules_s* R, int64_t row_begin, int64_t row_end,

@@ -239,3 +239,28 @@ def test_gl_boundary_mode_grid_3d(p, n):
                           np.abs(u[oasm.ell_columns(p, n, d, r)[oasm.ell_columns(p, n, d, r) >= 0]])
                           for i, r in enumerate(rows)])
         compare(y[k].cpu().numpy(), yref, ("gl-grid apply", p, n, k), scale, rowwise=False)
+
+
+@pytest.mark.parametrize("p,n,bnd", [(3, 10, 0), (2, 9, 1), (3, 12, 1)])
+def test_fourier2d_shell_rows_ragged_ranges(p, n, bnd):
+    """The 2D FOURIER shell pass (rows touching a GL-fallback class, generated on the device per
+    call) over row ranges that start and end inside lines, for the assembly, the load vector and
+    the matrix-free product: every range reproduces the whole-mesh rows bitwise."""
+    from paper_1710_01048_b200 import api, wgq
+    d = 2
+    N = n + p
+    rules = wgq.Rules(p, n, d, bnd)
+    c = api.coefficient(inputs.coefficient({"kind": "fourier_logn", "seed": 29, "n_modes": 8, "amp": 0.3}, d))
+    full = api.assemble(rules, c)
+    bfull = api.assemble_load(rules, c)
+    u = torch.from_numpy(np.random.default_rng(2).standard_normal(N * N)).cuda()
+    yfull = api.apply(rules, c, u)
+    for lo, hi in ((1, N + 2), (N - 1, 2 * N + 1), (3 * N + 1, N * N - 1), (N * N - N - 1, N * N)):
+        part = api.assemble(rules, c, row_begin=lo, row_end=hi)
+        b = api.assemble_load(rules, c, lo, hi)
+        y = api.apply(rules, c, u, row_begin=lo, row_end=hi)
+        torch.cuda.synchronize()
+        for k in ("mass", "stiffness"):
+            assert torch.equal(part[k], full[k][lo:hi]), (lo, hi, k)
+            assert torch.equal(y[k], yfull[k][lo:hi]), (lo, hi, k)
+        assert torch.equal(b, bfull[lo:hi]), (lo, hi)
