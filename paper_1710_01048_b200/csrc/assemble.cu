@@ -1011,14 +1011,15 @@ __host__ __device__ inline int64_t shell_line_start(const ShellDesc& d, int64_t 
 }
 
 __global__ void k_shell_rows(const ShellDesc d, int64_t* out) {
-    const int64_t l = d.l0 + blockIdx.y;
+    // one warp per line of the range
+    const int64_t l = d.l0 + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    const int lane = threadIdx.x & 31;
     if (l > d.l1) return;
     const int64_t a = l * d.N > d.rb ? l * d.N : d.rb, b = (l + 1) * d.N < d.re ? (l + 1) * d.N : d.re;
     const int64_t base = shell_line_start(d, l);
     if (shell_is_wide(d, l)) {
-        for (int64_t r = a + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < b; r += (int64_t)gridDim.x * blockDim.x)
-            out[base + (r - a)] = r;
-    } else if (blockIdx.x == 0 && threadIdx.x == 0) {
+        for (int64_t r = a + lane; r < b; r += 32) out[base + (r - a)] = r;
+    } else if (lane == 0) {
         int64_t c = 0;
         for (int k = 0; k < d.nw; ++k) {
             const int64_t r = l * d.N + d.w[k];
@@ -1045,8 +1046,8 @@ int shell_rows_2d(const wgq_rules_s* R, int64_t row_begin, int64_t row_end, cuda
     const int64_t total = d.l1 > d.l0 ? shell_line_start(d, d.l1) + shell_line_count(d, d.l1) : shell_line_count(d, d.l0);
     if (total == 0) return WGQ_OK;
     if (cudaMallocAsync((void**)rows, (size_t)total * sizeof(int64_t), st) != cudaSuccess) return WGQ_ENOMEM;
-    const dim3 g((unsigned)((R->N + 255) / 256), (unsigned)(d.l1 - d.l0 + 1));
-    k_shell_rows<<<g, 256, 0, st>>>(d, *rows);
+    const int64_t lines = d.l1 - d.l0 + 1;
+    k_shell_rows<<<(unsigned)((lines * 32 + 255) / 256), 256, 0, st>>>(d, *rows);
     *count = total;
     return cudaGetLastError() == cudaSuccess ? WGQ_OK : WGQ_ECUDA;
 }
@@ -1080,6 +1081,9 @@ int launch_assemble(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t*
         a.cw = c->kind == WGQ_COEF_TRIG_SEP ? 1 : 2 * a.coef.n_modes;
         const int64_t entries = 2 * (int64_t)R->dim * R->N * kMaxNodes;
         if (cudaMallocAsync((void**)&tab, (size_t)entries * a.cw * sizeof(double), st) != cudaSuccess) return WGQ_ENOMEM;
+        // unused node slots stay finite (0): the 2D kernels read 4 nodes per row and weigh the
+        // missing ones by 0
+        cudaMemsetAsync(tab, 0, (size_t)entries * a.cw * sizeof(double), st);
         k_coef_tables<<<(unsigned)((entries + 255) / 256), 256, 0, st>>>(a.coef, R->dim, T, tab, a.cw);
         a.ctab = tab;
     }
@@ -1096,16 +1100,11 @@ int launch_assemble(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t*
             return !(e && e[0] == '0');
         }();
         if (interior_on && f2d_interior_applies(R, T, c)) {
+            // class-I rows and the frame (per-row tables) in one launch (fourier2d.cu)
             rc = launch_f2d_interior(R, T, tab, a.cw, M, K, st);
-            if (rc != WGQ_OK) {
-                cudaFreeAsync(tab, st);
-                return rc;
-            }
-            a.frame = 1;
-            a.frame_lo = 2 * R->p;
-            a.frame_hi = (int)(R->N - 1 - 2 * R->p);
+        } else {
+            rc = R->p == 3 ? launch_fourier2d_p<3>(a, st) : launch_fourier2d_p<2>(a, st);
         }
-        rc = R->p == 3 ? launch_fourier2d_p<3>(a, st) : launch_fourier2d_p<2>(a, st);
         if (rc != WGQ_OK) {
             cudaFreeAsync(tab, st);
             return rc;

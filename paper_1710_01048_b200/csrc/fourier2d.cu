@@ -103,9 +103,178 @@ __device__ __forceinline__ void store_rows(double* d0, double* d1, const double*
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// The frame: every 2D row with an index outside class I (and no GL-fallback wide direction),
+// with the interior kernel's structure (2 lines x row pairs, DMMA exponent / y / x chain, table
+// exp) but per-line y and per-row x weighted tables (RowTables::AW) as the A fragments, and
+// per-row stores (a row is written only if it is in the frame: the interior kernel owns
+// [lo, hi]^2).  Items: line pairs whose both lines are class I contribute their two frame row
+// chunks [0, lo) and (hi, N); the other line pairs (the mesh's first and last lines) all their
+// row chunks.
+struct F2fArgs {
+    int64_t items;            // frame work items (done before the interior items)
+    const double* ctab;
+    int cw;
+    const double* AW;         // RowTables::AW [N][2][4][8]
+    int64_t N, row_begin, row_end;
+    int lo, hi;               // class-I range (the interior kernel's rows)
+    int L0, nlp;              // first line of the pairing, number of line pairs
+    int jA0, jA1;             // line pairs jA0 .. jA1 are interior (both lines class I)
+    int nw;                   // wide 1D indices (GL-fallback classes, > 4 nodes): left to the shell pass
+    int wide[2 * kMaxP];
+    double* Mv;
+    double* Kv;
+    int64_t ldM, ldK;
+    const int64_t* rpM;
+    const int64_t* rpK;
+    int csr;
+};
+
+__device__ __forceinline__ bool f2f_wide(const F2fArgs& a, int64_t r) {
+    bool w = false;
+#pragma unroll
+    for (int k = 0; k < 2 * kMaxP; ++k) w |= k < a.nw && a.wide[k] == r;
+    return w;
+}
+
+template <int KS>
+__device__ __forceinline__ void f2d_frame_item(const F2fArgs& a, int64_t it, const double* tbl, double* os, int lane,
+                                               uint64_t pol) {
+    constexpr int S = 7, P3 = 3;
+    const int g = lane >> 2, t = lane & 3;
+    const int copy = lane & 15;
+    const int64_t N = a.N;
+    const int cw = a.cw;
+    const int64_t nstride = (int64_t)kMaxNodes * cw;
+    const double ysg = (t & 1) ? -1.0 : 1.0;
+    const int nA = a.jA1 >= a.jA0 ? a.jA1 - a.jA0 + 1 : 0;
+    const int fullchunks = (int)((N + 2 * kF2iChunk - 1) / (2 * kF2iChunk));
+    // A fragment of a weighted table, lane (g, t) = Aw^T[o = g][k = t] of 1D row r, kind
+    auto afrag = [&](int64_t r, int kind) { return g < S ? __ldg(a.AW + r * 64 + kind * 32 + t * 8 + g) : 0.0; };
+    int j, x0, npair;
+    if (it < (int64_t)nA * 2) {
+        j = a.jA0 + (int)(it >> 1);
+        x0 = (it & 1) ? a.hi + 1 : 0;
+        npair = (it & 1) ? (int)(N - 1 - a.hi + 1) / 2 : (a.lo + 1) / 2;
+    } else {
+        const int64_t f = it - (int64_t)nA * 2;
+        const int jb = (int)(f / fullchunks);
+        j = jb < a.jA0 ? jb : (nA > 0 ? jb + nA : jb);
+        x0 = (int)(f % fullchunks) * 2 * kF2iChunk;
+        npair = (int)min((int64_t)kF2iChunk, (N - x0 + 1) / 2);
+    }
+    const int La = a.L0 + 2 * j;
+    const bool bval = La + 1 < N;
+    const int Lb = bval ? La + 1 : La;
+    double Ya[KS], Yb[KS], Yab[KS];
+    {
+        const int ky = g >> 1, hi = g & 1;
+        const double* pa = a.ctab + ((int64_t)(2 + hi) * N + La) * nstride + ky * cw + t;
+        const double* pb = a.ctab + ((int64_t)(2 + hi) * N + Lb) * nstride + ky * cw + t;
+        const double* pab = a.ctab + ((int64_t)2 * N + (hi ? Lb : La)) * nstride + ky * cw + t;
+#pragma unroll
+        for (int s = 0; s < KS; ++s) {
+            const bool in = 4 * s + t < cw;
+            Ya[s] = in ? ysg * __ldg(pa + 4 * s) : 0.0;
+            Yb[s] = in ? ysg * __ldg(pb + 4 * s) : 0.0;
+            Yab[s] = in ? ysg * __ldg(pab + 4 * s) : 0.0;
+        }
+    }
+    const double aMa = afrag(La, 0), aKa = afrag(La, 1), aMb = afrag(Lb, 0), aKb = afrag(Lb, 1);
+    const bool la_ok = !f2f_wide(a, La), lb_ok = bval && !f2f_wide(a, Lb);
+    const bool la_in = La >= a.lo && La <= a.hi, lb_in = Lb >= a.lo && Lb <= a.hi;
+    for (int pr = 0; pr < npair; ++pr) {
+        const int i1 = x0 + 2 * pr;
+        const int r0 = i1, r1 = i1 + 1 < N ? i1 + 1 : i1;
+        // x-node g = (kx = g >> 1, row i1 + (g & 1))
+        double XM[KS], XK[KS];
+        {
+            const int rr = (g & 1) ? r1 : r0;
+            const double* pm = a.ctab + (int64_t)rr * nstride + (g >> 1) * cw + t;
+            const double* pk = pm + N * nstride;
+#pragma unroll
+            for (int s = 0; s < KS; ++s) {
+                const bool in = 4 * s + t < cw;
+                XM[s] = in ? __ldg(pm + 4 * s) : 0.0;
+                XK[s] = in ? __ldg(pk + 4 * s) : 0.0;
+            }
+        }
+        double ea0 = 0.0, ea1 = 0.0, eb0 = 0.0, eb1 = 0.0, ek0 = 0.0, ek1 = 0.0;
+#pragma unroll
+        for (int s = 0; s < KS; ++s) {
+            dmma(ea0, ea1, XM[s], Ya[s]);
+            dmma(eb0, eb1, XM[s], Yb[s]);
+            dmma(ek0, ek1, XK[s], Yab[s]);
+        }
+        const double wMa = exp_tab(ea0, tbl, copy), wKya = exp_tab(ea1, tbl, copy);
+        const double wMb = exp_tab(eb0, tbl, copy), wKyb = exp_tab(eb1, tbl, copy);
+        const double wKxa = exp_tab(ek0, tbl, copy), wKxb = exp_tab(ek1, tbl, copy);
+        double tM[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, tKx[2][2] = {{0.0, 0.0}, {0.0, 0.0}},
+               tKy[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+        dmma(tM[0][0], tM[0][1], aMa, wMa);
+        dmma(tKy[0][0], tKy[0][1], aKa, wKya);
+        dmma(tKx[0][0], tKx[0][1], aMa, wKxa);
+        dmma(tM[1][0], tM[1][1], aMb, wMb);
+        dmma(tKy[1][0], tKy[1][1], aKb, wKyb);
+        dmma(tKx[1][0], tKx[1][1], aMb, wKxb);
+        const double aMx[2] = {afrag(r0, 0), afrag(r1, 0)}, aKx[2] = {afrag(r0, 1), afrag(r1, 1)};
+#pragma unroll
+        for (int L = 0; L < 2; ++L)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                double m0 = 0.0, m1 = 0.0, k0 = 0.0, k1 = 0.0;
+                dmma(m0, m1, aMx[i], tM[L][i]);
+                dmma(k0, k1, aKx[i], tKx[L][i]);
+                dmma(k0, k1, aMx[i], tKy[L][i]);
+                double* b = os + L * 2 * kF2iRun + i * 49 + g + 14 * t;
+                if (g < S) {
+                    b[0] = m0;
+                    b[kF2iRun] = k0;
+                    if (t < 3) {
+                        b[7] = m1;
+                        b[kF2iRun + 7] = k1;
+                    }
+                }
+            }
+        __syncwarp();
+        // a7: per row (frame rows are partly outside the mesh: ELL slots of missing columns
+        // hold +0.0, CSR rows are compacted to their valid columns, in slot order)
+#pragma unroll
+        for (int L = 0; L < 2; ++L) {
+            const int i2 = L ? Lb : La;
+            const bool lok = L ? lb_ok : la_ok, lin = L ? lb_in : la_in;
+            const int lo2 = max(-P3, -i2), w2h = min(P3, (int)N - 1 - i2);
+#pragma unroll
+            for (int mat = 0; mat < 2; ++mat) {
+                double* dst = mat ? a.Kv : a.Mv;
+                if (!dst) continue;
+                const double* src = os + (L * 2 + mat) * kF2iRun;
+                for (int e = lane; e < 98; e += 32) {
+                    const int i = e >= 49 ? 1 : 0, slot = e - 49 * i, r = i1 + i;
+                    const int64_t grow = (int64_t)i2 * N + r;
+                    if (!lok || r >= N || (lin && r >= a.lo && r <= a.hi) || f2f_wide(a, r) || grow < a.row_begin ||
+                        grow >= a.row_end)
+                        continue;
+                    const int64_t orow = grow - a.row_begin;
+                    const int o1 = slot % 7 - P3, o2 = slot / 7 - P3;
+                    if (a.csr) {
+                        const int lo1 = max(-P3, -r), hi1 = min(P3, (int)N - 1 - r);
+                        if (o1 < lo1 || o1 > hi1 || o2 < lo2 || o2 > w2h) continue;
+                        st_out(dst + (mat ? a.rpK : a.rpM)[orow] + (o1 - lo1) + (int64_t)(o2 - lo2) * (hi1 - lo1 + 1),
+                               src[e], pol);
+                    } else {
+                        st_out(dst + orow * (mat ? a.ldK : a.ldM) + slot, src[e] + 0.0, pol);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
 // EXACT: cw == 4 KS (every k-step column is a table column, no predicated loads)
 template <int KS, bool EXACT>
-__global__ void __launch_bounds__(kF2iWarps * 32, kF2iMinBlocks) k_f2d_interior(const F2iArgs a) {
+__global__ void __launch_bounds__(kF2iWarps * 32, kF2iMinBlocks) k_f2d_interior(const F2iArgs a, const F2fArgs fa) {
     constexpr int S = 7;
     __shared__ double tbl[64 * 16];
     extern __shared__ double stage[];      // per warp: T staging, output staging
@@ -137,8 +306,15 @@ __global__ void __launch_bounds__(kF2iWarps * 32, kF2iMinBlocks) k_f2d_interior(
     const int lpairs = (nlines + 1) >> 1;
     const int rpairs = (a.hi - a.lo + 2) >> 1;
     const int chunks = (rpairs + kF2iChunk - 1) / kF2iChunk;
-    const int64_t items = (int64_t)lpairs * chunks;
-    for (int64_t it = (int64_t)blockIdx.x * kF2iWarps + warp; it < items; it += (int64_t)gridDim.x * kF2iWarps) {
+    const int64_t items = a.line1 >= a.line0 ? (int64_t)lpairs * chunks : 0;
+    // the frame items first (their rows have per-row tables; a few per warp), then the interior
+    for (int64_t it0 = (int64_t)blockIdx.x * kF2iWarps + warp; it0 < fa.items + items;
+         it0 += (int64_t)gridDim.x * kF2iWarps) {
+        if (it0 < fa.items) {
+            f2d_frame_item<KS>(fa, it0, tbl, os, lane, pol);
+            continue;
+        }
+        const int64_t it = it0 - fa.items;
         const int lp = (int)(it / chunks), ch = (int)(it % chunks);
         const int La = a.line0 + 2 * lp;
         const bool bval = La + 1 <= a.line1;
@@ -333,6 +509,50 @@ bool f2d_interior_applies(const wgq_rules_s* R, const RowTables& T, const wgq_co
     return true;
 }
 
+namespace {
+F2fArgs frame_args(const wgq_rules_s* R, const RowTables& T, const double* ctab, int cw, const wgq_out_t* M,
+                   const wgq_out_t* K) {
+    const wgq_out_t* any = M ? M : K;
+    F2fArgs a{};
+    if (any->row_end <= any->row_begin) return a;
+    a.ctab = ctab;
+    a.cw = cw;
+    a.AW = T.AW;
+    a.N = R->N;
+    a.row_begin = any->row_begin;
+    a.row_end = any->row_end;
+    a.lo = 2 * R->p;
+    a.hi = (int)(R->N - 1 - 2 * R->p);
+    const int64_t l0 = a.row_begin / R->N, l1 = (a.row_end - 1) / R->N;
+    a.L0 = (int)l0;
+    a.nlp = (int)((l1 - l0 + 2) / 2);
+    // interior line pairs: both lines in [lo, hi] and inside the range
+    a.jA0 = (int)std::max<int64_t>(0, (a.lo - l0 + 1) / 2);
+    a.jA1 = -1;
+    for (int j = a.nlp - 1; j >= a.jA0; --j)
+        if (l0 + 2 * j + 1 <= std::min<int64_t>(a.hi, l1)) {
+            a.jA1 = j;
+            break;
+        }
+    if (a.jA1 < a.jA0) a.jA0 = a.nlp, a.jA1 = a.nlp - 1;     // none: every pair is a frame pair
+    for (int64_t r = 0; r < R->N && a.nw < 2 * kMaxP; ++r) {
+        const int cls = r < R->p ? (int)r : (r >= R->n ? (int)(R->n + R->p - 1 - r) : R->p);
+        if (R->rules[WGQ_MASS][cls].m > 4 || R->rules[WGQ_STIFFNESS][cls].m > 4) a.wide[a.nw++] = r;
+    }
+    a.Mv = M ? M->values : nullptr;
+    a.Kv = K ? K->values : nullptr;
+    a.ldM = M ? M->ld : 0;
+    a.ldK = K ? K->ld : 0;
+    a.rpM = M ? M->row_ptr : nullptr;
+    a.rpK = K ? K->row_ptr : nullptr;
+    a.csr = any->layout == WGQ_CSR;
+    const int nA = a.jA1 >= a.jA0 ? a.jA1 - a.jA0 + 1 : 0;
+    const int64_t fullchunks = (R->N + 2 * kF2iChunk - 1) / (2 * kF2iChunk);
+    a.items = (int64_t)nA * 2 + (int64_t)(a.nlp - nA) * fullchunks;
+    return a;
+}
+}  // namespace
+
 int launch_f2d_interior(const wgq_rules_s* R, const RowTables& T, const double* ctab, int cw, const wgq_out_t* M,
                         const wgq_out_t* K, cudaStream_t st) {
     const wgq_out_t* any = M ? M : K;
@@ -347,7 +567,8 @@ int launch_f2d_interior(const wgq_rules_s* R, const RowTables& T, const double* 
     const int64_t l0 = a.row_begin / R->N, l1 = (a.row_end - 1) / R->N;
     a.line0 = (int)std::max<int64_t>(l0, a.lo);
     a.line1 = (int)std::min<int64_t>(l1, a.hi);
-    if (a.row_end <= a.row_begin || a.line1 < a.line0) return WGQ_OK;
+    if (a.row_end <= a.row_begin) return WGQ_OK;
+    const F2fArgs fa = frame_args(R, T, ctab, cw, M, K);      // the frame rows, in the same launch
     a.Mv = M ? M->values : nullptr;
     a.Kv = K ? K->values : nullptr;
     a.ldM = M ? M->ld : 0;
@@ -370,14 +591,14 @@ int launch_f2d_interior(const wgq_rules_s* R, const RowTables& T, const double* 
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t lpairs = (a.line1 - a.line0 + 2) / 2;
     const int64_t rpairs = (a.hi - a.lo + 2) / 2;
-    const int64_t items = lpairs * ((rpairs + kF2iChunk - 1) / kF2iChunk);
+    const int64_t items = (a.line1 >= a.line0 ? lpairs * ((rpairs + kF2iChunk - 1) / kF2iChunk) : 0) + fa.items;
     int64_t blocks = std::min<int64_t>((items + kF2iWarps - 1) / kF2iWarps, (int64_t)sms * kF2iMinBlocks);
     blocks = std::max<int64_t>(blocks, 1);
     const size_t smem = (size_t)kF2iWarps * kF2iWarpSmem * sizeof(double);
     auto go = [&](auto kern) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
             return WGQ_ECUDA;
-        kern<<<(unsigned)blocks, kF2iWarps * 32, smem, st>>>(a);
+        kern<<<(unsigned)blocks, kF2iWarps * 32, smem, st>>>(a, fa);
         return WGQ_OK;
     };
     int rc;

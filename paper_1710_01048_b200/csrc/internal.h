@@ -58,6 +58,10 @@ struct RowTables {
     // to c * B_{r+o} when c is the vertex field's linear interpolant (R6).
     double* PM = nullptr;      // [N][kMaxV][kMaxS]
     double* PK = nullptr;      // [N][kMaxV][kMaxS]
+    // Weighted 1D tables of the first 4 nodes, for the 2D FOURIER kernels (fourier2d.cu):
+    // AW[r][kind][k][o] = w_k B_{r+o}(x_k) (kind 0, mass) / w_k B'_{r+o}(x_k) (kind 1), o < 7, zero
+    // for k >= m and o = 7 (rows with more than 4 nodes are not read through it)
+    double* AW = nullptr;      // [N][2][4][8]
     void* base = nullptr;      // single allocation
     // Host copies of one class-I (interior, 2p <= r <= N-1-2p) row's weighted tables
     // iAwM[k][o] = wM[k] VM[k][o], iAwK[k][o] = wK[k] DK[k][o] (shift-invariant up to rounding:
