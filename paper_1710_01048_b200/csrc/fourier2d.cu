@@ -40,7 +40,7 @@ namespace {
 
 constexpr int kF2iWarps = 8;
 constexpr int kF2iMinBlocks = 2;
-constexpr int kF2iChunk = 8;              // row pairs per work item (the line pair's y data is loaded once)
+constexpr int kF2iChunk = 16;              // row pairs per work item (the line pair's y data is loaded once)
 constexpr int kF2iRun = 100;                             // staging of one (line, matrix) run: 2 rows + shift + pad
 constexpr int kF2iWarpSmem = 4 * kF2iRun;                // output staging of 2 lines x M, K
 
@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(kF2iWarps * 32, kF2iMinBlocks) k_f2d_interior(
             continue;
         }
         const int64_t it = it0 - fa.items;
-        const int lp = (int)(it / chunks), ch = (int)(it % chunks);
+        const int lp = (int)(it % lpairs), ch = (int)(it / lpairs);
         const int La = a.line0 + 2 * lp;
         const bool bval = La + 1 <= a.line1;
         // ---- line-pair data: exponent B fragments
