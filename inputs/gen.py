@@ -67,10 +67,12 @@ def fourier_modes(seed=SEED, n_modes=8, amp=0.3, dim=2):
 
 
 def _white(seed, n, idx3):
-    """g0 at extended vertices given as (a, b, c) index arrays in [-4, n+4]."""
+    """g0 at extended vertices given as (a, b, c) index arrays in [-4, n_a+4]; n = elements per
+    direction (int or (n_x, n_y[, n_z])): key = ((c+4) ext_y + (b+4)) ext_x + (a+4), ext = n + 9
+    (for equal counts the key of SURVEY §8(c) c.4)."""
     a, b, c = idx3
-    ext = n + 9
-    key = ((c + 4) * ext + (b + 4)) * ext + (a + 4)
+    nx, ny = (n, n) if np.ndim(n) == 0 else (int(n[0]), int(n[1]))
+    key = ((c + 4) * (ny + 9) + (b + 4)) * (nx + 9) + (a + 4)
     key = key.astype(np.uint64)
     with np.errstate(over="ignore"):
         k2 = key * np.uint64(2)
@@ -86,15 +88,19 @@ def lognormal_grid(n, seed=SEED, sigma=0.5, dim=3, plane0=0, planes=None):
     indexed [c][b][a] (x fastest).  dim=2: returns [planes, n+1] for rows b (key uses c=0).
     dim=1: returns [n+1] (keys use b=c=0).
     Every value is a function of its global key only, so any slab equals the same slab
-    of the global field.
+    of the global field.  n may give the element count per direction (x, y[, z]): vertex
+    planes then hold (n_y+1) x (n_x+1) values and the slowest axis has n_dim + 1 planes.
     """
-    nv = n + 1
+    ns = [int(n)] * dim if np.ndim(n) == 0 else [int(v) for v in n][:dim]
+    n = (ns[0], ns[1] if dim >= 2 else ns[0])         # the key strides (x, y)
+    nv = ns[dim - 1] + 1
     if planes is None:
         planes = nv - plane0
-    ax = np.arange(-4, nv + 4, dtype=np.int64)
+    ax = np.arange(-4, ns[0] + 1 + 4, dtype=np.int64)
     if dim == 3:
         cz = np.arange(plane0 - 4, plane0 + planes + 4, dtype=np.int64)
-        C, B, A = np.meshgrid(cz, ax, ax, indexing="ij")
+        ay = np.arange(-4, ns[1] + 1 + 4, dtype=np.int64)
+        C, B, A = np.meshgrid(cz, ay, ax, indexing="ij")
         g = _white(seed, n, (A, B, C))
         for axis in (2, 1, 0):
             g = _valid_filter(g, axis)

@@ -14,8 +14,13 @@ and x^(a) the node tensor with stiffness nodes in direction a, mass nodes elsewh
 
 Output: ELL rows of s^d = (2p+1)^d slots, slot = (o1+p) + s*((o2+p) + s*(o3+p)) with
 o_a = j_a - i_a; columns outside [0, N) hold +0.0.  Rows are lexicographic with x
-fastest: i = i1 + N*(i2 + N*i3).  Each row is evaluated literally: the full product
+fastest: i = i1 + N1*(i2 + N2*i3).  Each row is evaluated literally: the full product
 table prod_a B_{j_a}(x_{k_a}) (no sum factorisation) times the weight vector.
+
+Element counts may differ per direction (n = (n_1, ..., n_d): eq:Gmap3 P:113-120 defines the
+knot vector of each parameter direction by its own element count n_EL^i, and eq:DimMulti
+P:134-136 the dimension N = prod_i (n_EL^i + p)); an int n means the same count in every
+direction.  Each direction then has its own spacing h_a = 1/n_a, rules and tables.
 """
 import numpy as np
 
@@ -54,11 +59,22 @@ def tables_1d(p, n, mode="gauss"):
     return out
 
 
+def dims(n, d):
+    """Per-direction element counts [n_1, ..., n_d] from an int or a sequence."""
+    if np.ndim(n) == 0:
+        return [int(n)] * d
+    ns = [int(v) for v in n]
+    assert len(ns) >= d, (n, d)
+    return ns[:d]
+
+
 def decode(row, N, d):
+    """Row index -> per-direction indices (x fastest); N an int or per-direction sizes."""
+    Ns = dims(N, d)
     idx = []
-    for _ in range(d):
-        idx.append(row % N)
-        row //= N
+    for a in range(d):
+        idx.append(row % Ns[a])
+        row //= Ns[a]
     return idx
 
 
@@ -94,13 +110,14 @@ def assemble_rows(p, n, d, rows, desc, kinds=("mass", "stiffness"), grid=None, p
     """ELL values of the requested global rows: {'mass': [R, s^d], 'stiffness': [R, s^d]}.
     absolute=True returns sum_k |term_k| per entry instead (the scale of FP64 rounding in
     that entry, used by the parity tests' conditioning-aware tolerance, R12)."""
-    tab = tables_1d(p, n, mode)
-    N = n + p
+    ns = dims(n, d)
+    tabs = [tables_1d(p, na, mode) for na in ns]
+    Ns = [na + p for na in ns]
     s = 2 * p + 1
     out = {k: np.zeros((len(rows), s ** d)) for k in kinds}
     for ri, row in enumerate(rows):
-        idx = decode(int(row), N, d)
-        R = [tab[i] for i in idx]
+        idx = decode(int(row), Ns, d)
+        R = [tabs[a][i] for a, i in enumerate(idx)]
         if "mass" in kinds:
             out["mass"][ri] = _term([(r.xM, r.wM, r.VM) for r in R], desc, n, grid, plane0, absolute)
         if "stiffness" in kinds:
@@ -118,14 +135,15 @@ def row_weight_sums(p, n, d, rows, desc, grid=None, plane0=0, mode="gauss"):
     mx[i,a] = sum_k W^M_{i,k} x^M_{k,a}         (= (M g^a)_i by linear reproduction)
     kx[i,a] = sum_k W^{K,a}_{i,k}               (= (K g^a)_i; its x-derivative is 1)
     computed directly from the rules and c (no basis tables involved)."""
-    tab = tables_1d(p, n, mode)
-    N = n + p
+    ns = dims(n, d)
+    tabs = [tables_1d(p, na, mode) for na in ns]
+    Ns = [na + p for na in ns]
     m1 = np.zeros(len(rows))
     mx = np.zeros((len(rows), d))
     kx = np.zeros((len(rows), d))
     for ri, row in enumerate(rows):
-        idx = decode(int(row), N, d)
-        R = [tab[i] for i in idx]
+        idx = decode(int(row), Ns, d)
+        R = [tabs[a][i] for a, i in enumerate(idx)]
         X = np.meshgrid(*[r.xM for r in R], indexing="ij")
         W = coeff.evaluate(desc, n, X, grid, plane0)
         for a in range(d):
@@ -153,9 +171,9 @@ def greville(p, n):
 
 def ell_columns(p, n, d, row):
     """Global column index of every ELL slot of ``row`` (-1 where out of range)."""
-    N = n + p
+    Ns = [na + p for na in dims(n, d)]
     s = 2 * p + 1
-    idx = decode(int(row), N, d)
+    idx = decode(int(row), Ns, d)
     cols = np.full(s ** d, -1, dtype=np.int64)
     for slot in range(s ** d):
         rem, col, stride, ok = slot, 0, 1, True
@@ -163,10 +181,10 @@ def ell_columns(p, n, d, row):
             o = rem % s - p
             rem //= s
             j = idx[a] + o
-            if not 0 <= j < N:
+            if not 0 <= j < Ns[a]:
                 ok = False
             col += j * stride
-            stride *= N
+            stride *= Ns[a]
         if ok:
             cols[slot] = col
     return cols

@@ -15,7 +15,8 @@ import numpy as np
 
 
 def evaluate(desc, n, pts, grid=None, plane0=0):
-    """c at points ``pts`` = list of d coordinate arrays (same shape)."""
+    """c at points ``pts`` = list of d coordinate arrays (same shape); n = elements per
+    direction (int, or one per direction: the GRID vertex spacing is 1/n_a)."""
     kind = desc["kind"]
     d = len(pts)
     if kind == "const":
@@ -48,12 +49,14 @@ def evaluate(desc, n, pts, grid=None, plane0=0):
 
 def _multilinear(grid, n, pts, plane0):
     """Vertex field interpolation.  grid is indexed [slowest] ... [x]; its slowest axis
-    starts at vertex plane ``plane0``.  Cell = element containing the point."""
+    starts at vertex plane ``plane0``.  Cell = element containing the point; vertex j of
+    direction a at j / n_a."""
     d = len(pts)
+    ns = [int(n)] * d if np.ndim(n) == 0 else [int(v) for v in n][:d]
     cells, fracs = [], []
     for a in range(d):
-        s = np.asarray(pts[a], dtype=np.float64) * n
-        e = np.clip(np.floor(s), 0, n - 1).astype(np.int64)
+        s = np.asarray(pts[a], dtype=np.float64) * ns[a]
+        e = np.clip(np.floor(s), 0, ns[a] - 1).astype(np.int64)
         cells.append(e)
         fracs.append(s - e)
     out = np.zeros(np.shape(pts[0]))

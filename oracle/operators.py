@@ -21,12 +21,13 @@ from . import assemble, coeff
 
 def load_rows(p, n, d, rows, desc, grid=None, plane0=0, mode="gauss"):
     """b_i for the requested global rows (f given by a coefficient descriptor)."""
-    tab = assemble.tables_1d(p, n, mode)
-    N = n + p
+    ns = assemble.dims(n, d)
+    tabs = [assemble.tables_1d(p, na, mode) for na in ns]
+    Ns = [na + p for na in ns]
     out = np.zeros(len(rows))
     for ri, row in enumerate(rows):
-        idx = assemble.decode(int(row), N, d)
-        R = [tab[i] for i in idx]
+        idx = assemble.decode(int(row), Ns, d)
+        R = [tabs[a][i] for a, i in enumerate(idx)]
         X = np.meshgrid(*[r.xM for r in R], indexing="ij")
         W = coeff.evaluate(desc, n, X, grid, plane0)
         for a in range(d):

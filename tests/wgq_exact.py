@@ -29,29 +29,34 @@ def exact_1d(p, n):
 
 
 def exact_nd(p, n, d):
-    M1, K1 = exact_1d(p, n)
-    M = M1
-    for _ in range(d - 1):
-        M = np.kron(M1, M)
+    """Kronecker products of the exact 1D matrices; n an int or one count per direction."""
+    ns = [n] * d if np.ndim(n) == 0 else list(n)[:d]
+    one = [exact_1d(p, na) for na in ns]
+    M = None
+    for a in range(d):              # row index i = i1 + N1 i2 + N1 N2 i3 -> kron(dir d-1, ..., dir 0)
+        M = one[a][0] if M is None else np.kron(one[a][0], M)
     K = np.zeros_like(M)
     for a in range(d):
         T = None
-        for b in range(d):          # row index i = i1 + N i2 + N^2 i3 -> kron(dir d-1, ..., dir 0)
-            f = K1 if b == a else M1
+        for b in range(d):
+            f = one[b][1] if b == a else one[b][0]
             T = f if T is None else np.kron(f, T)
         K += T
     return M, K
 
 
 def to_ell(A, p, n, d):
-    N = n + p
+    ns = [n] * d if np.ndim(n) == 0 else list(n)[:d]
+    Ns = [na + p for na in ns]
+    st = [int(np.prod(Ns[:a])) for a in range(d)]
+    rows = int(np.prod(Ns))
     s = 2 * p + 1
-    out = np.zeros((N ** d, s ** d))
-    for r in range(N ** d):
-        ir = [(r // N ** a) % N for a in range(d)]
+    out = np.zeros((rows, s ** d))
+    for r in range(rows):
+        ir = [(r // st[a]) % Ns[a] for a in range(d)]
         for slot in range(s ** d):
             o = [(slot // s ** a) % s - p for a in range(d)]
             j = [ir[a] + o[a] for a in range(d)]
-            if all(0 <= j[a] < N for a in range(d)):
-                out[r, slot] = A[r, sum(j[a] * N ** a for a in range(d))]
+            if all(0 <= j[a] < Ns[a] for a in range(d)):
+                out[r, slot] = A[r, sum(j[a] * st[a] for a in range(d))]
     return out
