@@ -122,9 +122,22 @@ const char* wgq_version(void);
  * else WGQ_ENOCONV).  No device work.  *out is owned by the caller: wgq_free_rules(). */
 int wgq_build_rules(int p, int64_t n_elems, int dim, wgq_rules_t* out);
 int wgq_build_rules_ex(int p, int64_t n_elems, int dim, int boundary_mode, wgq_rules_t* out);
+/* Per-direction element counts (eq:Gmap3 P:113-120: each parameter direction has its own
+ * knot vector with n_EL^i elements; eq:DimMulti P:134-136: N = prod_i (n_EL^i + p)).  HOST
+ * n_elems[a], a < dim, each >= p (else WGQ_EUNSUPPORTED); rows are lexicographic with x
+ * fastest, i = i1 + N1 (i2 + N2 i3), N_a = n_a + p; the product of the N_a must stay below 2^31
+ * (WGQ_ERANGE).  wgq_build_rules_ex(p, n, ...) is wgq_build_rules_ex2 with n in every direction.
+ * On an anisotropic mesh every call works; the specialised kernels (GRID line kernel,
+ * separable, 2D FOURIER tensor-core kernels) require equal counts and the assembly, load and
+ * apply calls use the generic per-row kernel there. */
+int wgq_build_rules_ex2(int p, const int64_t* n_elems, int dim, int boundary_mode, wgq_rules_t* out);
 void wgq_free_rules(wgq_rules_t rules);
 
-/* Sizes: N = n+p rows per direction, n_rows = N^dim, stencil = (2p+1)^dim (NULL skips). */
+/* Per-direction sizes: HOST n_elems[3] (0 past dim) and n_rows_dir[3] (N_a; 1 past dim), NULL skips. */
+int wgq_rules_dims(wgq_rules_t rules, int64_t* n_elems, int64_t* n_rows_dir);
+
+/* Sizes: N = n+p rows of direction 0 (every direction on an isotropic mesh), n_rows = the
+ * product of the per-direction row counts, stencil = (2p+1)^dim (NULL skips). */
 int wgq_rules_info(wgq_rules_t rules, int* p, int64_t* n_elems, int* dim,
                    int64_t* n_rows_1d, int64_t* n_rows, int* stencil);
 
@@ -208,6 +221,11 @@ int wgq_host_free(void* ptr);
  * agree with a global generation. */
 int wgq_generate_grid(int64_t n_elems, int dim, uint64_t seed, double sigma,
                       int64_t plane0, int64_t planes, double* grid, void* stream);
+/* The same field on a mesh with per-direction element counts (HOST n_elems[dim]; vertex planes
+ * of (n_y+1) x (n_x+1) values, n_z+1 planes in 3D): white-noise keys
+ * ((c+4)(n_y+9) + (b+4))(n_x+9) + (a+4) (SURVEY c.4 for equal counts). */
+int wgq_generate_grid_ex(const int64_t* n_elems, int dim, uint64_t seed, double sigma,
+                         int64_t plane0, int64_t planes, double* grid, void* stream);
 
 /* Per-row products of an assembled ELL slab with the vectors 1 and g^a (Greville abscissae
  * of direction a, sum_j g_j B_j(x) = x): out = DEVICE [rows][1+dim] = (A 1, A g^1, ..).

@@ -10,36 +10,53 @@ from . import wgq
 
 
 def slab_rows(N, dim, rank, world):
+    """N: rows per direction (an int, or per-direction sizes for an anisotropic mesh)."""
+    Ns = [int(N)] * dim if not hasattr(N, "__len__") else [int(v) for v in N]
+    return _slab_rows(Ns, dim, rank, world)
+
+
+def _slab_rows(Ns, dim, rank, world):
     """Row range [b, e) of rank's slab: contiguous rows along the slowest axes, split into
     whole x-lines (N rows; single rows in 1D) as evenly as possible (the first lines % world
     ranks get one more line).  Line granularity keeps the ranks within one line (0.01 % at C5
     on 8 GPUs) instead of one z-plane (1.9 %) of each other; a slab may start or end inside a
     z-plane, which every kernel and the halo logic handle."""
-    unit = N if dim >= 2 else 1
-    units = N ** dim // unit
+    unit = Ns[0] if dim >= 2 else 1
+    total = 1
+    for v in Ns[:dim]:
+        total *= v
+    units = total // unit
     base, extra = divmod(units, world)
     u0 = rank * base + min(rank, extra)
     u1 = u0 + base + (1 if rank < extra else 0)
     return u0 * unit, u1 * unit
 
 
+def _ns(rules):
+    return list(getattr(rules, "ns", [rules.n] * rules.dim)), list(getattr(rules, "Ns", [rules.N] * rules.dim))
+
+
 def grid_planes_for(rules, row_begin, row_end):
     """Vertex planes [lo, hi] of the slowest axis touched by rows [row_begin, row_end)."""
-    plane_rows = rules.N ** (rules.dim - 1)
+    ns, Ns = _ns(rules)
+    plane_rows = 1
+    for v in Ns[:rules.dim - 1]:
+        plane_rows *= v
     z0 = row_begin // plane_rows
     z1 = (row_end - 1) // plane_rows
-    return max(0, z0 - rules.p), min(rules.n, z1 + 1)
+    return max(0, z0 - rules.p), min(ns[rules.dim - 1], z1 + 1)
 
 
 def make_grid(rules, seed, sigma, row_begin, row_end, device=None, stream=None):
     """Device-generated lognormal vertex slab covering rows [row_begin, row_end):
     returns (grid tensor, plane0)."""
-    n, dim = rules.n, rules.dim
-    lo, hi = (0, n) if dim == 1 else grid_planes_for(rules, row_begin, row_end)
+    dim = rules.dim
+    ns, _ = _ns(rules)
+    lo, hi = (0, ns[0]) if dim == 1 else grid_planes_for(rules, row_begin, row_end)
     planes = hi - lo + 1
-    shape = {1: (n + 1,), 2: (planes, n + 1), 3: (planes, n + 1, n + 1)}[dim]
+    shape = {1: (ns[0] + 1,), 2: (planes, ns[0] + 1), 3: (planes, ns[1] + 1, ns[0] + 1)}[dim]
     g = torch.empty(shape, dtype=torch.float64, device=device or "cuda")
-    wgq.wgq_generate_grid(n, dim, seed, sigma, lo, planes, g, stream)
+    wgq.wgq_generate_grid(ns, dim, seed, sigma, lo, planes, g, stream)
     return g, lo
 
 

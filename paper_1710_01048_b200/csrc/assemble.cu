@@ -91,7 +91,10 @@ struct GenericArgs {
     // load-vector mode (wgq_assemble_load through k_fourier2d): b[i] = sum of the row's weighted mass samples
     int load;
     double* b;
-    int64_t n, N;
+    int64_t n, N;               // direction 0 (all directions on an isotropic mesh)
+    RowTables T3[3];            // per-direction tables (= T when isotropic)
+    Dims dims;                  // per-direction sizes
+    int64_t ctabN;              // row stride of ctab (max N over the directions)
     int64_t row_begin, row_end;
     // k_fourier2d frame mode: skip the rows with both indices in [frame_lo, frame_hi] (done by
     // the interior kernel of fourier2d.cu); off when frame == 0
@@ -116,13 +119,16 @@ struct Dir {
 //   FOURIER_LOGN: (C, S)_m = (cos, sin)(2 pi k_{m,a} x + [a = 0] theta_m) * ([a = 0] ? a_m : 1)
 // so that c = c0 + amp prod_a F_a, resp. c = exp(sum_m Re prod_a (C + i S)_m): the angle-sum
 // expansion of cos(2 pi k_m . x + theta_m) (R13), exact up to rounding.
-__global__ void k_coef_tables(const CoefDev c, int dim, RowTables T, double* tab, int cw) {
+__global__ void k_coef_tables(const CoefDev c, int dim, const RowTables T3a, const RowTables T3b, const RowTables T3c,
+                              int64_t ctabN, double* tab, int cw) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t per_ak = T.N * kMaxNodes;
+    const int64_t per_ak = ctabN * kMaxNodes;
     const int64_t ak = tid / per_ak;
     if (ak >= 2 * dim) return;
     const int a = (int)(ak / 2), kind = (int)(ak % 2);
+    const RowTables& T = a == 0 ? T3a : (a == 1 ? T3b : T3c);     // direction a's rows
     const int64_t r = (tid % per_ak) / kMaxNodes;
+    if (r >= T.N) return;
     const int k = (int)(tid % kMaxNodes);
     const int m = kind == WGQ_MASS ? T.mM[r] : T.mK[r];
     if (k >= m) return;
@@ -185,7 +191,7 @@ __device__ __forceinline__ void stage_term(const GenericArgs& a, const Dir d1, c
             cv = coef_from_tables<D>(a.coef, d1.ct + k1 * a.cw, d2.ct + k2 * a.cw, d3.ct + k3 * a.cw);
         } else {
             double x[3] = {d1.x[k1], d2.x[k2], d3.x[k3]};
-            cv = coef_eval<D>(a.coef, a.n, x);
+            cv = coef_eval<D>(a.coef, a.dims.n, x);
         }
         W[e] = cv * d1.w[k1] * d2.w[k2] * d3.w[k3];
     }
@@ -237,26 +243,21 @@ __global__ void __launch_bounds__(kMaxWarps * 32) k_assemble_generic(const Gener
     double* T1 = W + a.sg.w;
     double* T2 = T1 + a.sg.t1;
     double* T2b = T2 + a.sg.t2;
-    const RowTables& T = a.T;
     const Dir ones = {1, kOnes, kOnes, kOnes, kOnes};
 
     const int64_t nwork = a.rows_list ? a.nlist : a.row_end - a.row_begin;
     for (int64_t w = (int64_t)blockIdx.x * warps + warp; w < nwork; w += (int64_t)gridDim.x * warps) {
         const int64_t row = a.rows_list ? a.rows_list[w] : a.row_begin + w;
-        int64_t idx[3] = {0, 0, 0};
-        int64_t rem = row;
-#pragma unroll
-        for (int q = 0; q < D; ++q) {
-            idx[q] = rem % a.N;
-            rem /= a.N;
-        }
+        int64_t idx[3];
+        a.dims.decode(row, idx);
         Dir dm[3], dk[3];
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
             if (q < D) {
+                const RowTables& T = a.T3[q];
                 const int64_t r = idx[q];
-                const double* cm = a.ctab ? a.ctab + ((int64_t)(2 * q + WGQ_MASS) * a.N + r) * kMaxNodes * a.cw : nullptr;
-                const double* ck = a.ctab ? a.ctab + ((int64_t)(2 * q + WGQ_STIFFNESS) * a.N + r) * kMaxNodes * a.cw : nullptr;
+                const double* cm = a.ctab ? a.ctab + ((int64_t)(2 * q + WGQ_MASS) * a.ctabN + r) * kMaxNodes * a.cw : nullptr;
+                const double* ck = a.ctab ? a.ctab + ((int64_t)(2 * q + WGQ_STIFFNESS) * a.ctabN + r) * kMaxNodes * a.cw : nullptr;
                 dm[q] = {T.mM[r], T.xM + r * kMaxMassNodes, T.wM + r * kMaxMassNodes, T.VM + r * kMaxMassNodes * kMaxS, cm};
                 dk[q] = {T.mK[r], T.xK + r * kMaxStiffNodes, T.wK + r * kMaxStiffNodes, T.DK + r * kMaxStiffNodes * kMaxS, ck};
             } else {
@@ -298,9 +299,9 @@ __global__ void __launch_bounds__(kMaxWarps * 32) k_assemble_generic(const Gener
 #pragma unroll
                 for (int q = 0; q < D; ++q) {
                     const int64_t jq = idx[q] + o[q];
-                    ok = ok && jq >= 0 && jq < a.N;
+                    ok = ok && jq >= 0 && jq < a.dims.N[q];
                     col += jq * stride;
-                    stride *= a.N;
+                    stride *= a.dims.N[q];
                 }
                 if (!ok) continue;
                 const double uj = __ldg(a.u + (col - a.u_row0));
@@ -334,7 +335,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32) k_assemble_generic(const Gener
 #pragma unroll
                 for (int q = 0; q < D; ++q) {
                     const int64_t lo = idx[q] - P < 0 ? -idx[q] : -P;
-                    const int64_t hi = idx[q] + P > a.N - 1 ? a.N - 1 - idx[q] : P;
+                    const int64_t hi = idx[q] + P > a.dims.N[q] - 1 ? a.dims.N[q] - 1 - idx[q] : P;
                     if (o[q] < lo || o[q] > hi) ok = false;
                     pos += (o[q] - lo) * stride;
                     stride *= hi - lo + 1;
@@ -632,58 +633,58 @@ __global__ void __launch_bounds__(256) k_load(const GenericArgs a, const double*
     const int64_t rows = a.rows_list ? a.nlist : a.row_end - a.row_begin;   // rows_list: a shell pass
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < rows; t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t row = a.rows_list ? a.rows_list[t] : a.row_begin + t;
-        int64_t idx[3] = {0, 0, 0};
-        int64_t rem = row;
-#pragma unroll
-        for (int q = 0; q < D; ++q) {
-            idx[q] = rem % a.N;
-            rem /= a.N;
-        }
+        int64_t idx[3];
+        a.dims.decode(row, idx);
         double acc = 0.0;
         if (a.coef.kind == WGQ_COEF_GRID) {
-            const int64_t nv = a.n + 1;
+            // PW of direction q at PW + q ctabN kMaxV; vertex planes of (n_y+1) x (n_x+1)
+            const int64_t nvx = a.dims.n[0] + 1, nvy = D >= 2 ? a.dims.n[1] + 1 : 1;
+            const double* PWq[3] = {PW, PW + a.ctabN * kMaxV, PW + 2 * a.ctabN * kMaxV};
             int64_t base[3];
 #pragma unroll
             for (int q = 0; q < D; ++q) base[q] = idx[q] - P > 0 ? idx[q] - P : 0;
             const int Vz = D >= 3 ? V : 1, Vy = D >= 2 ? V : 1;
             for (int vz = 0; vz < Vz; ++vz) {
-                const double wz = D >= 3 ? PW[idx[2] * kMaxV + vz] : 1.0;
+                const double wz = D >= 3 ? PWq[2][idx[2] * kMaxV + vz] : 1.0;
                 for (int vy = 0; vy < Vy; ++vy) {
-                    const double wy = D >= 2 ? PW[idx[1] * kMaxV + vy] : 1.0;
+                    const double wy = D >= 2 ? PWq[1][idx[1] * kMaxV + vy] : 1.0;
                     const int64_t zz = D >= 3 ? base[2] + vz : 0, yy = D >= 2 ? base[1] + vy : 0;
                     const int64_t zrow = D == 3 ? zz : (D == 2 ? yy : 0);
-                    if (wz * wy == 0.0 || zz > a.n || yy > a.n) continue;
+                    if (wz * wy == 0.0 || (D >= 3 && zz > a.dims.n[2]) || (D >= 2 && yy > a.dims.n[1])) continue;
                     double sx = 0.0;
 #pragma unroll
                     for (int vx = 0; vx < V; ++vx) {
                         const int64_t xx = base[0] + vx;
-                        const double wx = PW[idx[0] * kMaxV + vx];
-                        if (wx == 0.0 || xx > a.n) continue;
+                        const double wx = PWq[0][idx[0] * kMaxV + vx];
+                        if (wx == 0.0 || xx > a.dims.n[0]) continue;
                         const double* g;
                         if (D == 1) g = a.coef.grid + (xx - a.coef.plane0);
-                        else if (D == 2) g = a.coef.grid + (zrow - a.coef.plane0) * nv + xx;
-                        else g = a.coef.grid + ((zz - a.coef.plane0) * nv + yy) * nv + xx;
+                        else if (D == 2) g = a.coef.grid + (zrow - a.coef.plane0) * nvx + xx;
+                        else g = a.coef.grid + ((zz - a.coef.plane0) * nvy + yy) * nvx + xx;
                         sx = fma(wx, __ldg(g), sx);
                     }
                     acc = fma(wz * wy, sx, acc);
                 }
             }
         } else {
-            const RowTables& T = a.T;
-            const int n1 = T.mM[idx[0]], n2 = D >= 2 ? T.mM[idx[1]] : 1, n3 = D >= 3 ? T.mM[idx[2]] : 1;
+            const RowTables& T1 = a.T3[0];
+            const RowTables& T2 = a.T3[1];
+            const RowTables& T3 = a.T3[2];
+            const int n1 = T1.mM[idx[0]], n2 = D >= 2 ? T2.mM[idx[1]] : 1, n3 = D >= 3 ? T3.mM[idx[2]] : 1;
             for (int k3 = 0; k3 < n3; ++k3) {
-                const double w3 = D >= 3 ? T.wM[idx[2] * kMaxMassNodes + k3] : 1.0;
+                const double w3 = D >= 3 ? T3.wM[idx[2] * kMaxMassNodes + k3] : 1.0;
                 for (int k2 = 0; k2 < n2; ++k2) {
-                    const double w2 = D >= 2 ? T.wM[idx[1] * kMaxMassNodes + k2] : 1.0;
+                    const double w2 = D >= 2 ? T2.wM[idx[1] * kMaxMassNodes + k2] : 1.0;
                     for (int k1 = 0; k1 < n1; ++k1) {
-                        const double w1 = T.wM[idx[0] * kMaxMassNodes + k1];
+                        const double w1 = T1.wM[idx[0] * kMaxMassNodes + k1];
                         double cv = a.coef.c0;
                         if (a.ctab) {
                             const int64_t k[3] = {k1, k2, k3};
                             const double* f[3];
 #pragma unroll
                             for (int q = 0; q < 3; ++q)
-                                f[q] = q < D ? a.ctab + ((int64_t)(2 * q + WGQ_MASS) * a.N + idx[q]) * kMaxNodes * a.cw + k[q] * a.cw
+                                f[q] = q < D ? a.ctab + ((int64_t)(2 * q + WGQ_MASS) * a.ctabN + idx[q]) * kMaxNodes * a.cw +
+                                                   k[q] * a.cw
                                              : nullptr;
                             cv = coef_from_tables<D>(a.coef, f[0], f[1], f[2]);
                         }
@@ -919,12 +920,12 @@ __global__ void __launch_bounds__(kLTW * 32) k_load_grid_tile(const GenericArgs 
 }
 
 template <int P, int D>
-int launch_load_pd(const GenericArgs& a, const double* PW, double* b, cudaStream_t st) {
+int launch_load_pd(const GenericArgs& a, const double* PW, double* b, bool special, cudaStream_t st) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t rows = a.row_end - a.row_begin;
-    if (D == 3 && a.coef.kind == WGQ_COEF_GRID && a.N * a.N * a.N < ((int64_t)1 << 31)) {
+    if (special && D == 3 && a.coef.kind == WGQ_COEF_GRID && a.N * a.N * a.N < ((int64_t)1 << 31)) {
         const int64_t pr = a.N * a.N;
         const int64_t planes = (a.row_end - 1) / pr - a.row_begin / pr + 1;
         constexpr int W = 32 - (P + 2) + 1;
@@ -938,7 +939,7 @@ int launch_load_pd(const GenericArgs& a, const double* PW, double* b, cudaStream
         k_load_grid_tile<P><<<g, kLTW * 32, smem, st>>>(a, PW, b);
         return cudaGetLastError() == cudaSuccess ? WGQ_OK : WGQ_ECUDA;
     }
-    if (D >= 2 && a.coef.kind == WGQ_COEF_GRID) {
+    if (special && D >= 2 && a.coef.kind == WGQ_COEF_GRID) {
         const int64_t items = ((a.row_end - 1) / a.N - a.row_begin / a.N + 1) * ((a.N + 31) / 32);
         const int64_t b2 = std::max<int64_t>(1, std::min<int64_t>((items + 7) / 8, (int64_t)sms * 16));
         k_load_grid_line<P, D><<<(unsigned)b2, 256, 0, st>>>(a, PW, b);
@@ -950,26 +951,42 @@ int launch_load_pd(const GenericArgs& a, const double* PW, double* b, cudaStream
 }
 
 // coefficient factor tables for an analytic kind (stream-ordered scratch) or nullptr
-int coef_tables(const wgq_rules_s* R, const RowTables& T, GenericArgs& a, const wgq_coeff_t* c, cudaStream_t st,
-                double** tab) {
+// Coefficient factor tables (stream-ordered scratch the caller frees): [2 dim][ctabN][kMaxNodes][cw],
+// unused node slots zero (the 2D kernels read 4 nodes per row and weigh the missing ones by 0).
+int coef_tables(const wgq_rules_s* R, GenericArgs& a, const wgq_coeff_t* c, cudaStream_t st, double** tab) {
     *tab = nullptr;
     if (c->kind != WGQ_COEF_TRIG_SEP && c->kind != WGQ_COEF_FOURIER_LOGN) return WGQ_OK;
     a.cw = c->kind == WGQ_COEF_TRIG_SEP ? 1 : 2 * a.coef.n_modes;
     if (a.cw == 0) a.cw = 1;
-    const int64_t entries = 2 * (int64_t)R->dim * R->N * kMaxNodes;
+    const int64_t entries = 2 * (int64_t)R->dim * a.ctabN * kMaxNodes;
     if (cudaMallocAsync((void**)tab, (size_t)entries * a.cw * sizeof(double), st) != cudaSuccess) return WGQ_ENOMEM;
-    k_coef_tables<<<(unsigned)((entries + 255) / 256), 256, 0, st>>>(a.coef, R->dim, T, *tab, a.cw);
+    cudaMemsetAsync(*tab, 0, (size_t)entries * a.cw * sizeof(double), st);
+    k_coef_tables<<<(unsigned)((entries + 255) / 256), 256, 0, st>>>(a.coef, R->dim, a.T3[0], a.T3[1], a.T3[2], a.ctabN,
+                                                                      *tab, a.cw);
     a.ctab = *tab;
     return WGQ_OK;
 }
 
-GenericArgs base_args(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, int64_t row_begin,
-                      int64_t row_end) {
-    GenericArgs a{};
-    a.T = T;
-    a.coef = make_coef(c);
+int64_t max_rows_1d(const wgq_rules_s* R) {
+    int64_t m = 0;
+    for (int a = 0; a < R->dim; ++a) m = std::max<int64_t>(m, R->dims.N[a]);
+    return m;
+}
+
+void set_dirs(GenericArgs& a, const wgq_rules_s* R, const Tables3& TT) {
+    a.T = TT.t[0];
+    for (int q = 0; q < 3; ++q) a.T3[q] = TT.t[q];
+    a.dims = R->dims;
+    a.ctabN = max_rows_1d(R);
     a.n = R->n;
     a.N = R->N;
+}
+
+GenericArgs base_args(const wgq_rules_s* R, const Tables3& TT, const wgq_coeff_t* c, int64_t row_begin,
+                      int64_t row_end) {
+    GenericArgs a{};
+    set_dirs(a, R, TT);
+    a.coef = make_coef(c);
     a.row_begin = row_begin;
     a.row_end = row_end;
     return a;
@@ -1052,19 +1069,20 @@ int shell_rows_2d(const wgq_rules_s* R, int64_t row_begin, int64_t row_end, cuda
     return cudaGetLastError() == cudaSuccess ? WGQ_OK : WGQ_ECUDA;
 }
 
-int launch_assemble(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, const wgq_out_t* M,
+int launch_assemble(const wgq_rules_s* R, const Tables3& TT, const wgq_coeff_t* c, const wgq_out_t* M,
                     const wgq_out_t* K, void* stream) {
-    static const bool force_generic = [] {
+    static const bool force_generic_env = [] {
         const char* e = getenv("WGQ_FORCE_GENERIC");
         return e && e[0] == '1';
     }();
+    // the specialised kernels assume equal element counts in every direction
+    const bool force_generic = force_generic_env || !R->iso;
+    const RowTables& T = TT.t[0];
     if (!force_generic && line_kernel_applies(R, c, M, K)) return launch_line(R, T, c, M, K, stream);
     if (!force_generic && sep_applies(c)) return launch_sep(R, T, c, M, K, stream);
     GenericArgs a{};
-    a.T = T;
+    set_dirs(a, R, TT);
     a.coef = make_coef(c);
-    a.n = R->n;
-    a.N = R->N;
     const wgq_out_t* any = M ? M : K;
     a.row_begin = any->row_begin;
     a.row_end = any->row_end;
@@ -1077,17 +1095,9 @@ int launch_assemble(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t*
     cudaStream_t st = (cudaStream_t)stream;
     // analytic coefficients: factor tables at the nodes (stream-ordered scratch, freed after)
     double* tab = nullptr;
-    if (c->kind == WGQ_COEF_TRIG_SEP || c->kind == WGQ_COEF_FOURIER_LOGN) {
-        a.cw = c->kind == WGQ_COEF_TRIG_SEP ? 1 : 2 * a.coef.n_modes;
-        const int64_t entries = 2 * (int64_t)R->dim * R->N * kMaxNodes;
-        if (cudaMallocAsync((void**)&tab, (size_t)entries * a.cw * sizeof(double), st) != cudaSuccess) return WGQ_ENOMEM;
-        // unused node slots stay finite (0): the 2D kernels read 4 nodes per row and weigh the
-        // missing ones by 0
-        cudaMemsetAsync(tab, 0, (size_t)entries * a.cw * sizeof(double), st);
-        k_coef_tables<<<(unsigned)((entries + 255) / 256), 256, 0, st>>>(a.coef, R->dim, T, tab, a.cw);
-        a.ctab = tab;
-    }
-    int rc = WGQ_EUNSUPPORTED;
+    int rc = coef_tables(R, a, c, st, &tab);
+    if (rc != WGQ_OK) return rc;
+    rc = WGQ_EUNSUPPORTED;
     const int key = R->p * 10 + R->dim;
     a.frame = 0;
     int64_t* shell = nullptr;            // 2D shell-row list (stream-ordered scratch)
@@ -1129,27 +1139,30 @@ int launch_assemble(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t*
     return rc;
 }
 
-int launch_load(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, int64_t row_begin, int64_t row_end,
+int launch_load(const wgq_rules_s* R, const Tables3& TT, const wgq_coeff_t* c, int64_t row_begin, int64_t row_end,
                 double* b, void* stream) {
     if (row_end <= row_begin) return WGQ_OK;
-    {
-        const char* e = getenv("WGQ_FORCE_GENERIC");
-        if (!(e && e[0] == '1') && sep_applies(c)) return launch_sep_load(R, T, c, row_begin, row_end, b, stream);
-    }
-    cudaStream_t st = (cudaStream_t)stream;
-    GenericArgs a = base_args(R, T, c, row_begin, row_end);
-    double* tab = nullptr;
-    double* PW = nullptr;
-    int rc = coef_tables(R, T, a, c, st, &tab);
-    if (rc != WGQ_OK) return rc;
-    if (c->kind == WGQ_COEF_GRID) {
-        if (cudaMallocAsync((void**)&PW, (size_t)R->N * kMaxV * sizeof(double), st) != cudaSuccess) return WGQ_ENOMEM;
-        k_vertex_weights<<<(unsigned)((R->N * kMaxV + 255) / 256), 256, 0, st>>>(T, R->p, PW);
-    }
-    static const bool force_generic = [] {
+    static const bool force_generic_env = [] {
         const char* e = getenv("WGQ_FORCE_GENERIC");
         return e && e[0] == '1';
     }();
+    const bool force_generic = force_generic_env || !R->iso;     // specialised kernels: equal counts
+    const RowTables& T = TT.t[0];
+    if (!force_generic && sep_applies(c)) return launch_sep_load(R, T, c, row_begin, row_end, b, stream);
+    cudaStream_t st = (cudaStream_t)stream;
+    GenericArgs a = base_args(R, TT, c, row_begin, row_end);
+    double* tab = nullptr;
+    double* PW = nullptr;
+    int rc = coef_tables(R, a, c, st, &tab);
+    if (rc != WGQ_OK) return rc;
+    if (c->kind == WGQ_COEF_GRID) {
+        // PW of direction q at PW + q ctabN kMaxV
+        if (cudaMallocAsync((void**)&PW, (size_t)3 * a.ctabN * kMaxV * sizeof(double), st) != cudaSuccess)
+            return WGQ_ENOMEM;
+        for (int q = 0; q < R->dim; ++q)
+            k_vertex_weights<<<(unsigned)((TT.t[q].N * kMaxV + 255) / 256), 256, 0, st>>>(TT.t[q], R->p,
+                                                                                         PW + q * a.ctabN * kMaxV);
+    }
     int64_t* shell = nullptr;            // 2D shell-row list (stream-ordered scratch)
     if (!force_generic && R->dim == 2 && c->kind == WGQ_COEF_FOURIER_LOGN && a.coef.n_modes > 0) {
         // the 2D tensor-core kernel in load mode (its exponent product and exp, no y / x stages),
@@ -1169,12 +1182,12 @@ int launch_load(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, 
     }
     rc = WGQ_EUNSUPPORTED;
     switch (R->p * 10 + R->dim) {
-        case 21: rc = launch_load_pd<2, 1>(a, PW, b, st); break;
-        case 22: rc = launch_load_pd<2, 2>(a, PW, b, st); break;
-        case 23: rc = launch_load_pd<2, 3>(a, PW, b, st); break;
-        case 31: rc = launch_load_pd<3, 1>(a, PW, b, st); break;
-        case 32: rc = launch_load_pd<3, 2>(a, PW, b, st); break;
-        case 33: rc = launch_load_pd<3, 3>(a, PW, b, st); break;
+        case 21: rc = launch_load_pd<2, 1>(a, PW, b, !force_generic, st); break;
+        case 22: rc = launch_load_pd<2, 2>(a, PW, b, !force_generic, st); break;
+        case 23: rc = launch_load_pd<2, 3>(a, PW, b, !force_generic, st); break;
+        case 31: rc = launch_load_pd<3, 1>(a, PW, b, !force_generic, st); break;
+        case 32: rc = launch_load_pd<3, 2>(a, PW, b, !force_generic, st); break;
+        case 33: rc = launch_load_pd<3, 3>(a, PW, b, !force_generic, st); break;
     }
     if (shell) cudaFreeAsync(shell, st);
     if (tab) cudaFreeAsync(tab, st);
@@ -1182,19 +1195,21 @@ int launch_load(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, 
     return rc;
 }
 
-int launch_apply(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, const double* u, int64_t u_row0,
+int launch_apply(const wgq_rules_s* R, const Tables3& TT, const wgq_coeff_t* c, const double* u, int64_t u_row0,
                  int64_t row_begin, int64_t row_end, double* yM, double* yK, void* stream) {
     if (row_end <= row_begin) return WGQ_OK;
-    static const bool force_generic = [] {
+    static const bool force_generic_env = [] {
         const char* e = getenv("WGQ_FORCE_GENERIC");
         return e && e[0] == '1';
     }();
+    const bool force_generic = force_generic_env || !R->iso;     // specialised kernels: equal counts
+    const RowTables& T = TT.t[0];
     if (!force_generic && line_apply_applies(R, c))
         return launch_line_apply(R, T, c, u, u_row0, row_begin, row_end, yM, yK, stream);
     if (!force_generic && sep_applies(c))
         return launch_sep_apply(R, T, c, u, u_row0, row_begin, row_end, yM, yK, stream);
     cudaStream_t st = (cudaStream_t)stream;
-    GenericArgs a = base_args(R, T, c, row_begin, row_end);
+    GenericArgs a = base_args(R, TT, c, row_begin, row_end);
     a.apply = 1;
     a.u = u;
     a.u_row0 = u_row0;
@@ -1204,7 +1219,7 @@ int launch_apply(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c,
     a.do_stiff = yK != nullptr;
     a.M.layout = WGQ_ELL;
     double* tab = nullptr;
-    int rc = coef_tables(R, T, a, c, st, &tab);
+    int rc = coef_tables(R, a, c, st, &tab);
     if (rc != WGQ_OK) return rc;
     int64_t* shell = nullptr;            // 2D shell-row list (stream-ordered scratch)
     if (!force_generic && R->dim == 2 && c->kind == WGQ_COEF_FOURIER_LOGN && a.coef.n_modes > 0) {

@@ -24,36 +24,37 @@ __device__ __host__ __forceinline__ int64_t prefix_1d(int64_t r, int p, int64_t 
     return r * (2 * p + 1) - (q * p - q * (q - 1) / 2) - u * (u + 1) / 2;
 }
 
-// global number of nonzeros before row i (lexicographic, x fastest)
-__device__ __host__ __forceinline__ int64_t nnz_before(int64_t row, int p, int64_t N, int dim) {
-    const int64_t S = prefix_1d(N, p, N);
+// global number of nonzeros before row i (lexicographic, x fastest); per-direction sizes
+__device__ __host__ __forceinline__ int64_t nnz_before(int64_t row, int p, const Dims& D) {
+    const int dim = D.dim;
     int64_t idx[3] = {0, 0, 0};
     int64_t rem = row;
     for (int q = 0; q < dim - 1; ++q) {
-        idx[q] = rem % N;
-        rem /= N;
+        idx[q] = rem % D.N[q];
+        rem /= D.N[q];
     }
-    idx[dim - 1] = rem;                  // may equal N for row == N^dim (end of the matrix)
+    idx[dim - 1] = rem;                  // may equal N_d for row == rows (end of the matrix)
     int64_t width = 1;
     // rows are ordered by (i_d, ..., i_1): accumulate from the slowest direction
     int64_t acc = 0;
     for (int q = dim - 1; q >= 0; --q) {
         int64_t Sp = 1;
-        for (int k = 0; k < q; ++k) Sp *= S;
-        acc += width * prefix_1d(idx[q], p, N) * Sp;
-        width *= cols_1d(idx[q], p, N);
+        for (int k = 0; k < q; ++k) Sp *= prefix_1d(D.N[k], p, D.N[k]);
+        acc += width * prefix_1d(idx[q], p, D.N[q]) * Sp;
+        width *= cols_1d(idx[q], p, D.N[q]);
     }
     return acc;
 }
 
-__global__ void k_row_ptr(int p, int64_t N, int dim, int64_t row_begin, int64_t rows, int64_t* row_ptr) {
-    const int64_t base = nnz_before(row_begin, p, N, dim);
+__global__ void k_row_ptr(int p, const Dims D, int64_t row_begin, int64_t rows, int64_t* row_ptr) {
+    const int64_t base = nnz_before(row_begin, p, D);
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t <= rows; t += (int64_t)gridDim.x * blockDim.x)
-        row_ptr[t] = nnz_before(row_begin + t, p, N, dim) - base;
+        row_ptr[t] = nnz_before(row_begin + t, p, D) - base;
 }
 
-__global__ void k_col_idx(int p, int64_t N, int dim, int64_t row_begin, int64_t rows, const int64_t* row_ptr,
+__global__ void k_col_idx(int p, const Dims D, int64_t row_begin, int64_t rows, const int64_t* row_ptr,
                           int32_t* col_idx) {
+    const int dim = D.dim;
     const int S = 2 * p + 1;
     int NS = 1;
     for (int q = 0; q < dim; ++q) NS *= S;
@@ -66,6 +67,7 @@ __global__ void k_col_idx(int p, int64_t N, int dim, int64_t row_begin, int64_t 
         bool ok = true;
         int s = slot;
         for (int q = 0; q < dim; ++q) {
+            const int64_t N = D.N[q];
             const int64_t i = rem % N;
             rem /= N;
             const int o = s % S - p;
@@ -94,20 +96,16 @@ __device__ __forceinline__ double greville(int64_t j, int p, int64_t n) {
     return s / p;
 }
 
-__global__ void k_row_moments(int p, int64_t n, int dim, int64_t row_begin, int64_t rows, const double* vals,
-                              int64_t ld, double* out) {
-    const int64_t N = n + p;
+__global__ void k_row_moments(int p, const Dims D, int64_t row_begin, int64_t rows, const double* vals, int64_t ld,
+                              double* out) {
+    const int dim = D.dim;
     const int S = 2 * p + 1;
     int NS = 1;
     for (int q = 0; q < dim; ++q) NS *= S;
     for (int64_t orow = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; orow < rows;
          orow += (int64_t)gridDim.x * blockDim.x) {
-        int64_t idx[3] = {0, 0, 0};
-        int64_t rem = row_begin + orow;
-        for (int q = 0; q < dim; ++q) {
-            idx[q] = rem % N;
-            rem /= N;
-        }
+        int64_t idx[3];
+        D.decode(row_begin + orow, idx);
         double m[4] = {0.0, 0.0, 0.0, 0.0};
         for (int slot = 0; slot < NS; ++slot) {
             int s = slot;
@@ -116,8 +114,8 @@ __global__ void k_row_moments(int p, int64_t n, int dim, int64_t row_begin, int6
             for (int q = 0; q < dim; ++q) {
                 const int64_t j = idx[q] + (s % S) - p;
                 s /= S;
-                if (j < 0 || j >= N) ok = false;
-                else g[q] = greville(j, p, n);
+                if (j < 0 || j >= D.N[q]) ok = false;
+                else g[q] = greville(j, p, D.n[q]);
             }
             if (!ok) continue;
             const double v = vals[orow * ld + slot];
@@ -134,7 +132,7 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
     return z ^ (z >> 31);
 }
 
-__global__ void k_checksum(int p, int64_t N, int dim, int64_t row_begin, int64_t rows, const double* vals, int64_t ld,
+__global__ void k_checksum(int p, int dim, int64_t row_begin, int64_t rows, const double* vals, int64_t ld,
                            unsigned long long* out) {
     const int S = 2 * p + 1;
     int NS = 1;
@@ -171,23 +169,23 @@ unsigned grid_for(int64_t total) {
 
 }  // namespace
 
-int64_t host_nnz_before(int64_t row, int p, int64_t N, int dim) { return nnz_before(row, p, N, dim); }
+int64_t host_nnz_before(int64_t row, int p, const Dims& D) { return nnz_before(row, p, D); }
 
 int launch_csr_structure(const wgq_rules_s* R, int64_t row_begin, int64_t row_end, int64_t* row_ptr, int32_t* col_idx,
                          void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t rows = row_end - row_begin;
-    k_row_ptr<<<grid_for(rows + 1), 256, 0, st>>>(R->p, R->N, R->dim, row_begin, rows, row_ptr);
+    k_row_ptr<<<grid_for(rows + 1), 256, 0, st>>>(R->p, R->dims, row_begin, rows, row_ptr);
     int NS = 1;
     for (int q = 0; q < R->dim; ++q) NS *= 2 * R->p + 1;
-    if (rows > 0) k_col_idx<<<grid_for(rows * NS), 256, 0, st>>>(R->p, R->N, R->dim, row_begin, rows, row_ptr, col_idx);
+    if (rows > 0) k_col_idx<<<grid_for(rows * NS), 256, 0, st>>>(R->p, R->dims, row_begin, rows, row_ptr, col_idx);
     return cudaGetLastError() == cudaSuccess ? WGQ_OK : WGQ_ECUDA;
 }
 
 int launch_row_moments(const wgq_rules_s* R, const wgq_out_t* A, double* out, void* stream) {
     const int64_t rows = A->row_end - A->row_begin;
     if (rows <= 0) return WGQ_OK;
-    k_row_moments<<<grid_for(rows), 256, 0, (cudaStream_t)stream>>>(R->p, R->n, R->dim, A->row_begin, rows, A->values,
+    k_row_moments<<<grid_for(rows), 256, 0, (cudaStream_t)stream>>>(R->p, R->dims, A->row_begin, rows, A->values,
                                                                      A->ld, out);
     return cudaGetLastError() == cudaSuccess ? WGQ_OK : WGQ_ECUDA;
 }
@@ -199,7 +197,7 @@ int launch_checksum(const wgq_rules_s* R, const wgq_out_t* A, unsigned long long
     if (rows <= 0) return WGQ_OK;
     int NS = 1;
     for (int q = 0; q < R->dim; ++q) NS *= 2 * R->p + 1;
-    k_checksum<<<grid_for(rows * NS), 256, 0, st>>>(R->p, R->N, R->dim, A->row_begin, rows, A->values, A->ld, out);
+    k_checksum<<<grid_for(rows * NS), 256, 0, st>>>(R->p, R->dim, A->row_begin, rows, A->values, A->ld, out);
     return cudaGetLastError() == cudaSuccess ? WGQ_OK : WGQ_ECUDA;
 }
 

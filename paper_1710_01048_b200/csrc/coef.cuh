@@ -21,29 +21,30 @@ struct CoefDev {
 
 // Multilinear interpolation of the vertex field (R6).  The cell is the element that
 // contains the point; the slowest axis is slab-local (plane0).
+// n: elements per direction (vertex j of direction a at j / n[a]; planes of (n[1]+1) x (n[0]+1))
 template <int D>
-__device__ __forceinline__ double grid_eval(const CoefDev& c, int64_t n, const double* x) {
+__device__ __forceinline__ double grid_eval(const CoefDev& c, const int64_t* n, const double* x) {
     int64_t e[3];
     double f[3];
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-        double s = __dmul_rn(x[a], (double)n);
+        double s = __dmul_rn(x[a], (double)n[a]);
         int64_t k = (int64_t)floor(s);
-        k = k < 0 ? 0 : (k > n - 1 ? n - 1 : k);
+        k = k < 0 ? 0 : (k > n[a] - 1 ? n[a] - 1 : k);
         e[a] = k;
         f[a] = s - (double)k;
     }
-    const int64_t nv = n + 1;
+    const int64_t nvx = n[0] + 1, nvy = D >= 2 ? n[1] + 1 : 1;
     double out = 0.0;
     if (D == 1) {
         const double* g = c.grid + (e[0] - c.plane0);
         out = (1.0 - f[0]) * g[0] + f[0] * g[1];
     } else if (D == 2) {
-        const double* g = c.grid + (e[1] - c.plane0) * nv + e[0];
-        out = (1.0 - f[1]) * ((1.0 - f[0]) * g[0] + f[0] * g[1]) + f[1] * ((1.0 - f[0]) * g[nv] + f[0] * g[nv + 1]);
+        const double* g = c.grid + (e[1] - c.plane0) * nvx + e[0];
+        out = (1.0 - f[1]) * ((1.0 - f[0]) * g[0] + f[0] * g[1]) + f[1] * ((1.0 - f[0]) * g[nvx] + f[0] * g[nvx + 1]);
     } else {
-        const double* g = c.grid + ((e[2] - c.plane0) * nv + e[1]) * nv + e[0];
-        const int64_t sy = nv, sz = nv * nv;
+        const double* g = c.grid + ((e[2] - c.plane0) * nvy + e[1]) * nvx + e[0];
+        const int64_t sy = nvx, sz = nvx * nvy;
         double c00 = (1.0 - f[0]) * g[0] + f[0] * g[1];
         double c10 = (1.0 - f[0]) * g[sy] + f[0] * g[sy + 1];
         double c01 = (1.0 - f[0]) * g[sz] + f[0] * g[sz + 1];
@@ -54,7 +55,7 @@ __device__ __forceinline__ double grid_eval(const CoefDev& c, int64_t n, const d
 }
 
 template <int D>
-__device__ __forceinline__ double coef_eval(const CoefDev& c, int64_t n, const double* x) {
+__device__ __forceinline__ double coef_eval(const CoefDev& c, const int64_t* n, const double* x) {
     switch (c.kind) {
         case WGQ_COEF_CONST:
             return c.c0;

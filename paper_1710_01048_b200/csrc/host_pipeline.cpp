@@ -63,7 +63,7 @@ extern "C" int wgq_assemble_host(wgq_rules_t R, const wgq_coeff_t* c, int64_t ro
     if (c->kind == WGQ_COEF_GRID) {
         if (!c->grid) return WGQ_EINVAL;
         int64_t plane = 1;
-        for (int q = 0; q < R->dim - 1; ++q) plane *= R->n + 1;
+        for (int q = 0; q < R->dim - 1; ++q) plane *= R->dims.n[q] + 1;
         const size_t bytes = (size_t)c->grid_planes * plane * sizeof(double);   // plane = 1 in 1D
         if (cudaMalloc(&cl.dev[0], bytes) != cudaSuccess) return WGQ_ECUDA;
         if (cudaMemcpyAsync(cl.dev[0], c->grid, bytes, cudaMemcpyHostToDevice, comp) != cudaSuccess) return WGQ_ECUDA;

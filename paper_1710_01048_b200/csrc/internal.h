@@ -12,6 +12,12 @@
 
 #include <nvtx3/nvToolsExt.h>
 
+#ifdef __CUDACC__
+#define WGQ_HD __host__ __device__
+#else
+#define WGQ_HD
+#endif
+
 namespace wgq {
 
 // NVTX range over a library call (SURVEY §5 tracing: rules, tables, grid generation, assembly,
@@ -24,6 +30,34 @@ struct NvtxRange {
 };
 
 constexpr int kMaxP = 3;
+
+// Mesh sizes per direction (eq:Gmap3 P:113-120: every parameter direction has its own element
+// count n_EL^i; eq:DimMulti P:134-136): n[a] elements and N[a] = n[a] + p basis functions in
+// direction a < dim (entries past dim are 1).  Rows are lexicographic with x fastest:
+// i = i_1 + N_1 (i_2 + N_2 i_3).
+struct Dims {
+    int dim = 1;
+    int64_t n[3] = {1, 1, 1};
+    int64_t N[3] = {1, 1, 1};
+    WGQ_HD int64_t rows() const { return N[0] * N[1] * N[2]; }
+    // rows of one slab unit along the slowest axis (a line in 2D, a plane in 3D)
+    WGQ_HD int64_t plane_rows() const {
+        int64_t r = 1;
+        for (int a = 0; a < dim - 1; ++a) r *= N[a];
+        return r;
+    }
+    WGQ_HD void decode(int64_t row, int64_t* idx) const {
+        for (int a = 0; a < 3; ++a) {
+            idx[a] = a < dim ? row % N[a] : 0;
+            if (a < dim) row /= N[a];
+        }
+    }
+    WGQ_HD bool iso() const {
+        for (int a = 1; a < dim; ++a)
+            if (n[a] != n[0]) return false;
+        return true;
+    }
+};
 constexpr int kMaxS = 2 * kMaxP + 1;   // stencil width per direction
 constexpr int kMaxNodes = 12;          // per direction: GL(p+1) on up to p elements (R1, WGQ_BND_GL)
 constexpr int kMaxMassNodes = kMaxNodes;
@@ -72,14 +106,21 @@ struct RowTables {
     double iAwK[kMaxP + 1][kMaxS] = {};
 };
 
+// The row tables of every direction (t[a] = t[0] on an isotropic mesh).
+struct Tables3 {
+    RowTables t[3];
+};
+
 }  // namespace wgq
 
 struct wgq_rules_s {
     int p = 0;
     int dim = 0;
     int bnd = WGQ_BND_GAUSS;
-    int64_t n = 0;
+    int64_t n = 0;             // direction 0 (every direction when the mesh is isotropic)
     int64_t N = 0;
+    wgq::Dims dims;            // per-direction sizes
+    bool iso = true;           // equal element counts in every direction (the specialised kernels)
     // rules[kind][cls]: cls 0..p-1 = left boundary weight j, cls p = interior
     wgq::ClassRule rules[2][wgq::kMaxP + 1];
     std::mutex mu;
@@ -101,7 +142,7 @@ void interior_vertex_tables(int p, const ClassRule& mass, const ClassRule& stiff
 void eval_counts(const wgq_rules_s* R, int kind, int64_t* gaussian, int64_t* newton_cotes);
 
 // tables.cu
-int build_row_tables(const wgq_rules_s* R, RowTables* T, void* stream);
+int build_row_tables(const wgq_rules_s* R, int64_t n, RowTables* T, void* stream);   // one direction, n elements
 void free_row_tables(RowTables* T);
 
 // assemble.cu
@@ -111,7 +152,7 @@ void free_row_tables(RowTables* T);
 int shell_rows_2d(const wgq_rules_s* R, int64_t row_begin, int64_t row_end, cudaStream_t st, int64_t** rows,
                   int64_t* count);
 #endif
-int launch_assemble(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c,
+int launch_assemble(const wgq_rules_s* R, const Tables3& TT, const wgq_coeff_t* c,
                     const wgq_out_t* M, const wgq_out_t* K, void* stream);
 int launch_csr_structure(const wgq_rules_s* R, int64_t row_begin, int64_t row_end,
                          int64_t* row_ptr, int32_t* col_idx, void* stream);
@@ -119,9 +160,9 @@ int launch_row_moments(const wgq_rules_s* R, const wgq_out_t* A, double* out, vo
 int launch_checksum(const wgq_rules_s* R, const wgq_out_t* A, unsigned long long* out, void* stream);
 
 // load vector / matrix-free application (assemble.cu)
-int launch_load(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, int64_t row_begin, int64_t row_end,
+int launch_load(const wgq_rules_s* R, const Tables3& TT, const wgq_coeff_t* c, int64_t row_begin, int64_t row_end,
                 double* b, void* stream);
-int launch_apply(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, const double* u, int64_t u_row0,
+int launch_apply(const wgq_rules_s* R, const Tables3& TT, const wgq_coeff_t* c, const double* u, int64_t u_row0,
                  int64_t row_begin, int64_t row_end, double* yM, double* yK, void* stream);
 
 // assemble_line.cu (GRID coefficient, d = 3, ELL)
@@ -145,7 +186,7 @@ bool f2d_interior_applies(const wgq_rules_s* R, const RowTables& T, const wgq_co
 int launch_f2d_interior(const wgq_rules_s* R, const RowTables& T, const double* ctab, int cw, const wgq_out_t* M,
                         const wgq_out_t* K, cudaStream_t st);
 #endif
-int fetch_interior_tables(const wgq_rules_s* R, RowTables* T);
+int fetch_interior_tables(const wgq_rules_s* R, int64_t n, RowTables* T);
 
 // separable.cu (CONST, TRIG_SEP coefficients)
 bool sep_applies(const wgq_coeff_t* c);
@@ -153,7 +194,7 @@ int launch_sep(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, c
                const wgq_out_t* K, void* stream);
 
 // grid.cu
-int launch_generate_grid(int64_t n, int dim, uint64_t seed, double sigma, int64_t plane0,
+int launch_generate_grid(const int64_t* n, int dim, uint64_t seed, double sigma, int64_t plane0,
                          int64_t planes, double* grid, void* stream);
 
 

@@ -486,9 +486,10 @@ int build_class_rules(int p, int bnd, ClassRule out[2][kMaxP + 1]) {
 // here and for the weighted Newton-Cotes point set of Calabro et al. (the knots and element
 // midpoints of supp B_r).  A tensor row costs the product over directions, so
 // the n^d mesh costs (sum_r count(r))^d.
-void eval_counts(const wgq_rules_s* R, int kind, int64_t* gaussian, int64_t* newton_cotes) {
+namespace {
+void eval_counts_1d(const wgq_rules_s* R, int kind, int64_t n, int64_t* g_out, int64_t* nc_out) {
     const int p = R->p;
-    const int64_t n = R->n, N = R->N;
+    const int64_t N = n + p;
     const int order = kind == WGQ_MASS ? 0 : 1;
     Knots K = unit_open_knots(p, (int)n);
     auto nonzero_at = [&](int64_t r, real x) {
@@ -514,8 +515,18 @@ void eval_counts(const wgq_rules_s* R, int kind, int64_t* gaussian, int64_t* new
             if (fabsl(bval(K, (int)r, x, order)) > 1e-12L) nc += nonzero_at(r, x);
         }
     }
+    *g_out = g;
+    *nc_out = nc;
+}
+}  // namespace
+
+// A tensor row costs the product of its directions' counts: the mesh costs the product over
+// directions of the per-direction sums (each direction with its own element count).
+void eval_counts(const wgq_rules_s* R, int kind, int64_t* gaussian, int64_t* newton_cotes) {
     int64_t G = 1, C = 1;
     for (int a = 0; a < R->dim; ++a) {
+        int64_t g = 0, nc = 0;
+        eval_counts_1d(R, kind, R->dims.n[a], &g, &nc);
         G *= g;
         C *= nc;
     }

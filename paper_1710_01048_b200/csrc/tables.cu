@@ -186,8 +186,8 @@ __global__ void k_weighted_tables(RowTables T) {
 
 }  // namespace
 
-int build_row_tables(const wgq_rules_s* R, RowTables* T, void* stream) {
-    const int64_t N = R->N;
+int build_row_tables(const wgq_rules_s* R, int64_t n_dir, RowTables* T, void* stream) {
+    const int64_t N = n_dir + R->p;
     size_t bytes = 2 * N * sizeof(int) +
                    N * (kMaxMassNodes * (2 + kMaxS) + kMaxStiffNodes * (2 + kMaxS) + 2 * kMaxV * kMaxS) * sizeof(double);
     bytes += N * 64 * sizeof(double);          // AW
@@ -215,7 +215,7 @@ int build_row_tables(const wgq_rules_s* R, RowTables* T, void* stream) {
     }
     ClassArgs A{};
     A.p = R->p;
-    A.n = R->n;
+    A.n = n_dir;
     A.N = N;
     for (int kind = 0; kind < 2; ++kind)
         for (int c = 0; c <= R->p; ++c) {
@@ -228,16 +228,16 @@ int build_row_tables(const wgq_rules_s* R, RowTables* T, void* stream) {
     const int64_t threads = N * 2 * kMaxStiffNodes;
     k_row_tables<<<(unsigned)((threads + 255) / 256), 256, 0, (cudaStream_t)stream>>>(A, *T);
     const int64_t vthreads = N * 2 * kMaxV * kMaxS;
-    k_vertex_tables<<<(unsigned)((vthreads + 255) / 256), 256, 0, (cudaStream_t)stream>>>(R->p, R->n, *T);
+    k_vertex_tables<<<(unsigned)((vthreads + 255) / 256), 256, 0, (cudaStream_t)stream>>>(R->p, n_dir, *T);
     k_weighted_tables<<<(unsigned)((N * 64 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(*T);
     if (cudaGetLastError() != cudaSuccess) return WGQ_ECUDA;
     return WGQ_OK;
 }
 
-int fetch_interior_tables(const wgq_rules_s* R, RowTables* T) {
+int fetch_interior_tables(const wgq_rules_s* R, int64_t n_dir, RowTables* T) {
     T->int_ok = false;
     const int64_t r = 2 * R->p;                  // first class-I row (class I: 2p <= r <= n-1-p)
-    if (r > R->n - 1 - R->p) return WGQ_OK;      // no class-I rows on this mesh
+    if (r > n_dir - 1 - R->p) return WGQ_OK;     // no class-I rows on this mesh
     int m[2];
     double w[2][kMaxNodes], A[2][kMaxNodes * kMaxS];
     if (cudaMemcpy(&m[0], T->mM + r, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess ||

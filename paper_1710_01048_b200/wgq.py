@@ -58,6 +58,8 @@ def lib():
         "wgq_version": (ctypes.c_char_p, []),
         "wgq_build_rules": (c_int, [c_int, c_i64, c_int, ctypes.POINTER(vp)]),
         "wgq_build_rules_ex": (c_int, [c_int, c_i64, c_int, c_int, ctypes.POINTER(vp)]),
+        "wgq_build_rules_ex2": (c_int, [c_int, ctypes.POINTER(c_i64), c_int, c_int, ctypes.POINTER(vp)]),
+        "wgq_rules_dims": (c_int, [vp, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),
         "wgq_free_rules": (None, [vp]),
         "wgq_rules_info": (c_int, [vp, ctypes.POINTER(c_int), ctypes.POINTER(c_i64), ctypes.POINTER(c_int),
                                    ctypes.POINTER(c_i64), ctypes.POINTER(c_i64), ctypes.POINTER(c_int)]),
@@ -72,6 +74,8 @@ def lib():
         "wgq_assemble_load": (c_int, [vp, ctypes.POINTER(wgq_coeff_t), c_i64, c_i64, vp, vp]),
         "wgq_apply": (c_int, [vp, ctypes.POINTER(wgq_coeff_t), vp, c_i64, c_i64, c_i64, c_i64, vp, vp, vp]),
         "wgq_generate_grid": (c_int, [c_i64, c_int, ctypes.c_uint64, ctypes.c_double, c_i64, c_i64, vp, vp]),
+        "wgq_generate_grid_ex": (c_int, [ctypes.POINTER(c_i64), c_int, ctypes.c_uint64, ctypes.c_double, c_i64, c_i64,
+                                         vp, vp]),
         "wgq_row_moments": (c_int, [vp, ctypes.POINTER(wgq_out_t), vp, vp]),
         "wgq_checksum": (c_int, [vp, ctypes.POINTER(wgq_out_t), vp, vp]),
         "wgq_assemble_host": (c_int, [vp, ctypes.POINTER(wgq_coeff_t), c_i64, c_i64, vp, vp, c_i64, c_i64]),
@@ -87,7 +91,8 @@ def lib():
 
 
 def exported_symbols():
-    return ["wgq_strerror", "wgq_version", "wgq_build_rules", "wgq_build_rules_ex", "wgq_free_rules",
+    return ["wgq_strerror", "wgq_version", "wgq_build_rules", "wgq_build_rules_ex", "wgq_build_rules_ex2",
+            "wgq_rules_dims", "wgq_generate_grid_ex", "wgq_free_rules",
             "wgq_rules_info", "wgq_rules_query", "wgq_nnz", "wgq_eval_counts", "wgq_assemble_mass", "wgq_assemble_stiffness",
             "wgq_assemble_mass_stiffness", "wgq_csr_structure", "wgq_assemble_load", "wgq_apply",
             "wgq_generate_grid", "wgq_row_moments",
@@ -112,13 +117,25 @@ def _stream(stream):
 # rules
 # ---------------------------------------------------------------------------------------
 class Rules:
-    """Owns a wgq_rules_t handle (wgq_build_rules_ex / wgq_free_rules)."""
+    """Owns a wgq_rules_t handle (wgq_build_rules_ex2 / wgq_free_rules).
+
+    n_elems: elements per direction, an int (every direction) or one count per direction
+    (eq:Gmap3 P:113-120).  Attributes: ns / Ns (per-direction elements / rows), n / N (those of
+    direction 0, the value of every direction on an isotropic mesh), n_rows, stencil."""
 
     def __init__(self, p, n_elems, dim, boundary_mode=WGQ_BND_GAUSS):
+        ns = [int(n_elems)] * dim if np.ndim(n_elems) == 0 else [int(v) for v in n_elems]
+        if len(ns) != dim:
+            raise ValueError(f"n_elems: expected {dim} counts, got {len(ns)}")
         h = ctypes.c_void_p()
-        _check("wgq_build_rules_ex", lib().wgq_build_rules_ex(p, n_elems, dim, boundary_mode, ctypes.byref(h)))
+        arr = (ctypes.c_int64 * 3)(*(ns + [1] * (3 - dim)))
+        _check("wgq_build_rules_ex2", lib().wgq_build_rules_ex2(p, arr, dim, boundary_mode, ctypes.byref(h)))
         self.handle = h
-        self.p, self.n, self.dim = p, n_elems, dim
+        self.p, self.dim = p, dim
+        self.ns = tuple(ns)
+        self.Ns = tuple(v + p for v in ns)
+        self.iso = all(v == ns[0] for v in ns)
+        self.n = ns[0]
         info = wgq_rules_info(self)
         self.N, self.n_rows, self.stencil = info["n_rows_1d"], info["n_rows"], info["stencil"]
 
@@ -288,9 +305,13 @@ def wgq_apply(rules, coeff, u, u_row0, row_begin, row_end, yM=None, yK=None, str
 
 
 def wgq_generate_grid(n_elems, dim, seed, sigma, plane0, planes, grid, stream=None):
-    _need(grid, "grid", numel=planes * (n_elems + 1) ** (dim - 1) if dim > 1 else n_elems + 1)
-    _check("wgq_generate_grid", lib().wgq_generate_grid(n_elems, dim, seed, sigma, plane0, planes, grid.data_ptr(),
-                                                        _stream(stream)))
+    """n_elems: an int (every direction) or one count per direction (wgq_generate_grid_ex)."""
+    ns = [int(n_elems)] * dim if np.ndim(n_elems) == 0 else [int(v) for v in n_elems]
+    plane = int(np.prod([v + 1 for v in ns[:dim - 1]])) if dim > 1 else 1
+    _need(grid, "grid", numel=planes * plane if dim > 1 else ns[0] + 1)
+    arr = (ctypes.c_int64 * 3)(*(ns + [1] * (3 - dim)))
+    _check("wgq_generate_grid_ex", lib().wgq_generate_grid_ex(arr, dim, seed, sigma, plane0, planes, grid.data_ptr(),
+                                                              _stream(stream)))
 
 
 def wgq_row_moments(rules, A, out, stream=None):
