@@ -536,6 +536,20 @@ def run_extras(rules5, coef5, peak):
         out["configs"][cfg["name"]] = {"ms": round(ms, 4), "nnz_per_s": nnz / (ms / 1e3),
                                        "hbm_gbs": round(alg / ms / 1e6, 1), "hbm_frac": round(alg / ms / 1e6 / peak, 4)}
         del o
+    # C5 with a different element count per direction (eq:Gmap3 P:113-120): 256 x 256 x 192,
+    # the same GRID kernel and coefficient recipe
+    ra = wgq.Rules(3, (256, 256, 192), 3)
+    ga, la = api.make_grid(ra, inputs.SEED, 0.5, 0, ra.n_rows)
+    ca = api.coefficient({"kind": "grid"}, ga, la)
+    oa = {k: api.alloc_ell(ra, 0, ra.n_rows) for k in ("mass", "stiffness")}
+    ms = _time_ms(lambda: api.assemble(ra, ca, out=oa), flush=flush)
+    alg = ra.n_rows * ra.stencil * 8 * 2
+    nnz = wgq.wgq_nnz(ra, 0, ra.n_rows) * 2
+    out["configs"]["3d_p3_n256x256x192_mk_grid"] = {"ms": round(ms, 4), "rows": ra.n_rows, "nnz_per_s": nnz / (ms / 1e3),
+                                                    "hbm_gbs": round(alg / ms / 1e6, 1),
+                                                    "hbm_frac": round(alg / ms / 1e6 / peak, 4)}
+    del oa, ga, ca
+    torch.cuda.empty_cache()
     # C5 in CSR layout (values of both matrices; the closed-form structure is built once, untimed)
     nnz5 = wgq.wgq_nnz(rules5, 0, rules5.n_rows)
     row_ptr = torch.empty(rules5.n_rows + 1, dtype=torch.int64, device="cuda")

@@ -1078,7 +1078,8 @@ int launch_assemble(const wgq_rules_s* R, const Tables3& TT, const wgq_coeff_t* 
     // the specialised kernels assume equal element counts in every direction
     const bool force_generic = force_generic_env || !R->iso;
     const RowTables& T = TT.t[0];
-    if (!force_generic && line_kernel_applies(R, c, M, K)) return launch_line(R, T, c, M, K, stream);
+    // the GRID line kernel takes per-direction sizes itself
+    if (!force_generic_env && line_kernel_applies(R, c, M, K)) return launch_line(R, TT, c, M, K, stream);
     if (!force_generic && sep_applies(c)) return launch_sep(R, T, c, M, K, stream);
     GenericArgs a{};
     set_dirs(a, R, TT);
@@ -1204,8 +1205,8 @@ int launch_apply(const wgq_rules_s* R, const Tables3& TT, const wgq_coeff_t* c, 
     }();
     const bool force_generic = force_generic_env || !R->iso;     // specialised kernels: equal counts
     const RowTables& T = TT.t[0];
-    if (!force_generic && line_apply_applies(R, c))
-        return launch_line_apply(R, T, c, u, u_row0, row_begin, row_end, yM, yK, stream);
+    if (!force_generic_env && line_apply_applies(R, c))
+        return launch_line_apply(R, TT, c, u, u_row0, row_begin, row_end, yM, yK, stream);
     if (!force_generic && sep_applies(c))
         return launch_sep_apply(R, T, c, u, u_row0, row_begin, row_end, yM, yK, stream);
     cudaStream_t st = (cudaStream_t)stream;

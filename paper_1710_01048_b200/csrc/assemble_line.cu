@@ -65,10 +65,12 @@ __device__ __forceinline__ int ring_slot(int c) {
 }
 
 struct LineArgs {
-    RowTables T;
+    RowTables T;                 // x-row tables (direction 0)
+    RowTables Ty, Tz;            // line tables of directions 1, 2 (= T on an isotropic mesh)
     const double* grid;
     int plane0, planes;
-    int n, N;
+    int n, N;                    // x: elements, rows per line
+    int ny, nz, Ny, Nz;          // y, z: elements, rows (eq:Gmap3: each direction its own count)
     int row_begin, row_end;
     double* M;
     double* K;
@@ -142,9 +144,9 @@ __device__ __forceinline__ void patch_row_init(const LineArgs& a, PatchRow& pr, 
     constexpr int V = P + 2;
     const int r = tid >> 3, vy = r % V, vz = r / V;
     const int y = max(0, i2 - P) + vy, z = max(0, i3 - P) + vz;
-    const int nv = a.n + 1;
-    const bool ok = r < V * V && y <= a.n && z <= a.n && z - a.plane0 < a.planes;
-    pr.base = ok ? a.grid + ((size_t)(z - a.plane0) * nv + y) * nv : nullptr;
+    const int nvx = a.n + 1, nvy = a.ny + 1;
+    const bool ok = r < V * V && y <= a.ny && z <= a.nz && z - a.plane0 < a.planes;
+    pr.base = ok ? a.grid + ((size_t)(z - a.plane0) * nvy + y) * nvx : nullptr;
 }
 
 // Issue the vertex patch of planes [c0, c0+nnew): patch[j][vz][vy]; out-of-range vertices
@@ -281,8 +283,8 @@ __device__ __forceinline__ void it_planes(TileIt& t, int N) {
 
 template <int P>
 __device__ __forceinline__ void it_line(const LineArgs& a, TileIt& t) {
-    t.i2 = t.line % a.N;
-    t.i3 = t.line / a.N;
+    t.i2 = t.line % a.Ny;
+    t.i3 = t.line / a.Ny;
     t.x0 = max(a.row_begin, t.line * a.N) - t.line * a.N;
     t.x1 = min(a.row_end, t.line * a.N + a.N) - t.line * a.N;
     t.t0 = t.x0;
@@ -327,7 +329,8 @@ __device__ __forceinline__ void tile_issue(const LineArgs& a, double* patches, d
             for (int e = tid; e < 4 * V * S; e += NT) {
                 const int which = e / (V * S), v = (e / S) % V, o = e % S;
                 const int r = which < 2 ? t.i2 : t.i3;
-                cp_async8(Q + e, ((which & 1) ? a.T.PK : a.T.PM) + ((size_t)r * kMaxV + v) * kMaxS + o, true);
+                const RowTables& TL = which < 2 ? a.Ty : a.Tz;
+                cp_async8(Q + e, ((which & 1) ? TL.PK : TL.PM) + ((size_t)r * kMaxV + v) * kMaxS + o, true);
             }
         }
         load_patch<P>(a, pr, patches + t.ps * PATCH_, t.lo, t.hi - t.lo + 1, tid);
@@ -344,12 +347,14 @@ __host__ __device__ __forceinline__ long long csr_A(long long r, int p, long lon
     const long long m = r < p ? r : p, q = r - (N - p) > 0 ? r - (N - p) : 0;
     return (2 * p + 1) * r - (m * p - m * (m - 1) / 2) - q * (q + 1) / 2;
 }
-__host__ __device__ __forceinline__ long long csr_start3(long long i1, long long i2, long long i3, int p, long long N) {
-    const long long S = csr_A(N, p, N);
-    return csr_A(i3, p, N) * S * S + csr_a(i3, p, N) * (csr_A(i2, p, N) * S + csr_a(i2, p, N) * csr_A(i1, p, N));
+// per-direction sizes: S_a = A_a(N_a), start = A_z(i3) S_y S_x + a_z(i3) (A_y(i2) S_x + a_y(i2) A_x(i1))
+__host__ __device__ __forceinline__ long long csr_start3(long long i1, long long i2, long long i3, int p, long long Nx,
+                                                          long long Ny, long long Nz) {
+    const long long Sx = csr_A(Nx, p, Nx), Sy = csr_A(Ny, p, Ny);
+    return csr_A(i3, p, Nz) * Sy * Sx + csr_a(i3, p, Nz) * (csr_A(i2, p, Ny) * Sx + csr_a(i2, p, Ny) * csr_A(i1, p, Nx));
 }
-__host__ __device__ __forceinline__ long long csr_start(long long row, int p, long long N) {
-    return csr_start3(row % N, (row / N) % N, row / (N * N), p, N);
+__host__ __device__ __forceinline__ long long csr_start(long long row, int p, long long Nx, long long Ny, long long Nz) {
+    return csr_start3(row % Nx, (row / Nx) % Ny, row / (Nx * Ny), p, Nx, Ny, Nz);
 }
 
 // What every warp needs to know about a tile; written by thread 0 when the tile is prefetched.
@@ -375,14 +380,13 @@ template <int P>
 __device__ __forceinline__ TileCsr make_csr(const LineArgs& a, const TileIt& t, int last_line) {
     TileCsr d{};
     if (t.line <= last_line) {
-        const long long N = a.N;
-        d.cs0 = csr_start3(t.t0, t.i2, t.i3, P, N) - a.csr_base;     // no divisions on thread 0's path
-        d.a2 = (int)csr_a(t.i2, P, N);
-        d.w23 = d.a2 * (int)csr_a(t.i3, P, N);
+        d.cs0 = csr_start3(t.t0, t.i2, t.i3, P, a.N, a.Ny, a.Nz) - a.csr_base;   // no divisions on thread 0's path
+        d.a2 = (int)csr_a(t.i2, P, a.Ny);
+        d.w23 = d.a2 * (int)csr_a(t.i3, P, a.Nz);
         d.lo2 = max(0, P - t.i2);
-        d.hi2 = min(2 * P, (int)N - 1 - t.i2 + P);
+        d.hi2 = min(2 * P, a.Ny - 1 - t.i2 + P);
         d.lo3 = max(0, P - t.i3);
-        d.hi3 = min(2 * P, (int)N - 1 - t.i3 + P);
+        d.hi3 = min(2 * P, a.Nz - 1 - t.i3 + P);
     }
     return d;
 }
@@ -800,12 +804,13 @@ __global__ void __launch_bounds__(kApplyThreads, TRA == 8 ? 3 : 2) k_line_apply(
     auto issue = [&](const TileIt& t, PatchRow& pr) {
         if (t.line <= last_line) {
             if (t.t0 == t.x0) {                                // new line: the rows' global offsets
-                const long long N2 = (long long)N * N;
+                const long long N2 = (long long)N * a.Ny;
 #pragma unroll
                 for (int m = 0; m < MU; ++m) {
                     const int o2 = uo23[m] % S, o3 = uo23[m] / S;
                     const int iy = t.i2 - P + o2, iz = t.i3 - P + o3;
-                    ubase[m] = (iy >= 0 && iy < N && iz >= 0 && iz < N) ? (long long)iz * N2 + (long long)iy * N - a.u_row0 : -1;
+                    ubase[m] = (iy >= 0 && iy < a.Ny && iz >= 0 && iz < a.Nz) ? (long long)iz * N2 + (long long)iy * N - a.u_row0
+                                                                              : -1;
                 }
             }
             const int nx = (a.dbg & 16) ? 0 : t.uhi - t.ulo + 1;
@@ -978,7 +983,8 @@ int launch_line_mode(const LineArgs& a, int mode, cudaStream_t st) {
 bool line_kernel_applies(const wgq_rules_s* R, const wgq_coeff_t* c, const wgq_out_t* M, const wgq_out_t* K) {
     const wgq_out_t* o = M ? M : K;
     if (c->kind != WGQ_COEF_GRID || R->dim != 3) return false;
-    if (R->n < R->p + 1) return false;
+    for (int d = 0; d < 3; ++d)
+        if (R->dims.n[d] < R->p + 1) return false;
     if (o->layout == WGQ_CSR) {
         for (const wgq_out_t* x : {M, K})
             if (x && ((uintptr_t)x->values) % 16 != 0) return false;
@@ -994,25 +1000,37 @@ bool line_kernel_applies(const wgq_rules_s* R, const wgq_coeff_t* c, const wgq_o
     return true;
 }
 
-int launch_line(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, const wgq_out_t* M,
+namespace {
+void line_dims(LineArgs& a, const wgq_rules_s* R, const Tables3& TT) {
+    a.T = TT.t[0];
+    a.Ty = TT.t[1];
+    a.Tz = TT.t[2];
+    a.n = (int)R->dims.n[0];
+    a.N = (int)R->dims.N[0];
+    a.ny = (int)R->dims.n[1];
+    a.Ny = (int)R->dims.N[1];
+    a.nz = (int)R->dims.n[2];
+    a.Nz = (int)R->dims.N[2];
+}
+}  // namespace
+
+int launch_line(const wgq_rules_s* R, const Tables3& TT, const wgq_coeff_t* c, const wgq_out_t* M,
                 const wgq_out_t* K, void* stream) {
     const wgq_out_t* o = M ? M : K;
     LineArgs a{};
-    a.T = T;
+    line_dims(a, R, TT);
     a.grid = c->grid;
     a.plane0 = (int)c->grid_plane0;
     a.planes = (int)c->grid_planes;
-    a.n = (int)R->n;
-    a.N = (int)R->N;
     a.row_begin = (int)o->row_begin;
     a.row_end = (int)o->row_end;
     a.M = M ? M->values : nullptr;
     a.K = K ? K->values : nullptr;
     a.ld = o->layout == WGQ_CSR ? (2 * R->p + 1) * (2 * R->p + 1) * (2 * R->p + 1) : o->ld;
-    a.csr_base = o->layout == WGQ_CSR ? csr_start(o->row_begin, R->p, R->N) : -1;
+    a.csr_base = o->layout == WGQ_CSR ? csr_start(o->row_begin, R->p, a.N, a.Ny, a.Nz) : -1;
     const int mode = (M ? 1 : 0) | (K ? 2 : 0);
-    a.h = 1.0 / (double)R->n;
-    a.inv_h = (double)R->n;
+    a.h = 1.0 / (double)a.n;                  // x spacing: the interior x-row tables P^
+    a.inv_h = (double)a.n;
     {
         double PM[kMaxV][kMaxS], PK[kMaxV][kMaxS];
         interior_vertex_tables(R->p, R->rules[WGQ_MASS][R->p], R->rules[WGQ_STIFFNESS][R->p], PM, PK);
@@ -1029,24 +1047,25 @@ int launch_line(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, 
 }
 
 bool line_apply_applies(const wgq_rules_s* R, const wgq_coeff_t* c) {
-    return c->kind == WGQ_COEF_GRID && R->dim == 3 && R->n >= R->p + 1;
+    if (c->kind != WGQ_COEF_GRID || R->dim != 3) return false;
+    for (int d = 0; d < 3; ++d)
+        if (R->dims.n[d] < R->p + 1) return false;
+    return true;
 }
 
-int launch_line_apply(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, const double* u,
+int launch_line_apply(const wgq_rules_s* R, const Tables3& TT, const wgq_coeff_t* c, const double* u,
                       int64_t u_row0, int64_t row_begin, int64_t row_end, double* yM, double* yK, void* stream) {
     if (row_end <= row_begin) return WGQ_OK;
     LineArgs a{};
-    a.T = T;
+    line_dims(a, R, TT);
     a.grid = c->grid;
     a.plane0 = (int)c->grid_plane0;
     a.planes = (int)c->grid_planes;
-    a.n = (int)R->n;
-    a.N = (int)R->N;
     a.row_begin = (int)row_begin;
     a.row_end = (int)row_end;
     a.ld = 0;
-    a.h = 1.0 / (double)R->n;
-    a.inv_h = (double)R->n;
+    a.h = 1.0 / (double)a.n;
+    a.inv_h = (double)a.n;
     double PM[kMaxV][kMaxS], PK[kMaxV][kMaxS];
     interior_vertex_tables(R->p, R->rules[WGQ_MASS][R->p], R->rules[WGQ_STIFFNESS][R->p], PM, PK);
     for (int v = 0; v < kMaxV; ++v)

@@ -167,14 +167,14 @@ int launch_apply(const wgq_rules_s* R, const Tables3& TT, const wgq_coeff_t* c, 
 
 // assemble_line.cu (GRID coefficient, d = 3, ELL)
 bool line_kernel_applies(const wgq_rules_s* R, const wgq_coeff_t* c, const wgq_out_t* M, const wgq_out_t* K);
-int launch_line(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, const wgq_out_t* M,
+int launch_line(const wgq_rules_s* R, const Tables3& TT, const wgq_coeff_t* c, const wgq_out_t* M,
                 const wgq_out_t* K, void* stream);
 bool line_apply_applies(const wgq_rules_s* R, const wgq_coeff_t* c);
 int launch_sep_load(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, int64_t row_begin, int64_t row_end,
                     double* b, void* stream);
 int launch_sep_apply(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, const double* u, int64_t u_row0,
                      int64_t row_begin, int64_t row_end, double* yM, double* yK, void* stream);
-int launch_line_apply(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c, const double* u,
+int launch_line_apply(const wgq_rules_s* R, const Tables3& TT, const wgq_coeff_t* c, const double* u,
                       int64_t u_row0, int64_t row_begin, int64_t row_end, double* yM, double* yK, void* stream);
 
 // api.cpp: the coefficient descriptor check of the assembly calls, for a row range

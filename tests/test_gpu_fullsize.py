@@ -243,3 +243,43 @@ def test_c5_full_scale_p9_identities():
             worst["Kg"] = max(worst["Kg"], float(np.max(np.abs(km[sl, 1 + a] - kx[:, a]) / sK[sl])))
     print("C5 P9 worst relative to row max:", worst, "planes", planes)
     assert worst["M1"] < 1e-13 and worst["Mg"] < 1e-13 and worst["Kg"] < 1e-13 and worst["K1"] < 1e-12, worst
+
+
+def test_aniso_c5_sized_sampled_rows():
+    """A C5-sized mesh with a different element count per direction (256 x 256 x 192; eq:Gmap3
+    P:113-120) through the GRID line kernel, as bench.py's extras time it: sampled rows of every
+    class combination against the oracle, and (K 1)_i = 0 on every row."""
+    from paper_1710_01048_b200 import api, wgq
+    p, n, d = 3, (256, 256, 192), 3
+    rules = wgq.Rules(p, n, d)
+    Ns = rules.Ns
+    g, lo = api.make_grid(rules, inputs.SEED, 0.5, 0, rules.n_rows)
+    out = api.assemble(rules, api.coefficient({"kind": "grid"}, g, lo))
+    torch.cuda.synchronize()
+    try:
+        rng = np.random.default_rng(192)
+        rows = set()
+        while len(rows) < 400:
+            idx = []
+            for a in range(d):
+                edge = list(range(0, 2 * p + 2)) + list(range(Ns[a] - 2 * p - 2, Ns[a]))
+                idx.append(int(rng.choice(edge)) if rng.random() < 0.5 else int(rng.integers(0, Ns[a])))
+            rows.add(idx[0] + Ns[0] * (idx[1] + Ns[1] * idx[2]))
+        rows = np.array(sorted(rows))
+        host = inputs.lognormal_grid(n, seed=inputs.SEED, sigma=0.5, dim=3)
+        desc = {"kind": "grid"}
+        ref = oasm.assemble_rows(p, n, d, rows, desc, grid=host)
+        sc = oasm.assemble_rows(p, n, d, rows, desc, grid=host, absolute=True)
+        idx_t = torch.from_numpy(rows).cuda()
+        for k in ("mass", "stiffness"):
+            check_rows(out[k].index_select(0, idx_t).cpu().numpy(), ref[k], sc[k], ("aniso C5", k))
+        mom = torch.empty((rules.n_rows, 1 + d), dtype=torch.float64, device="cuda")
+        wgq.wgq_row_moments(rules, wgq.make_out(out["stiffness"], 0, rules.n_rows), mom)
+        worst = 0.0
+        for b in range(0, rules.n_rows, 1 << 22):
+            rmax = out["stiffness"][b:b + (1 << 22)].abs().amax(dim=1)
+            worst = max(worst, float((mom[b:b + (1 << 22), 0].abs() / rmax).max()))
+        assert worst < 1e-12, worst
+    finally:
+        out.clear()
+        torch.cuda.empty_cache()
