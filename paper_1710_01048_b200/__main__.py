@@ -3,6 +3,7 @@
     python -m paper_1710_01048_b200 derive-rules --degree 3 [--kind mass|stiffness] [--boundary gauss|gl] [--out rules.json]
     python -m paper_1710_01048_b200 counts --degree 2 --dim 2 --mesh 100
     python -m paper_1710_01048_b200 assemble --degree 3 --dim 3 --mesh 64 [--coef grid|const|trig|fourier]
+        (--mesh 64,64,48: one element count per direction)
                                       [--kinds mass,stiffness] [--layout ell|csr] [--mtx out_prefix]
     python -m paper_1710_01048_b200 eigen --degree 2 --dim 1 --mesh 1000 [--count 10]
 
@@ -82,7 +83,7 @@ def cmd_assemble(a):
     if any(k not in ("mass", "stiffness") for k in kinds):
         print("kinds must be mass and/or stiffness", file=sys.stderr)
         return EXIT_CONFIG
-    rules = wgq.Rules(a.degree, a.mesh, a.dim)
+    rules = wgq.Rules(a.degree, a.mesh if len(a.mesh) > 1 else a.mesh[0], a.dim)
     c = _coef(a, rules)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if a.layout == "ell":
@@ -140,7 +141,8 @@ def main(argv=None):
     s = sub.add_parser("assemble", help="assemble M and/or K on the GPU")
     s.add_argument("--degree", type=int, required=True)
     s.add_argument("--dim", type=int, required=True)
-    s.add_argument("--mesh", type=int, required=True)
+    s.add_argument("--mesh", type=lambda v: [int(x) for x in v.split(",")], required=True,
+                   help="elements per direction: one count, or one per direction (e.g. 64,64,48)")
     s.add_argument("--coef", choices=["grid", "const", "trig", "fourier"], default="const")
     s.add_argument("--kinds", default="mass,stiffness")
     s.add_argument("--layout", choices=["ell", "csr"], default="ell")
