@@ -1103,16 +1103,28 @@ int launch_assemble(const wgq_rules_s* R, const Tables3& TT, const wgq_coeff_t* 
     a.frame = 0;
     int64_t* shell = nullptr;            // 2D shell-row list (stream-ordered scratch)
     if (!force_generic && R->dim == 2 && c->kind == WGQ_COEF_FOURIER_LOGN && a.coef.n_modes > 0) {
-        // class-I rows (both indices in [2p, N-1-2p]) in the interior kernel (fourier2d.cu), the
-        // frame in the per-row tensor-core kernel over the rows whose directions all have <= 4
-        // nodes, then the generic kernel over the remaining shell (GL-fallback classes, R1)
+        // p = 3: the fused interior / frame / shell launch of fourier2d.cu; otherwise the per-row
+        // tensor-core kernel over the rows whose directions all have <= 4 nodes, then the generic
+        // kernel over the remaining shell (GL-fallback classes, R1)
         static const bool interior_on = [] {
             const char* e = getenv("WGQ_F2D_INTERIOR");
             return !(e && e[0] == '0');
         }();
         if (interior_on && f2d_interior_applies(R, T, c)) {
-            // class-I rows and the frame (per-row tables) in one launch (fourier2d.cu)
-            rc = launch_f2d_interior(R, T, tab, a.cw, M, K, st);
+            // class-I rows, the frame (per-row tables) and, when no rule has more than 8 nodes,
+            // the shell rows (split into 4-node halves) in one launch (fourier2d.cu)
+            int maxm = 0;
+            for (int cl = 0; cl <= R->p; ++cl)
+                maxm = std::max(maxm, std::max(R->rules[WGQ_MASS][cl].m, R->rules[WGQ_STIFFNESS][cl].m));
+            int64_t nsh = 0;
+            if (maxm <= 8) rc = shell_rows_2d(R, a.row_begin, a.row_end, st, &shell, &nsh);
+            else rc = WGQ_OK;
+            if (rc == WGQ_OK) rc = launch_f2d_interior(R, T, tab, a.cw, M, K, shell, nsh, st);
+            if (rc != WGQ_OK || maxm <= 8) {          // done (the generic shell pass is not needed)
+                if (shell) cudaFreeAsync(shell, st);
+                cudaFreeAsync(tab, st);
+                return rc;
+            }
         } else {
             rc = R->p == 3 ? launch_fourier2d_p<3>(a, st) : launch_fourier2d_p<2>(a, st);
         }

@@ -115,13 +115,15 @@ struct F2fArgs {
     int64_t items;            // frame work items (done before the interior items)
     const double* ctab;
     int cw;
-    const double* AW;         // RowTables::AW [N][2][4][8]
+    const double* AW;         // RowTables::AW [N][2][8][8]
     int64_t N, row_begin, row_end;
     int lo, hi;               // class-I range (the interior kernel's rows)
     int L0, nlp;              // first line of the pairing, number of line pairs
     int jA0, jA1;             // line pairs jA0 .. jA1 are interior (both lines class I)
-    int nw;                   // wide 1D indices (GL-fallback classes, > 4 nodes): left to the shell pass
+    int nw;                   // wide 1D indices (GL-fallback classes, > 4 nodes): the shell rows
     int wide[2 * kMaxP];
+    const int64_t* shell;     // shell rows done in this launch (<= 8 nodes per direction), or null
+    int64_t nshell;
     double* Mv;
     double* Kv;
     int64_t ldM, ldK;
@@ -150,7 +152,7 @@ __device__ __forceinline__ void f2d_frame_item(const F2fArgs& a, int64_t it, con
     const int nA = a.jA1 >= a.jA0 ? a.jA1 - a.jA0 + 1 : 0;
     const int fullchunks = (int)((N + 2 * kF2iChunk - 1) / (2 * kF2iChunk));
     // A fragment of a weighted table, lane (g, t) = Aw^T[o = g][k = t] of 1D row r, kind
-    auto afrag = [&](int64_t r, int kind) { return g < S ? __ldg(a.AW + r * 64 + kind * 32 + t * 8 + g) : 0.0; };
+    auto afrag = [&](int64_t r, int kind) { return g < S ? __ldg(a.AW + r * 128 + kind * 64 + t * 8 + g) : 0.0; };
     int j, x0, npair;
     if (it < (int64_t)nA * 2) {
         j = a.jA0 + (int)(it >> 1);
@@ -272,6 +274,115 @@ __device__ __forceinline__ void f2d_frame_item(const F2fArgs& a, int64_t it, con
     }
 }
 
+// A shell row (a direction with a GL-fallback rule of 5..8 nodes, R1): its nodes are split into
+// two halves of 4 per direction (x: nodes 0-3 | 4-7, y likewise; a direction with <= 4 nodes
+// has an empty second half: zero weights), the four (x half, y half) combinations are the 2 x 2
+// rows of one step of the frame machinery, and the row is their sum: every sample of the
+// definition appears in exactly one combination (the mass nodes all lie in the first half).
+template <int KS>
+__device__ __forceinline__ void f2d_shell_item(const F2fArgs& a, int64_t row, const double* tbl, double* os, int lane,
+                                               uint64_t pol) {
+    constexpr int S = 7, P3 = 3;
+    const int g = lane >> 2, t = lane & 3;
+    const int copy = lane & 15;
+    const int64_t N = a.N;
+    const int cw = a.cw;
+    const int64_t nstride = (int64_t)kMaxNodes * cw;
+    const double ysg = (t & 1) ? -1.0 : 1.0;
+    const int i1 = (int)(row % N), i2 = (int)(row / N);
+    auto afrag = [&](int64_t r, int kind, int k0) {
+        return g < S ? __ldg(a.AW + r * 128 + kind * 64 + (k0 + t) * 8 + g) : 0.0;
+    };
+    // exponent B fragments: y-node (ky, type) of half L, mass y-nodes of both halves (tile B)
+    double Ya[KS], Yb[KS], Yab[KS];
+    {
+        const int ky = g >> 1, hi = g & 1;
+        const double* pa = a.ctab + ((int64_t)(2 + hi) * N + i2) * nstride + ky * cw + t;
+        const double* pb = pa + 4 * cw;                                          // nodes 4..7
+        const double* pab = a.ctab + ((int64_t)2 * N + i2) * nstride + (4 * hi + ky) * cw + t;
+#pragma unroll
+        for (int s = 0; s < KS; ++s) {
+            const bool in = 4 * s + t < cw;
+            Ya[s] = in ? ysg * __ldg(pa + 4 * s) : 0.0;
+            Yb[s] = in ? ysg * __ldg(pb + 4 * s) : 0.0;
+            Yab[s] = in ? ysg * __ldg(pab + 4 * s) : 0.0;
+        }
+    }
+    const double aMa = afrag(i2, 0, 0), aKa = afrag(i2, 1, 0), aMb = afrag(i2, 0, 4), aKb = afrag(i2, 1, 4);
+    // x-node g = (kx = g >> 1, half g & 1): node 4 (g & 1) + kx of row i1
+    double XM[KS], XK[KS];
+    {
+        const double* pm = a.ctab + (int64_t)i1 * nstride + (4 * (g & 1) + (g >> 1)) * cw + t;
+        const double* pk = pm + N * nstride;
+#pragma unroll
+        for (int s = 0; s < KS; ++s) {
+            const bool in = 4 * s + t < cw;
+            XM[s] = in ? __ldg(pm + 4 * s) : 0.0;
+            XK[s] = in ? __ldg(pk + 4 * s) : 0.0;
+        }
+    }
+    double ea0 = 0.0, ea1 = 0.0, eb0 = 0.0, eb1 = 0.0, ek0 = 0.0, ek1 = 0.0;
+#pragma unroll
+    for (int s = 0; s < KS; ++s) {
+        dmma(ea0, ea1, XM[s], Ya[s]);
+        dmma(eb0, eb1, XM[s], Yb[s]);
+        dmma(ek0, ek1, XK[s], Yab[s]);
+    }
+    const double wMa = exp_tab(ea0, tbl, copy), wKya = exp_tab(ea1, tbl, copy);
+    const double wMb = exp_tab(eb0, tbl, copy), wKyb = exp_tab(eb1, tbl, copy);
+    const double wKxa = exp_tab(ek0, tbl, copy), wKxb = exp_tab(ek1, tbl, copy);
+    double tM[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, tKx[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, tKy[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    dmma(tM[0][0], tM[0][1], aMa, wMa);
+    dmma(tKy[0][0], tKy[0][1], aKa, wKya);
+    dmma(tKx[0][0], tKx[0][1], aMa, wKxa);
+    dmma(tM[1][0], tM[1][1], aMb, wMb);
+    dmma(tKy[1][0], tKy[1][1], aKb, wKyb);
+    dmma(tKx[1][0], tKx[1][1], aMb, wKxb);
+    const double aMx[2] = {afrag(i1, 0, 0), afrag(i1, 0, 4)}, aKx[2] = {afrag(i1, 1, 0), afrag(i1, 1, 4)};
+#pragma unroll
+    for (int L = 0; L < 2; ++L)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            double m0 = 0.0, m1 = 0.0, k0 = 0.0, k1 = 0.0;
+            dmma(m0, m1, aMx[i], tM[L][i]);
+            dmma(k0, k1, aKx[i], tKx[L][i]);
+            dmma(k0, k1, aMx[i], tKy[L][i]);
+            double* b = os + L * 2 * kF2iRun + i * 49 + g + 14 * t;
+            if (g < S) {
+                b[0] = m0;
+                b[kF2iRun] = k0;
+                if (t < 3) {
+                    b[7] = m1;
+                    b[kF2iRun + 7] = k1;
+                }
+            }
+        }
+    __syncwarp();
+    if (row >= a.row_begin && row < a.row_end) {
+        const int64_t orow = row - a.row_begin;
+        const int lo1 = max(-P3, -i1), hi1 = min(P3, (int)N - 1 - i1);
+        const int lo2 = max(-P3, -i2), hi2 = min(P3, (int)N - 1 - i2);
+#pragma unroll
+        for (int mat = 0; mat < 2; ++mat) {
+            double* dst = mat ? a.Kv : a.Mv;
+            if (!dst) continue;
+            const double* src = os + mat * kF2iRun;
+            for (int slot = lane; slot < 49; slot += 32) {
+                const double v = src[slot] + src[49 + slot] + src[2 * kF2iRun + slot] + src[2 * kF2iRun + 49 + slot];
+                const int o1 = slot % 7 - P3, o2 = slot / 7 - P3;
+                if (a.csr) {
+                    if (o1 < lo1 || o1 > hi1 || o2 < lo2 || o2 > hi2) continue;
+                    st_out(dst + (mat ? a.rpK : a.rpM)[orow] + (o1 - lo1) + (int64_t)(o2 - lo2) * (hi1 - lo1 + 1), v,
+                           pol);
+                } else {
+                    st_out(dst + orow * (mat ? a.ldK : a.ldM) + slot, v + 0.0, pol);
+                }
+            }
+        }
+    }
+    __syncwarp();
+}
+
 // EXACT: cw == 4 KS (every k-step column is a table column, no predicated loads)
 template <int KS, bool EXACT>
 __global__ void __launch_bounds__(kF2iWarps * 32, kF2iMinBlocks) k_f2d_interior(const F2iArgs a, const F2fArgs fa) {
@@ -308,13 +419,17 @@ __global__ void __launch_bounds__(kF2iWarps * 32, kF2iMinBlocks) k_f2d_interior(
     const int chunks = (rpairs + kF2iChunk - 1) / kF2iChunk;
     const int64_t items = a.line1 >= a.line0 ? (int64_t)lpairs * chunks : 0;
     // the frame items first (their rows have per-row tables; a few per warp), then the interior
-    for (int64_t it0 = (int64_t)blockIdx.x * kF2iWarps + warp; it0 < fa.items + items;
+    for (int64_t it0 = (int64_t)blockIdx.x * kF2iWarps + warp; it0 < fa.items + fa.nshell + items;
          it0 += (int64_t)gridDim.x * kF2iWarps) {
         if (it0 < fa.items) {
             f2d_frame_item<KS>(fa, it0, tbl, os, lane, pol);
             continue;
         }
-        const int64_t it = it0 - fa.items;
+        if (it0 < fa.items + fa.nshell) {
+            f2d_shell_item<KS>(fa, fa.shell[it0 - fa.items], tbl, os, lane, pol);
+            continue;
+        }
+        const int64_t it = it0 - fa.items - fa.nshell;
         const int lp = (int)(it % lpairs), ch = (int)(it / lpairs);
         const int La = a.line0 + 2 * lp;
         const bool bval = La + 1 <= a.line1;
@@ -554,7 +669,7 @@ F2fArgs frame_args(const wgq_rules_s* R, const RowTables& T, const double* ctab,
 }  // namespace
 
 int launch_f2d_interior(const wgq_rules_s* R, const RowTables& T, const double* ctab, int cw, const wgq_out_t* M,
-                        const wgq_out_t* K, cudaStream_t st) {
+                        const wgq_out_t* K, const int64_t* shell, int64_t nshell, cudaStream_t st) {
     const wgq_out_t* any = M ? M : K;
     F2iArgs a{};
     a.ctab = ctab;
@@ -568,7 +683,9 @@ int launch_f2d_interior(const wgq_rules_s* R, const RowTables& T, const double* 
     a.line0 = (int)std::max<int64_t>(l0, a.lo);
     a.line1 = (int)std::min<int64_t>(l1, a.hi);
     if (a.row_end <= a.row_begin) return WGQ_OK;
-    const F2fArgs fa = frame_args(R, T, ctab, cw, M, K);      // the frame rows, in the same launch
+    F2fArgs fa = frame_args(R, T, ctab, cw, M, K);            // the frame rows, in the same launch
+    fa.shell = shell;                                         // and the shell rows (<= 8 nodes)
+    fa.nshell = shell ? nshell : 0;
     a.Mv = M ? M->values : nullptr;
     a.Kv = K ? K->values : nullptr;
     a.ldM = M ? M->ld : 0;
@@ -591,7 +708,7 @@ int launch_f2d_interior(const wgq_rules_s* R, const RowTables& T, const double* 
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t lpairs = (a.line1 - a.line0 + 2) / 2;
     const int64_t rpairs = (a.hi - a.lo + 2) / 2;
-    const int64_t items = (a.line1 >= a.line0 ? lpairs * ((rpairs + kF2iChunk - 1) / kF2iChunk) : 0) + fa.items;
+    const int64_t items = (a.line1 >= a.line0 ? lpairs * ((rpairs + kF2iChunk - 1) / kF2iChunk) : 0) + fa.items + fa.nshell;
     int64_t blocks = std::min<int64_t>((items + kF2iWarps - 1) / kF2iWarps, (int64_t)sms * kF2iMinBlocks);
     blocks = std::max<int64_t>(blocks, 1);
     const size_t smem = (size_t)kF2iWarps * kF2iWarpSmem * sizeof(double);

@@ -92,10 +92,10 @@ struct RowTables {
     // to c * B_{r+o} when c is the vertex field's linear interpolant (R6).
     double* PM = nullptr;      // [N][kMaxV][kMaxS]
     double* PK = nullptr;      // [N][kMaxV][kMaxS]
-    // Weighted 1D tables of the first 4 nodes, for the 2D FOURIER kernels (fourier2d.cu):
+    // Weighted 1D tables of the first 8 nodes, for the 2D FOURIER kernels (fourier2d.cu):
     // AW[r][kind][k][o] = w_k B_{r+o}(x_k) (kind 0, mass) / w_k B'_{r+o}(x_k) (kind 1), o < 7, zero
-    // for k >= m and o = 7 (rows with more than 4 nodes are not read through it)
-    double* AW = nullptr;      // [N][2][4][8]
+    // for k >= m and o = 7 (rows with more than 8 nodes are not read through it)
+    double* AW = nullptr;      // [N][2][8][8]
     void* base = nullptr;      // single allocation
     // Host copies of one class-I (interior, 2p <= r <= N-1-2p) row's weighted tables
     // iAwM[k][o] = wM[k] VM[k][o], iAwK[k][o] = wK[k] DK[k][o] (shift-invariant up to rounding:
@@ -184,7 +184,7 @@ int validate_coeff_range(const wgq_rules_s* R, const wgq_coeff_t* c, int64_t row
 bool f2d_interior_applies(const wgq_rules_s* R, const RowTables& T, const wgq_coeff_t* c);
 #ifdef __CUDACC__
 int launch_f2d_interior(const wgq_rules_s* R, const RowTables& T, const double* ctab, int cw, const wgq_out_t* M,
-                        const wgq_out_t* K, cudaStream_t st);
+                        const wgq_out_t* K, const int64_t* shell, int64_t nshell, cudaStream_t st);
 #endif
 int fetch_interior_tables(const wgq_rules_s* R, int64_t n, RowTables* T);
 

@@ -170,12 +170,12 @@ __global__ void k_vertex_tables(int p, int64_t n, RowTables T) {
     (kind == WGQ_MASS ? T.PM : T.PK)[(r * kMaxV + v) * kMaxS + o] = acc;
 }
 
-// AW[r][kind][k][o] = w_k A_k[o] for the first 4 nodes (fourier2d.cu): one thread per entry.
+// AW[r][kind][k][o] = w_k A_k[o] for the first 8 nodes (fourier2d.cu): one thread per entry.
 __global__ void k_weighted_tables(RowTables T) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= T.N * 64) return;
-    const int64_t r = e / 64;
-    const int kind = (int)(e / 32) % 2, k = (int)(e / 8) % 4, o = (int)(e % 8);
+    if (e >= T.N * 128) return;
+    const int64_t r = e / 128;
+    const int kind = (int)(e / 64) % 2, k = (int)(e / 8) % 8, o = (int)(e % 8);
     const int m = kind == WGQ_MASS ? T.mM[r] : T.mK[r];
     double v = 0.0;
     if (k < m && o < kMaxS)
@@ -190,7 +190,7 @@ int build_row_tables(const wgq_rules_s* R, int64_t n_dir, RowTables* T, void* st
     const int64_t N = n_dir + R->p;
     size_t bytes = 2 * N * sizeof(int) +
                    N * (kMaxMassNodes * (2 + kMaxS) + kMaxStiffNodes * (2 + kMaxS) + 2 * kMaxV * kMaxS) * sizeof(double);
-    bytes += N * 64 * sizeof(double);          // AW
+    bytes += N * 128 * sizeof(double);         // AW
     bytes += 256;
     void* base = nullptr;
     if (cudaMalloc(&base, bytes) != cudaSuccess) return WGQ_ECUDA;
@@ -205,7 +205,7 @@ int build_row_tables(const wgq_rules_s* R, int64_t n_dir, RowTables* T, void* st
     T->DK = d; d += N * kMaxStiffNodes * kMaxS;
     T->PM = d; d += N * kMaxV * kMaxS;
     T->PK = d; d += N * kMaxV * kMaxS;
-    T->AW = d; d += N * 64;
+    T->AW = d; d += N * 128;
     T->mM = (int*)d;
     T->mK = T->mM + N;
     T->maxM = T->maxK = 0;
@@ -229,7 +229,7 @@ int build_row_tables(const wgq_rules_s* R, int64_t n_dir, RowTables* T, void* st
     k_row_tables<<<(unsigned)((threads + 255) / 256), 256, 0, (cudaStream_t)stream>>>(A, *T);
     const int64_t vthreads = N * 2 * kMaxV * kMaxS;
     k_vertex_tables<<<(unsigned)((vthreads + 255) / 256), 256, 0, (cudaStream_t)stream>>>(R->p, n_dir, *T);
-    k_weighted_tables<<<(unsigned)((N * 64 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(*T);
+    k_weighted_tables<<<(unsigned)((N * 128 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(*T);
     if (cudaGetLastError() != cudaSuccess) return WGQ_ECUDA;
     return WGQ_OK;
 }
