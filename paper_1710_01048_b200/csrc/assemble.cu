@@ -774,20 +774,29 @@ __global__ void __launch_bounds__(256) k_load_grid_line(const GenericArgs a, con
 // z is finished: s = sum_vz PW_z q (z) per column, then sum_vx PW_x s over each row's window by
 // shuffles (x).  One block barrier per vertex plane; each vertex value is read from global
 // memory once per tile.
-constexpr int kLTW = 8;        // warps per block
+constexpr int kLTW = 4;        // warps per block
 constexpr int kLTLW = 2;       // lines per warp
 constexpr int kLTZ = 32;       // output planes per block
-constexpr int kLTA = 4;        // vertex planes in flight ahead
-constexpr int kLTR = 8;        // ring depth, a power of two >= p + 2 + kLTA - 1 (a plane's q stays while its window is open)
-static_assert(kLTR >= kMaxP + 2 + kLTA - 1 && (kLTR & (kLTR - 1)) == 0, "load ring depth");
+constexpr int kLTA = 2;        // vertex planes in flight ahead
+constexpr int kLTR = 8;        // q ring depth, a power of two >= p + 2 (a plane's q stays while its window is open)
+constexpr int kLTRR = 4;       // raw ring depth (vertex planes), a power of two >= kLTA + 1
+static_assert(kLTR >= kMaxP + 2 && (kLTR & (kLTR - 1)) == 0, "load q ring depth");
+static_assert(kLTRR >= kLTA + 1 && (kLTRR & (kLTRR - 1)) == 0, "load raw ring depth");
+
+template <int P>
+constexpr size_t load_tile_smem() {
+    constexpr int V = P + 2, LT = kLTW * kLTLW, TILE = (LT + V - 1) * 32;
+    return (size_t)(kLTRR * TILE + LT * kLTR * 32 + kLTZ * V) * sizeof(double);
+}
 
 template <int P>
 __global__ void __launch_bounds__(kLTW * 32) k_load_grid_tile(const GenericArgs a, const double* PW, double* b) {
     constexpr int V = P + 2, W = 32 - V + 1, LT = kLTW * kLTLW, EY = LT + V - 1, TILE = EY * 32;
     constexpr int NT = kLTW * 32, LPT = (TILE + NT - 1) / NT;
     extern __shared__ __align__(16) double lt_smem[];
-    double* raw = lt_smem;                                      // [kLTR][EY][32] vertex planes
-    double* qr = raw + kLTR * TILE;                             // [LT][kLTR][32] y-contracted planes per line
+    double* raw = lt_smem;                                      // [kLTRR][EY][32] vertex planes
+    double* qr = raw + kLTRR * TILE;                            // [LT][kLTR][32] y-contracted planes per line
+    double* swz = qr + LT * kLTR * 32;                          // [kLTZ][V] z weights of the block's outputs
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     // 32-bit indices: the launcher requires N^3 < 2^31 (so (n + 1)^3 too)
     const int N = (int)a.N, n = (int)a.n, nv = n + 1;
@@ -802,29 +811,40 @@ __global__ void __launch_bounds__(kLTW * 32) k_load_grid_tile(const GenericArgs 
     const int zs = max(0, z_lo - P);
     const int ze = min(n, max(V - 1, z_hi));                     // last output z_hi - 1 needs z_hi
     const int zg0 = (int)a.coef.plane0, zg1 = (int)(a.coef.plane0 + a.coef.planes);
-    // load roles: tile element e = tid + NT m -> (row by0 + e / 32, column c0 + e % 32)
-    int goff[LPT];
+    for (int t = tid; t < (z_hi - z_lo) * V; t += NT) swz[t] = __ldg(PW + (z_lo + t / V) * kMaxV + t % V);
+    // load roles: tile element e = tid + NT m -> (row by0 + e / 32, column c0 + e % 32);
+    // out-of-mesh elements are zero-filled (source size 0)
+    int goff[LPT], gsz[LPT];
     uint32_t sdst[LPT];
 #pragma unroll
     for (int m = 0; m < LPT; ++m) {
         const int e = tid + NT * m;
         const int y = by0 + e / 32, x = c0 + e % 32;
-        goff[m] = (e < TILE && y <= n && x >= 0 && x <= n) ? y * nv + x : -1;
+        const bool ok = e < TILE && y <= n && x >= 0 && x <= n;
+        goff[m] = ok ? y * nv + x : 0;
+        gsz[m] = ok ? 8 : 0;
         sdst[m] = (uint32_t)__cvta_generic_to_shared(raw + (e < TILE ? e : 0));
     }
     const int plane_el = nv * nv;
     auto issue = [&](int z) {                                    // one commit group per plane
         if (z <= ze) {
-            const uint32_t so = (uint32_t)((z & (kLTR - 1)) * TILE * sizeof(double));
-            const bool zok = z >= zg0 && z < zg1;
-            const double* gz = a.coef.grid + (int64_t)(z - zg0) * plane_el;
+            const uint32_t so = (uint32_t)((z & (kLTRR - 1)) * TILE * sizeof(double));
+            if (z >= zg0 && z < zg1) {
+                const double* gz = a.coef.grid + (int64_t)(z - zg0) * plane_el;
 #pragma unroll
-            for (int m = 0; m < LPT; ++m) {
-                if (tid + NT * m >= TILE) break;
-                const bool ok = zok && goff[m] >= 0;
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sdst[m] + so),
-                             "l"(ok ? gz + goff[m] : a.coef.grid), "r"(ok ? 8 : 0)
-                             : "memory");
+                for (int m = 0; m < LPT; ++m) {
+                    if (TILE % NT != 0 && tid + NT * m >= TILE) break;
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sdst[m] + so), "l"(gz + goff[m]),
+                                 "r"(gsz[m])
+                                 : "memory");
+                }
+            } else {                                             // plane outside the supplied slab: zeros
+#pragma unroll
+                for (int m = 0; m < LPT; ++m) {
+                    if (TILE % NT != 0 && tid + NT * m >= TILE) break;
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, 0;" ::"r"(sdst[m] + so), "l"(a.coef.grid)
+                                 : "memory");
+                }
             }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
@@ -835,6 +855,7 @@ __global__ void __launch_bounds__(kLTW * 32) k_load_grid_tile(const GenericArgs 
     constexpr int YW = V + kLTLW - 1;                             // rows of the warp's window
     const int i2w = y0 + kLTLW * warp;
     const int byw = max(0, i2w - P);
+    const bool yfast = i2w >= P;                                 // by_l = by_0 + l for every line
     double wy[kLTLW][YW];
     bool lok[kLTLW];
 #pragma unroll
@@ -858,30 +879,37 @@ __global__ void __launch_bounds__(kLTW * 32) k_load_grid_tile(const GenericArgs 
     double* q = qr + (kLTLW * warp) * kLTR * 32 + lane;          // q[l][slot] at q[(l kLTR + slot) 32]
     const double* rl = raw + (byw - by0) * 32 + lane;
     double* bl = b + ((int64_t)i2w * N + i1 - a.row_begin);      // row (i3 = 0, line i2w) of this lane
-    // weights of a class-I plane (any i3 in [2p, N-1-2p]; all such rows share them) and whether
-    // every row of the block lies in the slab
-    double wzi[V];
-    const int i3i = min(2 * P, N - 1);
+    bool sok[kLTLW];
 #pragma unroll
-    for (int v = 0; v < V; ++v) wzi[v] = __ldg(PW + i3i * kMaxV + v);
+    for (int l = 0; l < kLTLW; ++l) sok[l] = xok && lok[l];
     const bool all_in = (int64_t)z_lo * pr >= a.row_begin && (int64_t)z_hi * pr <= a.row_end;
     for (int k = 0; k < kLTA; ++k) issue(zs + k);
     for (int z = zs; z <= ze; ++z) {
         asm volatile("cp.async.wait_group %0;" ::"n"(kLTA - 1) : "memory");
-        __syncthreads();                                         // plane z landed; slot of z - kLTR + kLTA free
+        __syncthreads();                                         // plane z landed; raw slot of z - kLTRR + kLTA free
         issue(z + kLTA);
         // y stage of plane z at this lane's column, for each line of the warp
         const int sl = z & (kLTR - 1);
-        const double* rz = rl + sl * TILE;
+        const double* rz = rl + (z & (kLTRR - 1)) * TILE;
         double g[YW];
 #pragma unroll
         for (int v = 0; v < YW; ++v) g[v] = rz[v * 32];
+        if (yfast) {                                             // line l's window: rows l .. l + V - 1
 #pragma unroll
-        for (int l = 0; l < kLTLW; ++l) {
-            double qz = 0.0;
+            for (int l = 0; l < kLTLW; ++l) {
+                double qz = wy[l][l] * g[l];
 #pragma unroll
-            for (int v = 0; v < YW; ++v) qz = fma(wy[l][v], g[v], qz);
-            q[(l * kLTR + sl) * 32] = qz;
+                for (int v = 1; v < V; ++v) qz = fma(wy[l][l + v], g[l + v], qz);
+                q[(l * kLTR + sl) * 32] = qz;
+            }
+        } else {
+#pragma unroll
+            for (int l = 0; l < kLTLW; ++l) {
+                double qz = 0.0;
+#pragma unroll
+                for (int v = 0; v < YW; ++v) qz = fma(wy[l][v], g[v], qz);
+                q[(l * kLTR + sl) * 32] = qz;
+            }
         }
         // the outputs whose window [bz, bz + V - 1] (clipped to the mesh) ends at plane z,
         // last(i3) = min(n, max(V - 1, i3 + 1)): i3 = z - 1 in the steady state, [0, P] at
@@ -894,24 +922,33 @@ __global__ void __launch_bounds__(kLTW * 32) k_load_grid_tile(const GenericArgs 
         o1 = min(o1, z_hi - 1);
         for (int i3 = o0; i3 <= o1; ++i3) {
             const int bz = max(0, i3 - P);
-            double wz[V];
-            const bool interior = i3 >= 2 * P && i3 <= N - 1 - 2 * P;   // class-I plane: the shared weights
-#pragma unroll
-            for (int v = 0; v < V; ++v) wz[v] = interior ? wzi[v] : __ldg(PW + i3 * kMaxV + v);
-            const int64_t rowz = i3 * pr;
-            const bool rin = all_in || (rowz + (int64_t)i2w * N + x0 >= a.row_begin &&
-                                        rowz + (int64_t)(i2w + kLTLW - 1) * N + x0 + W <= a.row_end);
+            const double* wz = swz + (i3 - z_lo) * V;
+            double* bo = bl + (int64_t)i3 * pr;
+            const bool rin = all_in || ((int64_t)i3 * pr + (int64_t)i2w * N + x0 >= a.row_begin &&
+                                        (int64_t)i3 * pr + (int64_t)(i2w + kLTLW - 1) * N + x0 + W <= a.row_end);
+            double s[kLTLW];
 #pragma unroll
             for (int l = 0; l < kLTLW; ++l) {
-                double s = 0.0;
+                s[l] = 0.0;
 #pragma unroll
-                for (int v = 0; v < V; ++v) s = fma(wz[v], q[(l * kLTR + ((bz + v) & (kLTR - 1))) * 32], s);
-                double acc = 0.0;
+                for (int v = 0; v < V; ++v) s[l] = fma(wz[v], q[(l * kLTR + ((bz + v) & (kLTR - 1))) * 32], s[l]);
+            }
+            double acc[kLTLW];
 #pragma unroll
-                for (int v = 0; v < V; ++v) acc = fma(wx[v], __shfl_sync(0xffffffffu, s, (off + v) & 31), acc);
-                if (xok && lok[l]) {
-                    const int64_t row = rowz + (int64_t)(i2w + l) * N + i1;
-                    if (rin || (row >= a.row_begin && row < a.row_end)) bl[rowz + (int64_t)l * N] = acc;
+            for (int l = 0; l < kLTLW; ++l) {
+                acc[l] = 0.0;
+#pragma unroll
+                for (int v = 0; v < V; ++v) acc[l] = fma(wx[v], __shfl_sync(0xffffffffu, s[l], (off + v) & 31), acc[l]);
+            }
+            if (rin) {
+#pragma unroll
+                for (int l = 0; l < kLTLW; ++l)
+                    if (sok[l]) bo[(int64_t)l * N] = acc[l];
+            } else {
+#pragma unroll
+                for (int l = 0; l < kLTLW; ++l) {
+                    const int64_t row = (int64_t)i3 * pr + (int64_t)(i2w + l) * N + i1;
+                    if (sok[l] && row >= a.row_begin && row < a.row_end) bo[(int64_t)l * N] = acc[l];
                 }
             }
         }
@@ -929,8 +966,8 @@ int launch_load_pd(const GenericArgs& a, const double* PW, double* b, bool speci
         const int64_t pr = a.N * a.N;
         const int64_t planes = (a.row_end - 1) / pr - a.row_begin / pr + 1;
         constexpr int W = 32 - (P + 2) + 1;
-        constexpr int LT = kLTW * kLTLW, TILE = (LT + P + 1) * 32;
-        const size_t smem = (size_t)(kLTR * TILE + LT * kLTR * 32) * sizeof(double);
+        constexpr int LT = kLTW * kLTLW;
+        constexpr size_t smem = load_tile_smem<P>();
         if (cudaFuncSetAttribute(k_load_grid_tile<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
             cudaSuccess)
             return WGQ_ECUDA;
