@@ -287,11 +287,11 @@ def arm_config(cfg, world, ld=None):
 
 
 def gpu_launches_per_step(cfg):
-    """Kernels of one assembly call: one, except the 2D FOURIER path (factor tables, then for
-    p = 3 the class-I interior kernel, the frame kernel and the GL-shell pass; for p = 2 the
-    per-row kernel and the shell pass)."""
+    """Kernels of one assembly call: one, except the 2D FOURIER path: factor tables, the
+    device-generated GL-shell row list, then for p = 3 one fused launch (class-I interior, frame
+    and shell items) and for p = 2 the per-row kernel plus the generic shell pass."""
     if cfg["dim"] == 2 and cfg["coeff"]["kind"] == "fourier_logn":
-        return 4 if cfg["p"] == 3 else 3
+        return 3 if cfg["p"] == 3 else 4
     return 1
 
 
