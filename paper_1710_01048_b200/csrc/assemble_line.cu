@@ -721,6 +721,57 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 2) k_line_grid3(const __grid_const
 // cores (the 10 of 16 8x8 blocks with |X - c| <= 1 block, DMMA m8n8k4 items of 13 k-steps);
 // the H planes come from the assembly's phase A, the u columns X (49 values each) are
 // prefetched with the vertex patches into a ring.  Nothing is stored but y.
+// Band of the apply's D product on DFMA: D_X(c, X) = sum_k H_X[c][k] U[X][k] for the tile
+// planes c = b0 + i (i = 8 pb + g) and the diagonals X - c = D0 .. D0 + ND - 1 (the structural
+// band of the x-direction tables is X - c in [-1, p]: a node of element e touches vertex planes
+// e, e+1 and columns e .. e+p).  Lane (g, t4) accumulates k = t4 (mod 4) — the operand rows are
+// read in the DMMA fragment pattern, conflict-free — and the four partial sums are combined by
+// shuffles.  Both matrices share the U operands.
+template <int P, int D0, int ND, int HS, int RING, int URING>
+__device__ __forceinline__ void d_band(const double* Hm, const double* Hk, const double* U, const double* zrow,
+                                       double* Dm, double* Dk, int DC, int DR, int b0, int hi_plane, int Xhi,
+                                       int upos0, int pb, int g, int t4) {
+    constexpr int S2 = (2 * P + 1) * (2 * P + 1), KSD = (S2 + 3) / 4;
+    const int i = 8 * pb + g, c = b0 + i;
+    const bool cv = c <= hi_plane;
+    const double* hm = (cv ? Hm + ring_slot<RING>(c) * HS : zrow) + t4;
+    const double* hk = (cv ? Hk + ring_slot<RING>(c) * HS : zrow) + t4;
+    const double* ur[ND];
+#pragma unroll
+    for (int q = 0; q < ND; ++q) {
+        const int j = i + D0 + q;                          // X - Xlo (Xlo = b0)
+        const bool xv = j >= 0 && b0 + j <= Xhi;
+        int up = upos0 + j;
+        up = up >= URING ? up - URING : up;
+        ur[q] = (xv ? U + up * HS : zrow) + t4;
+    }
+    double am[ND], ak[ND];
+#pragma unroll
+    for (int q = 0; q < ND; ++q) am[q] = ak[q] = 0.0;
+#pragma unroll
+    for (int s = 0; s < KSD; ++s) {
+        const double hmv = hm[4 * s], hkv = hk[4 * s];
+#pragma unroll
+        for (int q = 0; q < ND; ++q) {
+            const double uv = ur[q][4 * s];
+            am[q] = fma(hmv, uv, am[q]);
+            ak[q] = fma(hkv, uv, ak[q]);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < ND; ++q) {
+        am[q] += __shfl_xor_sync(0xffffffffu, am[q], 1);
+        ak[q] += __shfl_xor_sync(0xffffffffu, ak[q], 1);
+        am[q] += __shfl_xor_sync(0xffffffffu, am[q], 2);
+        ak[q] += __shfl_xor_sync(0xffffffffu, ak[q], 2);
+        const int j = i + D0 + q;
+        if (t4 == (q & 3) && i < DR && j >= 0 && j < DC) {
+            Dm[i * DC + j] = am[q];
+            Dk[i * DC + j] = ak[q];
+        }
+    }
+}
+
 // Tile geometry of the apply for TRA rows per tile: the vertex-plane window (TRA + p + 1 planes,
 // H ring RING_A >= that), the D product's plane x column blocks of 8 (only blocks within the band
 // |column - plane| <= 1 block carry nonzero P^ weights), the u ring (the next tile's window of
@@ -750,7 +801,7 @@ struct ApplyGeom {
 };
 
 #ifndef WGQ_APPLY_THREADS
-#define WGQ_APPLY_THREADS 320
+#define WGQ_APPLY_THREADS 256
 #endif
 constexpr int kApplyThreads = WGQ_APPLY_THREADS;
 
@@ -784,6 +835,8 @@ __global__ void __launch_bounds__(kApplyThreads, TRA == 8 ? 3 : 2) k_line_apply(
     for (int e = tid; e < 2 * V * S; e += NT) pint[e] = e < V * S ? a.PMh[e / S][e % S] : a.PKi[(e - V * S) / S][e % S];
     // zero rows and the padding columns [S2, HS) of the H and U rows: the D fragments then need no masks
     for (int e = tid; e < HS; e += NT) zrow[e] = 0.0;
+    // D entries off the band are never written and stay zero (their x tables are structural zeros)
+    for (int e = tid; e < 2 * G::DR * DC; e += NT) Dm[e] = 0.0;
     for (int e = tid; e < (2 * RING + URING) * (HS - S2); e += NT) {
         const int row = e / (HS - S2), col = S2 + e % (HS - S2);
         (row < 2 * RING ? Hm + row * HS : U + (row - 2 * RING) * HS)[col] = 0.0;
@@ -851,37 +904,19 @@ __global__ void __launch_bounds__(kApplyThreads, TRA == 8 ? 3 : 2) k_line_apply(
         const TileDesc dA = desc[(k + 1) & 7];
         const int b0 = max(0, d.t0 - P);
         const int hi_plane = max(0, d.t0 + d.tr - 1 - P) + V - 1;
-        // ---- S1a: D_X = H_X (planes b0..) x U (columns Xlo..) on the tensor cores ----------
-        // items: (matrix, band block); block b enumerates (mt, nt) with |nt - mt| <= 1
-#pragma unroll
-        for (int it = warp; it < 2 * G::NB; it += NW) {
-            const int kind = it / G::NB;
-            int b = it % G::NB, mt = 0, nt = 0;
-            for (int q = 0, cnt = 0; q < G::DB * G::XBK; ++q) {
-                const int qm = q / G::XBK, qn = q % G::XBK;
-                if (qn - qm > 1 || qm - qn > 1) continue;
-                if (cnt++ == b) {
-                    mt = qm;
-                    nt = qn;
-                    break;
-                }
+        // ---- S1a: D_X = H_X (planes b0..) x U (columns Xlo..) on the band X - c in [-1, p] --
+        // items (plane block of 8, diagonal half): diagonals -1 .. NDA - 2 and NDA - 1 .. p
+        {
+            constexpr int ND = P + 2, NDA = (ND + 1) / 2;
+            for (int it = warp; it < 2 * G::DB; it += NW) {
+                if (a.dbg & 8) break;
+                if (it & 1)
+                    d_band<P, NDA - 1, ND - NDA, HS, RING, URING>(Hm, Hk, U, zrow, Dm, Dk, DC, G::DR, b0, hi_plane,
+                                                                   d.Xhi, d.upos, it >> 1, g, t4);
+                else
+                    d_band<P, -1, NDA, HS, RING, URING>(Hm, Hk, U, zrow, Dm, Dk, DC, G::DR, b0, hi_plane, d.Xhi,
+                                                         d.upos, it >> 1, g, t4);
             }
-            const double* H = kind ? Hk : Hm;
-            const int c = b0 + 8 * mt + g, X = d.Xlo + 8 * nt + g;
-            const bool cv = c <= hi_plane, xv = X <= d.Xhi;
-            const double* hrow = (cv ? H + ring_slot<RING>(c) * HS : zrow) + t4;
-            int upos = d.upos + 8 * nt + g;
-            upos = upos >= URING ? upos - URING : upos;
-            const double* urow = (xv ? U + upos * HS : zrow) + t4;
-            constexpr int KSD = (S2 + 3) / 4;                  // k-steps; padding columns are zero: no masks
-            double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};   // four independent chains
-            if (!(a.dbg & 8)) {
-#pragma unroll
-                for (int s = 0; s < KSD; ++s) dmma(acc[s & 3][0], acc[s & 3][1], hrow[4 * s], urow[4 * s]);
-            }
-            double* D = kind ? Dk : Dm;
-            D[(8 * mt + g) * DC + 8 * nt + 2 * t4] = (acc[0][0] + acc[1][0]) + (acc[2][0] + acc[3][0]);
-            D[(8 * mt + g) * DC + 8 * nt + 2 * t4 + 1] = (acc[0][1] + acc[1][1]) + (acc[2][1] + acc[3][1]);
         }
         __syncthreads();
         // ---- S1b: rows of tile k, phase A of tile k+1, prefetch tile k+PFD ------------------
