@@ -792,8 +792,6 @@ struct ApplyGeom {
     // (at most TRA + 2p each: a tile that starts a slab inside a line)
     static constexpr int URING = TRA == 8 ? ApplyCfg::URING : PFD * (TRA + 2 * P) + 1;
     static constexpr int HS = (S2 + 3) / 4 * 4 + ((S2 + 3) / 4 % 2 == 0 ? 4 : 0);   // row stride = 4 (mod 8)
-    // band blocks (mt, nt) with |nt - mt| <= 1, in order
-    static constexpr int NB = DB * XBK - ((DB > 2 ? (DB - 2) * (DB - 1) / 2 : 0) + (XBK > 2 ? (XBK - 2) * (XBK - 1) / 2 : 0));
     static constexpr size_t smem_doubles() {
         return (size_t)2 * RING * HS + PFD * 4 * V * S + PFD * PATCH + 4 * P * 2 * V * S + (size_t)URING * HS +
                2 * DR * DC + 2 * V * S + HS;
