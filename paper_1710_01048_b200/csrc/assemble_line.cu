@@ -785,7 +785,9 @@ struct ApplyGeom {
     static constexpr int PFD = ApplyCfg::PFD;
     static constexpr int DB = (W + 7) / 8;                             // plane blocks of D
     static constexpr int XBK = (TRA + 2 * P + 7) / 8;                  // column blocks of D
-    static constexpr int DR = DB * 8, DC = XBK * 8;                    // D extents
+    // D extents; the row stride DC = 4 (mod 8) doubles keeps the finishing stage's reads (lanes
+    // (row, vertex plane): consecutive rows step one column and one D row) conflict-free
+    static constexpr int DR = DB * 8, DC = XBK * 8 + 4;
     static constexpr int UXMAX = (TRA + 2 * P + 7) / 8 * 8;            // new columns per tile (a slab's first
                                                                        // tile may start mid-line: TRA + 2p)
     // live columns when tile k+PFD is issued: tile k+1's window and the new columns of k+2..k+PFD
