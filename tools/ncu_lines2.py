@@ -33,7 +33,7 @@ for r in rows:
             return float(r[hdr.index(k)].replace(",", "") or 0)
         except (ValueError, IndexError):
             return 0.0
-    conf = [h for h in hdr if "Conflicts Shared" in h]
+    conf = [h for h in hdr if "Wavefronts Shared Excessive" in h]
     res.append((ln, f("Instructions Executed"), f("Warp Stall Sampling (All Samples)"),
                 f(conf[0]) if conf else 0.0, r[1][:80]))
 ti = sum(x[1] for x in res) or 1

@@ -46,4 +46,14 @@ for p in (2, 3):
     run(p, 8, 2, trig(2))                                # separable 2D
     run(p, 5, 3, four(3))                                # generic
     run(p, 11, 1, {"kind": "const", "c0": 1.0})
+run(3, 21, 2, four(2))                                   # fused 2D FOURIER launch: interior, frame, shell items
+run(3, 40, 3, {"kind": "grid"})                          # several load-tile blocks in x, y and z
+for p in (2, 3):                                         # per-direction element counts
+    r = wgq.Rules(p, (7, 9, 11), 3)
+    gt = api.make_grid(r, 5, 0.5, 0, r.n_rows)[0]
+    c = api.coefficient({"kind": "grid"}, gt, 0)
+    api.assemble(r, c, ("mass", "stiffness"))
+    api.assemble_load(r, c)
+    api.apply(r, c, torch.randn(r.n_rows, dtype=torch.float64, device="cuda"), ("mass", "stiffness"))
+    torch.cuda.synchronize()
 print("sanitize case done")
