@@ -87,6 +87,9 @@ struct LineArgs {
     long long u_row0;
     double* yM;
     double* yK;
+    // assembly: line tickets (stream-ordered scratch, zeroed per launch) or null for the static
+    // round-robin line order
+    unsigned long long* ticket;
 };
 
 // L2 policies: the assembled matrices stream through L2 once (evict_first), the vertex grid
@@ -263,6 +266,8 @@ struct ApplyCfg {
 // (paid by every thread of the CTA) is a few adds and compares.
 struct TileIt {
     int line, i2, i3, x0, x1, t0;
+    int nchg;    // line changes so far (ticketed order: which s_line slot the next line is in)
+    bool pending;   // ticketed order: the next line is being fetched (resolved after a barrier)
     int qs;      // Q buffer of the line: line ordinal % PFD
     int ps;      // patch buffer of the tile: tile ordinal % PFD
     int lo, hi;  // vertex planes the tile adds to the line's H ring
@@ -293,6 +298,8 @@ __device__ __forceinline__ void it_line(const LineArgs& a, TileIt& t) {
 template <int P, int TR_ = Cfg<P>::TR>
 __device__ __forceinline__ void it_init(const LineArgs& a, TileIt& t) {
     t.line = a.row_begin / a.N + blockIdx.x;
+    t.nchg = 0;
+    t.pending = false;
     t.qs = 0;
     t.ps = 0;
     t.lpos = 0;
@@ -310,6 +317,37 @@ __device__ __forceinline__ void it_next(const LineArgs& a, TileIt& t) {
         t.qs = t.qs == PFD_ - 1 ? 0 : t.qs + 1;
         it_line<P>(a, t);
     }
+    it_planes<P, TR_>(t, a.N);
+}
+
+// Ticketed line order (assembly): the first line of CTA b is line b of the range, each further
+// line is the next unclaimed one (a global atomic counter), so the lines in flight stay the
+// ~gridDim most recent ones and the write stream advances through memory as one front (a static
+// round-robin order lets the CTAs drift apart: 6.4 vs 7.3 TB/s for the same bulk stores,
+// tools/write_probe3.cu).  Thread 0 claims the next line when the iterator leaves a line and
+// publishes it in s_line[nchg & 1]; every thread picks it up after the next block barrier
+// (it_resolve).  Two slots: a slot is rewritten two line changes later, after a barrier that
+// every reader of its previous value has passed.
+template <int P, int PFD_ = Cfg<P>::PFD, int TR_ = Cfg<P>::TR>
+__device__ __forceinline__ void it_next_ticket(const LineArgs& a, TileIt& t, int* s_line, int tid) {
+    t.t0 += TR_;
+    t.ps = t.ps == PFD_ - 1 ? 0 : t.ps + 1;
+    if (t.t0 >= t.x1) {
+        if (tid == 0)
+            s_line[t.nchg & 1] = a.row_begin / a.N + (int)gridDim.x + (int)atomicAdd(a.ticket, 1ull);
+        t.pending = true;
+        t.qs = t.qs == PFD_ - 1 ? 0 : t.qs + 1;
+    } else {
+        it_planes<P, TR_>(t, a.N);
+    }
+}
+template <int P, int TR_ = Cfg<P>::TR>
+__device__ __forceinline__ void it_resolve(const LineArgs& a, TileIt& t, const int* s_line) {
+    if (!t.pending) return;
+    t.line = s_line[t.nchg & 1];
+    ++t.nchg;
+    t.pending = false;
+    it_line<P>(a, t);
     it_planes<P, TR_>(t, a.N);
 }
 
@@ -543,6 +581,7 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 2) k_line_grid3(const __grid_const
 
     __shared__ TileDesc desc[8];                          // tiles k .. k+PFD (ring)
     __shared__ TileCsr cdesc[CSR ? 8 : 1];
+    __shared__ int s_line[2];                             // ticketed line order (it_next_ticket)
     constexpr int PFD = C::PFD;
     const int tid = threadIdx.x;
     const int n = a.n;
@@ -581,11 +620,21 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 2) k_line_grid3(const __grid_const
     PatchRow prow;
     prow.base = nullptr;
     it_init<P>(a, itP);
+    const bool ticketed = a.ticket != nullptr;
+    auto advance = [&]() {
+        if (itP.line > last_line) return;
+        if (ticketed) it_next_ticket<P>(a, itP, s_line, tid);
+        else it_next<P>(a, itP);
+    };
     for (int k = 0; k < PFD; ++k) {
         tile_issue<P>(a, patches, qbufs, itP, prow, last_line, tid);
         if (tid == 0) desc[k] = make_desc<P>(a, itP, last_line, padded);
         if (CSR && tid == 0) cdesc[k & (CSR ? 7 : 0)] = make_csr<P>(a, itP, last_line);
-        if (itP.line <= last_line) it_next<P>(a, itP);
+        advance();
+        if (ticketed) {
+            __syncthreads();
+            it_resolve<P>(a, itP, s_line);
+        }
     }
     cp_async_wait<PFD - 1>();                             // tile 0 landed
     __syncthreads();
@@ -597,6 +646,7 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 2) k_line_grid3(const __grid_const
     __syncthreads();
 
     for (int k = 0;; ++k) {
+        it_resolve<P>(a, itP, s_line);                    // the line claimed last iteration (ticketed)
         const TileDesc d = desc[k & 7];
         if (d.line < 0) break;
         const TileDesc dA = desc[(k + 1) & 7];
@@ -699,7 +749,7 @@ __global__ void __launch_bounds__(Cfg<P>::NT, 2) k_line_grid3(const __grid_const
         else tile_issue<P>(a, patches, qbufs, itP, prow, last_line, tid);    // tile k+PFD
         if (tid == 0) desc[(k + PFD) & 7] = make_desc<P>(a, itP, last_line, padded);
         if (CSR && tid == 0) cdesc[(k + PFD) & (CSR ? 7 : 0)] = make_csr<P>(a, itP, last_line);
-        if (itP.line <= last_line) it_next<P>(a, itP);
+        advance();
         cp_async_wait<PFD - 2>();                                  // tile k+2 landed
         if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // staging free
         __syncthreads();
@@ -1078,7 +1128,17 @@ int launch_line(const wgq_rules_s* R, const Tables3& TT, const wgq_coeff_t* c, c
     if (const char* e = getenv("WGQ_LINE_DBG")) a.dbg = atoi(e);
     if (a.row_end <= a.row_begin) return WGQ_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    return R->p == 3 ? launch_line_mode<3>(a, mode, st) : launch_line_mode<2>(a, mode, st);
+    static const bool static_order = [] {
+        const char* e = getenv("WGQ_LINE_STATIC");
+        return e && e[0] == '1';
+    }();
+    if (!static_order) {
+        if (cudaMallocAsync((void**)&a.ticket, sizeof(unsigned long long), st) != cudaSuccess) return WGQ_ENOMEM;
+        cudaMemsetAsync(a.ticket, 0, sizeof(unsigned long long), st);
+    }
+    const int rc = R->p == 3 ? launch_line_mode<3>(a, mode, st) : launch_line_mode<2>(a, mode, st);
+    if (a.ticket) cudaFreeAsync(a.ticket, st);
+    return rc;
 }
 
 bool line_apply_applies(const wgq_rules_s* R, const wgq_coeff_t* c) {
