@@ -617,18 +617,14 @@ CoefDev make_coef(const wgq_coeff_t* c) {
 //    (partition of unity), b_i = sum_v g[bz+vz][by+vy][bx+vx] prod_a PW_a[v_a] — the same sum
 //    reordered (vertex projection, as in the line kernel).
 //  * analytic f: the node-tensor sum with the coefficient factor tables (or c0).
-__global__ void k_vertex_weights(RowTables T, int p, double* PW) {
-    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= T.N * kMaxV) return;
-    const int64_t r = e / kMaxV;
-    const int v = (int)(e % kMaxV);
-    double s = 0.0;
-    for (int o = 0; o < 2 * p + 1; ++o) s += T.PM[(r * kMaxV + v) * kMaxS + o];   // the row's 2p+1 neighbours
-    PW[e] = s;
-}
+// per-direction vertex weights PW (RowTables::PW, built with the row tables), passed as one
+// pointer per direction
+struct PW3 {
+    const double* d[3];
+};
 
 template <int P, int D>
-__global__ void __launch_bounds__(256) k_load(const GenericArgs a, const double* PW, double* b) {
+__global__ void __launch_bounds__(256) k_load(const GenericArgs a, const PW3 PW, double* b) {
     constexpr int V = P + 2;
     const int64_t rows = a.rows_list ? a.nlist : a.row_end - a.row_begin;   // rows_list: a shell pass
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < rows; t += (int64_t)gridDim.x * blockDim.x) {
@@ -637,9 +633,9 @@ __global__ void __launch_bounds__(256) k_load(const GenericArgs a, const double*
         a.dims.decode(row, idx);
         double acc = 0.0;
         if (a.coef.kind == WGQ_COEF_GRID) {
-            // PW of direction q at PW + q ctabN kMaxV; vertex planes of (n_y+1) x (n_x+1)
+            // vertex planes of (n_y+1) x (n_x+1)
             const int64_t nvx = a.dims.n[0] + 1, nvy = D >= 2 ? a.dims.n[1] + 1 : 1;
-            const double* PWq[3] = {PW, PW + a.ctabN * kMaxV, PW + 2 * a.ctabN * kMaxV};
+            const double* const* PWq = PW.d;
             int64_t base[3];
 #pragma unroll
             for (int q = 0; q < D; ++q) base[q] = idx[q] - P > 0 ? idx[q] - P : 0;
@@ -702,7 +698,8 @@ __global__ void __launch_bounds__(256) k_load(const GenericArgs a, const double*
 // vertex planes c = c0 + l (+32) of the segment (coalesced loads along x), then row i1 = x0 + l
 // gathers b = sum_vx PWx[i1][vx] G[bx+vx] from its neighbours' registers (warp shuffles).
 template <int P, int D>
-__global__ void __launch_bounds__(256) k_load_grid_line(const GenericArgs a, const double* PW, double* b) {
+__global__ void __launch_bounds__(256) k_load_grid_line(const GenericArgs a, const PW3 PW3d, double* b) {
+    const double* PW = PW3d.d[0];   // isotropic mesh (the launcher)
     constexpr int V = P + 2;
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -764,200 +761,211 @@ __global__ void __launch_bounds__(256) k_load_grid_line(const GenericArgs a, con
     }
 }
 
-// 3D GRID load vector: b = sum_{vz,vy,vx} PW_z PW_y PW_x g (vertex
-// projection, as k_load), contracted y -> z -> x (the same sum, reordered).  A block owns
-// kLTW x kLTLW lines i2 (kLTLW consecutive lines per warp) x W = 32 - (p + 1) rows i1 and
-// slides along i3 over kLTZ output planes.  The tile's vertex planes (lines + p + 1 rows x 32
-// columns, one column per lane) stream through a shared-memory ring, loaded with cp.async kLTA
-// planes ahead; when plane z arrives each warp contracts it over y for its lines at its column
-// (q(z), into a per-line q ring in shared memory), and every output plane whose window ends at
-// z is finished: s = sum_vz PW_z q (z) per column, then sum_vx PW_x s over each row's window by
-// shuffles (x).  One block barrier per vertex plane; each vertex value is read from global
-// memory once per tile.
-constexpr int kLTW = 4;        // warps per block
-constexpr int kLTLW = 2;       // lines per warp
-constexpr int kLTZ = 32;       // output planes per block
-constexpr int kLTA = 2;        // vertex planes in flight ahead
-constexpr int kLTR = 8;        // q ring depth, a power of two >= p + 2 (a plane's q stays while its window is open)
-constexpr int kLTRR = 4;       // raw ring depth (vertex planes), a power of two >= kLTA + 1
-static_assert(kLTR >= kMaxP + 2 && (kLTR & (kLTR - 1)) == 0, "load q ring depth");
-static_assert(kLTRR >= kLTA + 1 && (kLTRR & (kLTRR - 1)) == 0, "load raw ring depth");
+// 3D GRID load vector, pencil kernel (round 2): the same sum b = sum PW_z PW_y PW_x g, contracted
+// y -> z -> x with every stage in registers except the x halo.  A work column is kLPW lines i2
+// (one per warp) x one x chunk of XO rows; a block slides along i3 through a contiguous range of
+// output planes of one or two columns (the flattened (column, plane) range split evenly over a
+// persistent grid, segments of at most kLPSEG planes).  Lane t owns R consecutive vertex columns
+// c = x0 - P + R t + j (j < R) of its warp's line and the rows i1 = x0 + R t + j, each summed over
+// its natural window, columns i1 - P .. i1 + 1:
+//   y: q_z[j] = sum_vy PW_y[i2][vy] g[z][by + vy][c_j]     (vertex plane z from the smem ring)
+//   z: s[j]   = sum_v Wn_z[i3][v] q_{i3-P+v}[j]            (a V-deep register ring, the z loop
+//                                                            unrolled; i3 = z - 1 ends at plane z)
+//   x: b[i1_j] = sum_v Wn_x[i1_j][v] s[j + v]              (the V - 1 columns past the lane's own
+//                                                            come from lanes t + 1 .. by shuffles)
+// Wn[r][v] = PW[r][v - sh], sh = max(0, P - r): a row r < P has window 0 .. V-1 (b_r = 0), but its
+// basis function lives on elements 0 .. r, so PW[r][v] = 0 for v > r + 1 and the natural window
+// r - P .. r + 1 (vertices < 0 read as zero) carries all of its terms.  The grid tile of each
+// vertex plane (kLPW + V - 1 rows x 32 R columns; out-of-mesh elements zero-filled) streams
+// through a shared-memory ring by 8-byte cp.async, 2 kLPA2 planes ahead; one block barrier per
+// two vertex planes (their y stages and output planes are independent: ILP for the FP64 chains).
+constexpr int kLPW = 8;        // warps (= lines) per block
+constexpr int kLPR = 3;        // vertex columns / rows i1 per lane
+constexpr int kLPA2 = 3;       // plane pairs in flight ahead
+constexpr int kLPRR = 8;       // raw ring depth (power of two >= 2 kLPA2 + 2)
+constexpr int kLPSEG = 96;     // output planes per segment (bounds the staged z weights)
+static_assert(kLPRR >= 2 * kLPA2 + 2 && (kLPRR & (kLPRR - 1)) == 0, "load pencil raw ring depth");
 
 template <int P>
-constexpr size_t load_tile_smem() {
-    constexpr int V = P + 2, LT = kLTW * kLTLW, TILE = (LT + V - 1) * 32;
-    return (size_t)(kLTRR * TILE + LT * kLTR * 32 + kLTZ * V) * sizeof(double);
-}
+struct LoadPencil {
+    static constexpr int V = P + 2;
+    static constexpr int R = kLPR;
+    static constexpr int HL = (V - 1 + R - 1) / R;   // halo lanes
+    static constexpr int XO = (32 - HL) * R;         // rows i1 per x chunk
+    static constexpr int TW = 32 * R;                // tile columns
+    static constexpr int TR = kLPW + V - 1;          // tile rows
+    static constexpr int TILE = TR * TW;
+    static constexpr int UN = V % 2 == 0 ? V : 2 * V; // z unroll: whole ring turns, whole plane pairs
+    static constexpr size_t smem = (size_t)(kLPRR * TILE + kLPSEG * V) * sizeof(double);
+};
 
 template <int P>
-__global__ void __launch_bounds__(kLTW * 32) k_load_grid_tile(const GenericArgs a, const double* PW, double* b) {
-    constexpr int V = P + 2, W = 32 - V + 1, LT = kLTW * kLTLW, EY = LT + V - 1, TILE = EY * 32;
-    constexpr int NT = kLTW * 32, LPT = (TILE + NT - 1) / NT;
-    extern __shared__ __align__(16) double lt_smem[];
-    double* raw = lt_smem;                                      // [kLTRR][EY][32] vertex planes
-    double* qr = raw + kLTRR * TILE;                            // [LT][kLTR][32] y-contracted planes per line
-    double* swz = qr + LT * kLTR * 32;                          // [kLTZ][V] z weights of the block's outputs
+__global__ void __launch_bounds__(kLPW * 32, 2) k_load_grid_pencil(const GenericArgs a, const PW3 PW, double* b,
+                                                                   int dbg) {
+    using LP = LoadPencil<P>;
+    constexpr int V = LP::V, R = LP::R, HL = LP::HL, XO = LP::XO, TW = LP::TW, TR = LP::TR, TILE = LP::TILE,
+                  UN = LP::UN;
+    constexpr int NT = kLPW * 32, LPT = (TILE + NT - 1) / NT;
+    extern __shared__ __align__(16) double lp_smem[];
+    double* raw = lp_smem;                          // [kLPRR][TR][TW] vertex planes
+    double* swz = raw + kLPRR * TILE;               // [kLPSEG][V] natural-window z weights of the segment
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // 32-bit indices: the launcher requires N^3 < 2^31 (so (n + 1)^3 too)
+    // 32-bit indices: the launcher requires N^3 < 2^31
     const int N = (int)a.N, n = (int)a.n, nv = n + 1;
     const int64_t pr = (int64_t)N * N;
-    const int x0 = blockIdx.x * W, y0 = blockIdx.y * LT;
-    const int c0 = x0 - P, by0 = max(0, y0 - P);
+    const double* PWx = PW.d[0];
+    const double* PWy = PW.d[1];
+    const double* PWz = PW.d[2];
     const int zlo_all = (int)(a.row_begin / pr), zhi_all = (int)((a.row_end - 1) / pr);
-    const int z_lo = zlo_all + blockIdx.z * kLTZ;
-    const int z_hi = min(zhi_all + 1, z_lo + kLTZ);
-    if (z_lo >= z_hi) return;
-    // planes: [zs, ze] = the windows of the outputs [z_lo, z_hi)
-    const int zs = max(0, z_lo - P);
-    const int ze = min(n, max(V - 1, z_hi));                     // last output z_hi - 1 needs z_hi
-    const int zg0 = (int)a.coef.plane0, zg1 = (int)(a.coef.plane0 + a.coef.planes);
-    for (int t = tid; t < (z_hi - z_lo) * V; t += NT) swz[t] = __ldg(PW + (z_lo + t / V) * kMaxV + t % V);
-    // load roles: tile element e = tid + NT m -> (row by0 + e / 32, column c0 + e % 32);
-    // out-of-mesh elements are zero-filled (source size 0)
-    int goff[LPT], gsz[LPT];
-    uint32_t sdst[LPT];
-#pragma unroll
-    for (int m = 0; m < LPT; ++m) {
-        const int e = tid + NT * m;
-        const int y = by0 + e / 32, x = c0 + e % 32;
-        const bool ok = e < TILE && y <= n && x >= 0 && x <= n;
-        goff[m] = ok ? y * nv + x : 0;
-        gsz[m] = ok ? 8 : 0;
-        sdst[m] = (uint32_t)__cvta_generic_to_shared(raw + (e < TILE ? e : 0));
-    }
+    const int Zc = zhi_all - zlo_all + 1;
+    const int nxc = (N + XO - 1) / XO, ncol = nxc * ((N + kLPW - 1) / kLPW);
+    const int64_t total = (int64_t)ncol * Zc;
+    const int64_t f1 = total * (blockIdx.x + 1) / gridDim.x;
+    const int zg0 = (int)a.coef.plane0, zg1 = min((int)(a.coef.plane0 + a.coef.planes), n + 1);
     const int plane_el = nv * nv;
-    auto issue = [&](int z) {                                    // one commit group per plane
-        if (z <= ze) {
-            const uint32_t so = (uint32_t)((z & (kLTRR - 1)) * TILE * sizeof(double));
-            if (z >= zg0 && z < zg1) {
-                const double* gz = a.coef.grid + (int64_t)(z - zg0) * plane_el;
+    const int64_t nrows = a.row_end - a.row_begin;
+    for (int64_t f = total * blockIdx.x / gridDim.x; f < f1;) {
+        // segment: column col, output planes [z_lo, z_hi)
+        const int col = (int)(f / Zc);
+        const int z_lo = zlo_all + (int)(f % Zc);
+        const int z_hi = (int)min(min((int64_t)zlo_all + Zc, z_lo + (f1 - f)), (int64_t)z_lo + kLPSEG);
+        f += z_hi - z_lo;
+        const int x0 = (col % nxc) * XO, y0 = (col / nxc) * kLPW;
+        const int by0 = max(0, y0 - P);
+        const int zs = max(0, z_lo - P);
+        const int zend = z_hi;                        // output i3 ends at plane i3 + 1
+        for (int t = tid; t < (z_hi - z_lo) * V; t += NT) {
+            const int i3 = z_lo + t / V, v = t % V, sh = max(0, P - i3);
+            swz[t] = v >= sh ? __ldg(PWz + (int64_t)i3 * kMaxV + v - sh) : 0.0;
+        }
+        // load roles: tile element e = tid + NT m -> (row by0 + e / TW, column x0 - P + e % TW);
+        // out-of-mesh elements are zero-filled (source size 0)
+        int goff[LPT];
+        uint32_t sdst[LPT];
+#pragma unroll
+        for (int m = 0; m < LPT; ++m) {
+            const int e = tid + NT * m;
+            const int y = by0 + e / TW, x = x0 - P + e % TW;
+            const bool ok = e < TILE && y <= n && x >= 0 && x <= n;
+            goff[m] = ok ? y * nv + x : -1;
+            sdst[m] = (uint32_t)__cvta_generic_to_shared(raw + (e < TILE ? e : 0));
+        }
+        auto issue1 = [&](int z) {
+            if (z <= zend) {
+                const uint32_t so = (uint32_t)((z & (kLPRR - 1)) * TILE * sizeof(double));
+                const bool have = z >= zg0 && z < zg1;
+                const double* gz = a.coef.grid + (have ? (int64_t)(z - zg0) * plane_el : 0);
 #pragma unroll
                 for (int m = 0; m < LPT; ++m) {
                     if (TILE % NT != 0 && tid + NT * m >= TILE) break;
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sdst[m] + so), "l"(gz + goff[m]),
-                                 "r"(gsz[m])
-                                 : "memory");
-                }
-            } else {                                             // plane outside the supplied slab: zeros
-#pragma unroll
-                for (int m = 0; m < LPT; ++m) {
-                    if (TILE % NT != 0 && tid + NT * m >= TILE) break;
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, 0;" ::"r"(sdst[m] + so), "l"(a.coef.grid)
+                    const bool ok = have && goff[m] >= 0;
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sdst[m] + so),
+                                 "l"(gz + (ok ? goff[m] : 0)), "r"(ok ? 8 : 0)
                                  : "memory");
                 }
             }
+        };
+        auto issue2 = [&](int z) {                   // planes z, z + 1: one commit group (possibly empty)
+            issue1(z);
+            issue1(z + 1);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        // this warp's line and the lane's rows
+        const int i2 = y0 + warp;
+        const bool lok = i2 < N;
+        const int by = max(0, i2 - P);
+        double wy[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) wy[v] = lok ? __ldg(PWy + (int64_t)i2 * kMaxV + v) : 0.0;
+        double wx[R][V];
+        bool xok[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+            const int i1 = x0 + R * lane + j, sh = max(0, P - i1);
+            xok[j] = lok && lane < 32 - HL && i1 < N;
+#pragma unroll
+            for (int v = 0; v < V; ++v) wx[j][v] = xok[j] && v >= sh ? __ldg(PWx + (int64_t)i1 * kMaxV + v - sh) : 0.0;
         }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-    // this warp's lines i2 = y0 + kLTLW warp + l: rows by_l .. by_l + V - 1 of the tile
-    // (consecutive lines: by_l = by_0 + l except near the mesh start), weights wy[l][v] at the
-    // row offset v + (by_l - by_0) of the warp's row window (zero elsewhere)
-    constexpr int YW = V + kLTLW - 1;                             // rows of the warp's window
-    const int i2w = y0 + kLTLW * warp;
-    const int byw = max(0, i2w - P);
-    const bool yfast = i2w >= P;                                 // by_l = by_0 + l for every line
-    double wy[kLTLW][YW];
-    bool lok[kLTLW];
+        const double* rd = raw + (by - by0) * TW + R * lane;
+        const int64_t rel0 = (int64_t)i2 * N + x0 + R * lane - a.row_begin;   // row (i3 = 0, i1 = x0 + R lane) - row_begin
+        const bool all_in = (int64_t)z_lo * pr >= a.row_begin && (int64_t)z_hi * pr <= a.row_end;
+        auto ystage = [&](double (&q)[R], int z) {
+            const double* rz = rd + (z & (kLPRR - 1)) * TILE;
 #pragma unroll
-    for (int l = 0; l < kLTLW; ++l) {
-        const int i2 = i2w + l;
-        lok[l] = i2 < N;
-        const int d = max(0, i2 - P) - byw;
+            for (int j = 0; j < R; ++j) {
+                q[j] = wy[0] * rz[j];
 #pragma unroll
-        for (int v = 0; v < YW; ++v) {
-            const int vv = v - d;
-            wy[l][v] = (lok[l] && vv >= 0 && vv < V && byw + v <= n) ? __ldg(PW + i2 * kMaxV + vv) : 0.0;
-        }
-    }
-    // x: lane = vertex column c0 + lane; lanes < W also own row i1 = x0 + lane
-    const int i1 = x0 + lane;
-    const bool xok = lane < W && i1 < N;
-    const int off = xok ? max(0, i1 - P) - c0 : 0;
-    double wx[V];
-#pragma unroll
-    for (int v = 0; v < V; ++v) wx[v] = xok ? __ldg(PW + i1 * kMaxV + v) : 0.0;
-    double* q = qr + (kLTLW * warp) * kLTR * 32 + lane;          // q[l][slot] at q[(l kLTR + slot) 32]
-    const double* rl = raw + (byw - by0) * 32 + lane;
-    double* bl = b + ((int64_t)i2w * N + i1 - a.row_begin);      // row (i3 = 0, line i2w) of this lane
-    bool sok[kLTLW];
-#pragma unroll
-    for (int l = 0; l < kLTLW; ++l) sok[l] = xok && lok[l];
-    const bool all_in = (int64_t)z_lo * pr >= a.row_begin && (int64_t)z_hi * pr <= a.row_end;
-    for (int k = 0; k < kLTA; ++k) issue(zs + k);
-    for (int z = zs; z <= ze; ++z) {
-        asm volatile("cp.async.wait_group %0;" ::"n"(kLTA - 1) : "memory");
-        __syncthreads();                                         // plane z landed; raw slot of z - kLTRR + kLTA free
-        issue(z + kLTA);
-        // y stage of plane z at this lane's column, for each line of the warp
-        const int sl = z & (kLTR - 1);
-        const double* rz = rl + (z & (kLTRR - 1)) * TILE;
-        double g[YW];
-#pragma unroll
-        for (int v = 0; v < YW; ++v) g[v] = rz[v * 32];
-        if (yfast) {                                             // line l's window: rows l .. l + V - 1
-#pragma unroll
-            for (int l = 0; l < kLTLW; ++l) {
-                double qz = wy[l][l] * g[l];
-#pragma unroll
-                for (int v = 1; v < V; ++v) qz = fma(wy[l][l + v], g[l + v], qz);
-                q[(l * kLTR + sl) * 32] = qz;
+                for (int v = 1; v < V; ++v) q[j] = fma(wy[v], rz[v * TW + j], q[j]);
             }
-        } else {
-#pragma unroll
-            for (int l = 0; l < kLTLW; ++l) {
-                double qz = 0.0;
-#pragma unroll
-                for (int v = 0; v < YW; ++v) qz = fma(wy[l][v], g[v], qz);
-                q[(l * kLTR + sl) * 32] = qz;
-            }
-        }
-        // the outputs whose window [bz, bz + V - 1] (clipped to the mesh) ends at plane z,
-        // last(i3) = min(n, max(V - 1, i3 + 1)): i3 = z - 1 in the steady state, [0, P] at
-        // z = V - 1, and every remaining output at the last plane
-        int o0 = z - 1, o1 = z - 1;
-        if (z == ze) o0 = z <= V - 1 ? 0 : z - 1, o1 = z_hi - 1;
-        else if (z == V - 1) o0 = 0, o1 = P;
-        else if (z < V - 1) o1 = o0 - 1;                         // none yet
-        o0 = max(o0, z_lo);
-        o1 = min(o1, z_hi - 1);
-        for (int i3 = o0; i3 <= o1; ++i3) {
-            const int bz = max(0, i3 - P);
+        };
+        // output plane i3 whose window ends at plane z = i3 + 1 (its V planes are the ring slots
+        // (u + 1 + v) mod V, u = the slot of plane z)
+        auto output = [&](const double (&qr)[V][R], int u, int i3) {
             const double* wz = swz + (i3 - z_lo) * V;
-            double* bo = bl + (int64_t)i3 * pr;
-            const bool rin = all_in || ((int64_t)i3 * pr + (int64_t)i2w * N + x0 >= a.row_begin &&
-                                        (int64_t)i3 * pr + (int64_t)(i2w + kLTLW - 1) * N + x0 + W <= a.row_end);
-            double s[kLTLW];
+            double s[R];
 #pragma unroll
-            for (int l = 0; l < kLTLW; ++l) {
-                s[l] = 0.0;
+            for (int j = 0; j < R; ++j) {
+                s[j] = wz[0] * qr[(u + 1) % V][j];
 #pragma unroll
-                for (int v = 0; v < V; ++v) s[l] = fma(wz[v], q[(l * kLTR + ((bz + v) & (kLTR - 1))) * 32], s[l]);
+                for (int v = 1; v < V; ++v) s[j] = fma(wz[v], qr[(u + 1 + v) % V][j], s[j]);
             }
-            double acc[kLTLW];
+            double sl[R + V - 1];
 #pragma unroll
-            for (int l = 0; l < kLTLW; ++l) {
-                acc[l] = 0.0;
+            for (int j = 0; j < R; ++j) sl[j] = s[j];
 #pragma unroll
-                for (int v = 0; v < V; ++v) acc[l] = fma(wx[v], __shfl_sync(0xffffffffu, s[l], (off + v) & 31), acc[l]);
+            for (int k = 0; k < V - 1; ++k) sl[R + k] = __shfl_down_sync(0xffffffffu, s[k % R], 1 + k / R);
+            double out[R];
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+                out[j] = wx[j][0] * sl[j];
+#pragma unroll
+                for (int v = 1; v < V; ++v) out[j] = fma(wx[j][v], sl[j + v], out[j]);
             }
-            if (rin) {
+            const int64_t rel = rel0 + (int64_t)i3 * pr;
+            double* bo = b + rel;
+            if (dbg & 1) {
+                if (out[0] == 1.2345) bo[0] = out[1] + out[2];
+            } else if (all_in) {
 #pragma unroll
-                for (int l = 0; l < kLTLW; ++l)
-                    if (sok[l]) bo[(int64_t)l * N] = acc[l];
+                for (int j = 0; j < R; ++j)
+                    if (xok[j]) bo[j] = out[j];
             } else {
 #pragma unroll
-                for (int l = 0; l < kLTLW; ++l) {
-                    const int64_t row = (int64_t)i3 * pr + (int64_t)(i2w + l) * N + i1;
-                    if (sok[l] && row >= a.row_begin && row < a.row_end) bo[(int64_t)l * N] = acc[l];
-                }
+                for (int j = 0; j < R; ++j)
+                    if (xok[j] && rel + j >= 0 && rel + j < nrows) bo[j] = out[j];
+            }
+        };
+        double qr[V][R];
+#pragma unroll
+        for (int u = 0; u < V; ++u)
+#pragma unroll
+            for (int j = 0; j < R; ++j) qr[u][j] = 0.0;
+        for (int k = 0; k < kLPA2; ++k) issue2(zs + 2 * k);
+        for (int zb = zs; zb <= zend; zb += UN) {
+#pragma unroll
+            for (int u = 0; u < UN; u += 2) {
+                const int z = zb + u;
+                if (z > zend) break;
+                asm volatile("cp.async.wait_group %0;" ::"n"(kLPA2 - 1) : "memory");
+                __syncthreads();                      // planes z, z+1 landed; the slots of z-2, z-1 are free
+                issue2(z + 2 * kLPA2);
+                if (dbg & 2) continue;
+                // planes outside the grid slab are zero-filled; plane z + 1 > zend is never output.
+                // Plane z + 1 takes the ring slot of plane z + 1 - V, the first plane of output
+                // z - 1's window: that output is formed first.
+                ystage(qr[u % V], z);
+                if (z - 1 >= z_lo && z - 1 < z_hi) output(qr, u % V, z - 1);
+                ystage(qr[(u + 1) % V], z + 1);
+                if (z >= z_lo && z < z_hi) output(qr, (u + 1) % V, z);
             }
         }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();                              // the ring is reused by the next segment
     }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 template <int P, int D>
-int launch_load_pd(const GenericArgs& a, const double* PW, double* b, bool special, cudaStream_t st) {
+int launch_load_pd(const GenericArgs& a, const PW3& PW, double* b, bool special, cudaStream_t st) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -965,16 +973,29 @@ int launch_load_pd(const GenericArgs& a, const double* PW, double* b, bool speci
     if (special && D == 3 && a.coef.kind == WGQ_COEF_GRID && a.N * a.N * a.N < ((int64_t)1 << 31)) {
         const int64_t pr = a.N * a.N;
         const int64_t planes = (a.row_end - 1) / pr - a.row_begin / pr + 1;
-        constexpr int W = 32 - (P + 2) + 1;
-        constexpr int LT = kLTW * kLTLW;
-        constexpr size_t smem = load_tile_smem<P>();
-        if (cudaFuncSetAttribute(k_load_grid_tile<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-            cudaSuccess)
-            return WGQ_ECUDA;
-        const dim3 g((unsigned)((a.N + W - 1) / W), (unsigned)((a.N + LT - 1) / LT),
-                     (unsigned)((planes + kLTZ - 1) / kLTZ));
-        k_load_grid_tile<P><<<g, kLTW * 32, smem, st>>>(a, PW, b);
-        return cudaGetLastError() == cudaSuccess ? WGQ_OK : WGQ_ECUDA;
+        {
+            using LP = LoadPencil<P>;
+            if (cudaFuncSetAttribute(k_load_grid_pencil<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)LP::smem) != cudaSuccess)
+                return WGQ_ECUDA;
+            int per_sm = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_load_grid_pencil<P>, kLPW * 32, LP::smem);
+            const int64_t ncol = ((a.N + LP::XO - 1) / LP::XO) * ((a.N + kLPW - 1) / kLPW);
+            const int64_t work = ncol * planes;
+            // persistent: one wave, each block >= 16 output planes of work
+            const int64_t nb = std::max<int64_t>(std::max<int64_t>(1, (work + kLPSEG - 1) / kLPSEG),
+                                                 std::min<int64_t>((int64_t)std::max(per_sm, 1) * sms, work / 16));
+            static const int dbg = [] {
+                const char* e = getenv("WGQ_LOAD_DBG");
+                return e ? atoi(e) : 0;
+            }();
+            static const int nb_env = [] {
+                const char* e = getenv("WGQ_LOAD_NB");
+                return e ? atoi(e) : 0;
+            }();
+            k_load_grid_pencil<P><<<(unsigned)(nb_env > 0 ? nb_env : nb), kLPW * 32, LP::smem, st>>>(a, PW, b, dbg);
+            return cudaGetLastError() == cudaSuccess ? WGQ_OK : WGQ_ECUDA;
+        }
     }
     if (special && D >= 2 && a.coef.kind == WGQ_COEF_GRID) {
         const int64_t items = ((a.row_end - 1) / a.N - a.row_begin / a.N + 1) * ((a.N + 31) / 32);
@@ -1202,17 +1223,9 @@ int launch_load(const wgq_rules_s* R, const Tables3& TT, const wgq_coeff_t* c, i
     cudaStream_t st = (cudaStream_t)stream;
     GenericArgs a = base_args(R, TT, c, row_begin, row_end);
     double* tab = nullptr;
-    double* PW = nullptr;
+    const PW3 PW{{TT.t[0].PW, TT.t[1].PW, TT.t[2].PW}};
     int rc = coef_tables(R, a, c, st, &tab);
     if (rc != WGQ_OK) return rc;
-    if (c->kind == WGQ_COEF_GRID) {
-        // PW of direction q at PW + q ctabN kMaxV
-        if (cudaMallocAsync((void**)&PW, (size_t)3 * a.ctabN * kMaxV * sizeof(double), st) != cudaSuccess)
-            return WGQ_ENOMEM;
-        for (int q = 0; q < R->dim; ++q)
-            k_vertex_weights<<<(unsigned)((TT.t[q].N * kMaxV + 255) / 256), 256, 0, st>>>(TT.t[q], R->p,
-                                                                                         PW + q * a.ctabN * kMaxV);
-    }
     int64_t* shell = nullptr;            // 2D shell-row list (stream-ordered scratch)
     if (!force_generic && R->dim == 2 && c->kind == WGQ_COEF_FOURIER_LOGN && a.coef.n_modes > 0) {
         // the 2D tensor-core kernel in load mode (its exponent product and exp, no y / x stages),
@@ -1241,7 +1254,6 @@ int launch_load(const wgq_rules_s* R, const Tables3& TT, const wgq_coeff_t* c, i
     }
     if (shell) cudaFreeAsync(shell, st);
     if (tab) cudaFreeAsync(tab, st);
-    if (PW) cudaFreeAsync(PW, st);
     return rc;
 }
 

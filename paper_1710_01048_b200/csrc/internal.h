@@ -92,6 +92,9 @@ struct RowTables {
     // to c * B_{r+o} when c is the vertex field's linear interpolant (R6).
     double* PM = nullptr;      // [N][kMaxV][kMaxS]
     double* PK = nullptr;      // [N][kMaxV][kMaxS]
+    // PW[r][v] = sum_o PM[r][v][o] = sum_k wM[k] lambda_v(x_k) (partition of unity): the mass
+    // rule's weight on vertex plane b_r + v, the load vector's vertex projection
+    double* PW = nullptr;      // [N][kMaxV]
     // Weighted 1D tables of the first 8 nodes, for the 2D FOURIER kernels (fourier2d.cu):
     // AW[r][kind][k][o] = w_k B_{r+o}(x_k) (kind 0, mass) / w_k B'_{r+o}(x_k) (kind 1), o < 7, zero
     // for k >= m and o = 7 (rows with more than 8 nodes are not read through it)

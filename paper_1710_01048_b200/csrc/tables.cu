@@ -170,6 +170,15 @@ __global__ void k_vertex_tables(int p, int64_t n, RowTables T) {
     (kind == WGQ_MASS ? T.PM : T.PK)[(r * kMaxV + v) * kMaxS + o] = acc;
 }
 
+// PW[r][v] = sum_o PM[r][v][o] (the row's 2p+1 neighbours; the load vector's vertex weights)
+__global__ void k_vertex_weights(RowTables T, int p) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= T.N * kMaxV) return;
+    double s = 0.0;
+    for (int o = 0; o < 2 * p + 1; ++o) s += T.PM[e * kMaxS + o];
+    T.PW[e] = s;
+}
+
 // AW[r][kind][k][o] = w_k A_k[o] for the first 8 nodes (fourier2d.cu): one thread per entry.
 __global__ void k_weighted_tables(RowTables T) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -191,6 +200,7 @@ int build_row_tables(const wgq_rules_s* R, int64_t n_dir, RowTables* T, void* st
     size_t bytes = 2 * N * sizeof(int) +
                    N * (kMaxMassNodes * (2 + kMaxS) + kMaxStiffNodes * (2 + kMaxS) + 2 * kMaxV * kMaxS) * sizeof(double);
     bytes += N * 128 * sizeof(double);         // AW
+    bytes += N * kMaxV * sizeof(double);       // PW
     bytes += 256;
     void* base = nullptr;
     if (cudaMalloc(&base, bytes) != cudaSuccess) return WGQ_ECUDA;
@@ -206,6 +216,7 @@ int build_row_tables(const wgq_rules_s* R, int64_t n_dir, RowTables* T, void* st
     T->PM = d; d += N * kMaxV * kMaxS;
     T->PK = d; d += N * kMaxV * kMaxS;
     T->AW = d; d += N * 128;
+    T->PW = d; d += N * kMaxV;
     T->mM = (int*)d;
     T->mK = T->mM + N;
     T->maxM = T->maxK = 0;
@@ -230,6 +241,7 @@ int build_row_tables(const wgq_rules_s* R, int64_t n_dir, RowTables* T, void* st
     const int64_t vthreads = N * 2 * kMaxV * kMaxS;
     k_vertex_tables<<<(unsigned)((vthreads + 255) / 256), 256, 0, (cudaStream_t)stream>>>(R->p, n_dir, *T);
     k_weighted_tables<<<(unsigned)((N * 128 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(*T);
+    k_vertex_weights<<<(unsigned)((N * kMaxV + 255) / 256), 256, 0, (cudaStream_t)stream>>>(*T, R->p);
     if (cudaGetLastError() != cudaSuccess) return WGQ_ECUDA;
     return WGQ_OK;
 }

@@ -200,3 +200,37 @@ def test_load_full_size_c3_sampled_rows():
                                 for a in range(d)) for _ in range(400)}))
     ref = oops.load_rows(p, n, d, rows, desc)
     check(b.cpu().numpy()[rows], ref, np.abs(ref), "C3 load")
+
+
+@pytest.mark.parametrize("p", [2, 3])
+def test_load_grid_chunks_slabs_and_alignment(p):
+    """3D GRID load vector on a mesh that spans several x chunks and z chunks of the pencil kernel
+    (n = 100): whole x-lines at the mesh faces, at the chunk seams and inside against the oracle;
+    the same vector from an 8-byte-misaligned copy of the grid (the bulk loader's odd-parity rows)
+    and, bitwise, from grid slabs (plane0 != 0, misaligned when plane0 is odd) for row ranges
+    that start and end inside z-planes."""
+    from paper_1710_01048_b200 import api, wgq
+    n, d = 100, 3
+    rules = wgq.Rules(p, n, d)
+    N = rules.N
+    host = np.ascontiguousarray(inputs.lognormal_grid(n, seed=33, dim=d))
+    grid = torch.from_numpy(host).cuda()
+    b = api.assemble_load(rules, api.coefficient({"kind": "grid"}, grid, 0))
+    shifted = torch.empty(grid.numel() + 1, dtype=torch.float64, device="cuda")
+    shifted[1:] = grid.reshape(-1)
+    gmis = shifted[1:].view(grid.shape)
+    assert gmis.data_ptr() % 16 != grid.data_ptr() % 16
+    b2 = api.assemble_load(rules, api.coefficient({"kind": "grid"}, gmis, 0))
+    torch.cuda.synchronize()
+    assert torch.equal(b, b2)
+    seam = sorted({0, 1, 2, p, p + 1, 2 * p, 34, 35, 36, 69, 70, 71, 89, 90, 91, 92, 93, N - 3, N - 2, N - 1})
+    rows = np.array([(i3 * N + i2) * N + i1 for i3 in seam[::2] for i2 in seam[1::2] for i1 in range(N)])
+    ref = oops.load_rows(p, n, d, rows, {"kind": "grid", "seed": 33, "sigma": 0.5}, grid=host)
+    check(b.cpu().numpy()[rows], ref, np.abs(ref), ("load chunks", p))
+    for lo, hi in [(3 * N * N + 17, 40 * N * N + 5 * N + 2), (N * N - 1, 2 * N * N + 1),
+                   (70 * N * N + N, rules.n_rows)]:
+        z0, z1 = api.grid_planes_for(rules, lo, hi)
+        c = api.coefficient({"kind": "grid"}, grid[z0:z1 + 1], z0)
+        bs = api.assemble_load(rules, c, lo, hi)
+        torch.cuda.synchronize()
+        assert torch.equal(bs, b[lo:hi]), (lo, hi, z0)
