@@ -103,6 +103,13 @@ __device__ __forceinline__ void store_rows(double* d0, double* d1, const double*
     }
 }
 
+// The interior kernel's per-row store of one staged row pair (line Ln, rows i1, i1 + 1) of matrix
+// mat when the pair is not part of a contiguous run (ragged ranges, padded ld): kept out of line
+// so that its row checks and pointer arithmetic are not hoisted into the run path.
+__device__ __noinline__ void store_pair_general(double* dst, const int64_t* rp, int64_t ld, int64_t N, int hi,
+                                                int64_t row_begin, int64_t row_end, const double* src, int Ln, int i1,
+                                                bool line_ok, int lane, uint64_t pol);
+
 // ---------------------------------------------------------------------------------------------
 // The frame: every 2D row with an index outside class I (and no GL-fallback wide direction),
 // with the interior kernel's structure (2 lines x row pairs, DMMA exponent / y / x chain, table
@@ -383,6 +390,20 @@ __device__ __forceinline__ void f2d_shell_item(const F2fArgs& a, int64_t row, co
     __syncwarp();
 }
 
+__device__ __noinline__ void store_pair_general(double* dst, const int64_t* rp, int64_t ld, int64_t N, int hi,
+                                                int64_t row_begin, int64_t row_end, const double* src, int Ln, int i1,
+                                                bool line_ok, int lane, uint64_t pol) {
+    double* d[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const int64_t grow = (int64_t)Ln * N + i1 + i;
+        const bool ok = line_ok && i1 + i <= hi && grow >= row_begin && grow < row_end;
+        const int64_t orow = grow - row_begin;
+        d[i] = !ok ? nullptr : dst + (rp ? rp[orow] : orow * ld);         // rp: CSR row starts
+    }
+    store_rows(d[0], d[1], src, lane, pol);
+}
+
 // EXACT: cw == 4 KS (every k-step column is a table column, no predicated loads)
 template <int KS, bool EXACT>
 __global__ void __launch_bounds__(kF2iWarps * 32, kF2iMinBlocks) k_f2d_interior(const F2iArgs a, const F2fArgs fa) {
@@ -590,17 +611,9 @@ __global__ void __launch_bounds__(kF2iWarps * 32, kF2iMinBlocks) k_f2d_interior(
                         dl[L][mat] = d + 98;
                         continue;
                     }
-                    const double* src = os + (L * 2 + mat) * kF2iRun + sh[L];
-                    double* d[2];
-#pragma unroll
-                    for (int i = 0; i < 2; ++i) {
-                        const int64_t grow = (int64_t)(La + L) * N + i1 + i;
-                        const bool ok = (L == 0 || bval) && i1 + i <= a.hi && grow >= a.row_begin && grow < a.row_end;
-                        const int64_t orow = grow - a.row_begin;
-                        d[i] = !ok ? nullptr
-                                   : dst + (a.csr ? (mat ? a.rpK : a.rpM)[orow] : orow * (mat ? a.ldK : a.ldM));
-                    }
-                    store_rows(d[0], d[1], src, lane, pol);
+                    store_pair_general(dst, a.csr ? (mat ? a.rpK : a.rpM) : nullptr, mat ? a.ldK : a.ldM, N, a.hi,
+                                       a.row_begin, a.row_end, os + (L * 2 + mat) * kF2iRun + sh[L], La + L, i1,
+                                       L == 0 || bval, lane, pol);
                 }
             }
             __syncwarp();                         // the staging is rewritten by the next pair
