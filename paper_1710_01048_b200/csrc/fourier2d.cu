@@ -32,6 +32,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <type_traits>
 
 #include "internal.h"
 
@@ -71,8 +72,9 @@ __constant__ double kExp5[6] = {1.0, 1.0, 0.5, 1.0 / 6.0, 1.0 / 24.0, 1.0 / 120.
 
 // exp(x), |x| < 700: x = k ln2/64 + r with k = rint(64 x / ln2) (the 1.5*2^52 shifter leaves k
 // in the low word), |r| <= ln2/128 (Cody-Waite two-part ln2/64), e^x = 2^(k>>6) 2^((k&63)/64) e^r.
-// tbl holds 2^(j/64) at [j * 16 + copy]: the 16 lanes of a half-warp read 16 different banks.
-__device__ __forceinline__ double exp_tab(double x, const double* tbl, int copy) {
+// tbl holds 2^(j/64) at [j * 16 + copy], tb = tbl + copy (copy = lane & 15): the 16 lanes of a
+// half-warp read 16 different banks.
+__device__ __forceinline__ double exp_tab(double x, const double* tb) {
     const double s = fma(x, 92.332482616893656877, 6755399441055744.0);   // 64/ln2, 1.5*2^52
     const double kd = s - 6755399441055744.0;
     const int k = __double2loint(s);
@@ -81,7 +83,7 @@ __device__ __forceinline__ double exp_tab(double x, const double* tbl, int copy)
     double q = kExp5[5];
 #pragma unroll
     for (int i = 4; i >= 0; --i) q = fma(q, r, kExp5[i]);
-    const double t = tbl[((k & 63) << 4) | copy];
+    const double t = tb[(k & 63) << 4];
     return q * __hiloint2double(__double2hiint(t) + ((k >> 6) << 20), __double2loint(t));
 }
 
@@ -215,9 +217,9 @@ __device__ __forceinline__ void f2d_frame_item(const F2fArgs& a, int64_t it, con
             dmma(eb0, eb1, XM[s], Yb[s]);
             dmma(ek0, ek1, XK[s], Yab[s]);
         }
-        const double wMa = exp_tab(ea0, tbl, copy), wKya = exp_tab(ea1, tbl, copy);
-        const double wMb = exp_tab(eb0, tbl, copy), wKyb = exp_tab(eb1, tbl, copy);
-        const double wKxa = exp_tab(ek0, tbl, copy), wKxb = exp_tab(ek1, tbl, copy);
+        const double wMa = exp_tab(ea0, tbl + copy), wKya = exp_tab(ea1, tbl + copy);
+        const double wMb = exp_tab(eb0, tbl + copy), wKyb = exp_tab(eb1, tbl + copy);
+        const double wKxa = exp_tab(ek0, tbl + copy), wKxb = exp_tab(ek1, tbl + copy);
         double tM[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, tKx[2][2] = {{0.0, 0.0}, {0.0, 0.0}},
                tKy[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
         dmma(tM[0][0], tM[0][1], aMa, wMa);
@@ -335,9 +337,9 @@ __device__ __forceinline__ void f2d_shell_item(const F2fArgs& a, int64_t row, co
         dmma(eb0, eb1, XM[s], Yb[s]);
         dmma(ek0, ek1, XK[s], Yab[s]);
     }
-    const double wMa = exp_tab(ea0, tbl, copy), wKya = exp_tab(ea1, tbl, copy);
-    const double wMb = exp_tab(eb0, tbl, copy), wKyb = exp_tab(eb1, tbl, copy);
-    const double wKxa = exp_tab(ek0, tbl, copy), wKxb = exp_tab(ek1, tbl, copy);
+    const double wMa = exp_tab(ea0, tbl + copy), wKya = exp_tab(ea1, tbl + copy);
+    const double wMb = exp_tab(eb0, tbl + copy), wKyb = exp_tab(eb1, tbl + copy);
+    const double wKxa = exp_tab(ek0, tbl + copy), wKxb = exp_tab(ek1, tbl + copy);
     double tM[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, tKx[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, tKy[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
     dmma(tM[0][0], tM[0][1], aMa, wMa);
     dmma(tKy[0][0], tKy[0][1], aKa, wKya);
@@ -404,8 +406,9 @@ __device__ __noinline__ void store_pair_general(double* dst, const int64_t* rp, 
     store_rows(d[0], d[1], src, lane, pol);
 }
 
-// EXACT: cw == 4 KS (every k-step column is a table column, no predicated loads)
-template <int KS, bool EXACT>
+// EXACT: cw == 4 KS (every k-step column is a table column, no predicated loads); DBG: the
+// profiling switches (WGQ_F2D_DBG; 0 in production: no switch code in the hot loop)
+template <int KS, bool EXACT, int DBG>
 __global__ void __launch_bounds__(kF2iWarps * 32, kF2iMinBlocks) k_f2d_interior(const F2iArgs a, const F2fArgs fa) {
     constexpr int S = 7;
     __shared__ double tbl[64 * 16];
@@ -413,7 +416,7 @@ __global__ void __launch_bounds__(kF2iWarps * 32, kF2iMinBlocks) k_f2d_interior(
     for (int e = threadIdx.x; e < 64 * 16; e += blockDim.x) tbl[e] = exp2((double)(e >> 4) * (1.0 / 64.0));
     __syncthreads();
     const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, warp = threadIdx.x >> 5;
-    const int copy = lane & 15;
+    const double* tb = tbl + (lane & 15);
     double* ws = stage + warp * kF2iWarpSmem;
     double* os = ws;
     const uint64_t pol = pol_evict_first();
@@ -511,7 +514,8 @@ __global__ void __launch_bounds__(kF2iWarps * 32, kF2iMinBlocks) k_f2d_interior(
             }
             sb[L] = os + L * 2 * kF2iRun + sh[L] + g + 14 * t;
         }
-        // x-node g of the pair = (kx = g >> 1, row i1 + (g & 1)); prefetched one pair ahead
+        // x-node g of the pair = (kx = g >> 1, row i1 + (g & 1)); prefetched one pair ahead (the
+        // last step re-reads its own pair: no branch in the loop)
         const double* pxm = a.ctab + (int64_t)(a.lo + 2 * p0 + (g & 1)) * nstride + (g >> 1) * cw + jt;
         const double* pxk = pxm + N * nstride;
         double XM[KS], XK[KS];
@@ -521,103 +525,112 @@ __global__ void __launch_bounds__(kF2iWarps * 32, kF2iMinBlocks) k_f2d_interior(
             XM[s] = in && p0 < p1 ? __ldg(pxm + 4 * s) : 0.0;
             XK[s] = in && p0 < p1 ? __ldg(pxk + 4 * s) : 0.0;
         }
-        for (int pr = p0; pr < p1; ++pr) {
-            const int i1 = a.lo + 2 * pr;
-            // ---- exponents (a3): three 8 x 8 x 2n_modes products
-            double ea0 = 0.0, ea1 = 0.0, eb0 = 0.0, eb1 = 0.0, ek0 = 0.0, ek1 = 0.0;
-            if (a.dbg & 2) {
-                ea0 = XM[0], ea1 = XM[1], eb0 = XM[2], eb1 = XM[3], ek0 = XK[0], ek1 = XK[1];
-            } else
+        // FAST: both lines are full runs of both matrices (the common case): the store code is
+        // straight-line (lane predicates only)
+        auto steps = [&](auto fastc) {
+            constexpr bool FAST = decltype(fastc)::value;
+            for (int pr = p0; pr < p1; ++pr) {
+                const int i1 = a.lo + 2 * pr;
+                // ---- exponents (a3): three 8 x 8 x 2n_modes products
+                double ea0 = 0.0, ea1 = 0.0, eb0 = 0.0, eb1 = 0.0, ek0 = 0.0, ek1 = 0.0;
+                if constexpr (DBG & 2) {
+                    ea0 = XM[0], ea1 = XM[1], eb0 = XM[2], eb1 = XM[3], ek0 = XK[0], ek1 = XK[1];
+                } else {
 #pragma unroll
-            for (int s = 0; s < KS; ++s) {
-                dmma(ea0, ea1, XM[s], Ya[s]);
-                dmma(eb0, eb1, XM[s], Yb[s]);
-                dmma(ek0, ek1, XK[s], Yab[s]);
-            }
-            pxm += 2 * nstride;
-            pxk += 2 * nstride;
-            if (pr + 1 < p1) {
+                    for (int s = 0; s < KS; ++s) {
+                        dmma(ea0, ea1, XM[s], Ya[s]);
+                        dmma(eb0, eb1, XM[s], Yb[s]);
+                        dmma(ek0, ek1, XK[s], Yab[s]);
+                    }
+                }
+                const int64_t adv = pr + 1 < p1 ? 2 * nstride : 0;
+                pxm += adv;
+                pxk += adv;
 #pragma unroll
                 for (int s = 0; s < KS; ++s) {
                     const bool in = EXACT || 4 * s + jt < cw;
                     XM[s] = in ? __ldg(pxm + 4 * s) : 0.0;
                     XK[s] = in ? __ldg(pxk + 4 * s) : 0.0;
                 }
-            }
-            // ---- samples c = exp(E): lane (g, t) holds x-node g against y-node (ky = t, *)
-            double wMa, wKya, wMb, wKyb, wKxa, wKxb;
-            if (a.dbg & 2) {
-                wMa = ea0, wKya = ea1, wMb = eb0, wKyb = eb1, wKxa = ek0, wKxb = ek1;
-            } else {
-                wMa = exp_tab(ea0, tbl, copy), wKya = exp_tab(ea1, tbl, copy);
-                wMb = exp_tab(eb0, tbl, copy), wKyb = exp_tab(eb1, tbl, copy);
-                wKxa = exp_tab(ek0, tbl, copy), wKxb = exp_tab(ek1, tbl, copy);
-            }
-            // ---- y stage (a5): T^T[o2][x-node] = Aw_y^T[o2][ky] W^T[ky][x-node]
-            double tM[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, tKx[2][2] = {{0.0, 0.0}, {0.0, 0.0}},
-                   tKy[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-            dmma(tM[0][0], tM[0][1], aMy, wMa);
-            dmma(tKy[0][0], tKy[0][1], aKy, wKya);
-            dmma(tKx[0][0], tKx[0][1], aMy, wKxa);
-            dmma(tM[1][0], tM[1][1], aMy, wMb);
-            dmma(tKy[1][0], tKy[1][1], aKy, wKyb);
-            dmma(tKx[1][0], tKx[1][1], aMy, wKxb);
-            // lane (g, t) now holds T[line][row i][kx = t][o2 = g] in component i: exactly the B
-            // fragment of the x stage of row i,
-            // ---- x stage (a5, a6) on DMMA: M[o1][o2] = Aw_x^T[o1][kx] T[kx][o2] (the class-I A
-            // operand Aw^T[o1 = g][kx = t] is the y stage's), K = AwK_x^T T_Kx + AwM_x^T T_Ky;
-            // lane (g, t) receives M[o1 = g][o2 = 2t + j], staged at slot o1 + 7 o2 of its row
+                // ---- samples c = exp(E): lane (g, t) holds x-node g against y-node (ky = t, *)
+                double wMa, wKya, wMb, wKyb, wKxa, wKxb;
+                if constexpr (DBG & 2) {
+                    wMa = ea0, wKya = ea1, wMb = eb0, wKyb = eb1, wKxa = ek0, wKxb = ek1;
+                } else {
+                    wMa = exp_tab(ea0, tb), wKya = exp_tab(ea1, tb);
+                    wMb = exp_tab(eb0, tb), wKyb = exp_tab(eb1, tb);
+                    wKxa = exp_tab(ek0, tb), wKxb = exp_tab(ek1, tb);
+                }
+                // ---- y stage (a5): T^T[o2][x-node] = Aw_y^T[o2][ky] W^T[ky][x-node]
+                double tM[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, tKx[2][2] = {{0.0, 0.0}, {0.0, 0.0}},
+                       tKy[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+                dmma(tM[0][0], tM[0][1], aMy, wMa);
+                dmma(tKy[0][0], tKy[0][1], aKy, wKya);
+                dmma(tKx[0][0], tKx[0][1], aMy, wKxa);
+                dmma(tM[1][0], tM[1][1], aMy, wMb);
+                dmma(tKy[1][0], tKy[1][1], aKy, wKyb);
+                dmma(tKx[1][0], tKx[1][1], aMy, wKxb);
+                // lane (g, t) now holds T[line][row i][kx = t][o2 = g] in component i: exactly the B
+                // fragment of the x stage of row i,
+                // ---- x stage (a5, a6) on DMMA: M[o1][o2] = Aw_x^T[o1][kx] T[kx][o2] (the class-I A
+                // operand Aw^T[o1 = g][kx = t] is the y stage's), K = AwK_x^T T_Kx + AwM_x^T T_Ky;
+                // lane (g, t) receives M[o1 = g][o2 = 2t + j], staged at slot o1 + 7 o2 of its row
 #pragma unroll
-            for (int L = 0; L < 2; ++L)
+                for (int L = 0; L < 2; ++L)
 #pragma unroll
-                for (int i = 0; i < 2; ++i) {
-                    double m0 = 0.0, m1 = 0.0, k0 = 0.0, k1 = 0.0;
-                    dmma(m0, m1, aMy, tM[L][i]);
-                    dmma(k0, k1, aKy, tKx[L][i]);
-                    dmma(k0, k1, aMy, tKy[L][i]);
-                    double* b = sb[L] + i * 49;
-                    if (g < S) {
-                        b[0] = m0;
-                        b[kF2iRun] = k0;
-                        if (t < 3) {
-                            b[7] = m1;
-                            b[kF2iRun + 7] = k1;
+                    for (int i = 0; i < 2; ++i) {
+                        double m0 = 0.0, m1 = 0.0, k0 = 0.0, k1 = 0.0;
+                        dmma(m0, m1, aMy, tM[L][i]);
+                        dmma(k0, k1, aKy, tKx[L][i]);
+                        dmma(k0, k1, aMy, tKy[L][i]);
+                        double* b = sb[L] + i * 49;
+                        if (g < S) {
+                            b[0] = m0;
+                            b[kF2iRun] = k0;
+                            if (t < 3) {
+                                b[7] = m1;
+                                b[kF2iRun + 7] = k1;
+                            }
                         }
                     }
-                }
-            __syncwarp();
-            // ---- a7: the two rows of each line (one 98-double run when full[L]: 16-byte streaming
-            // stores, loads from the staging first), M and K
+                __syncwarp();
+                // ---- a7: the two rows of each line (one 98-double run when full[L]: 16-byte
+                // streaming stores, loads from the staging first), M and K
 #pragma unroll
-            for (int L = 0; L < 2; ++L) {
+                for (int L = 0; L < 2; ++L) {
 #pragma unroll
-                for (int mat = 0; mat < 2; ++mat) {
-                    double* dst = mat ? a.Kv : a.Mv;
-                    if (!dst || (a.dbg & 1)) continue;
-                    if (full[L]) {
-                        // this lane's 16-byte pair(s) of the run; with sh = 1 lanes 0 / 1 also
-                        // store the run's first / last element (offsets -1 / +94 from their pair)
-                        const double* sp = sl[L][mat];
-                        const double2 v0 = *reinterpret_cast<const double2*>(sp);
-                        double2 v1 = make_double2(0.0, 0.0);
-                        const bool two = lane + 32 < 49 - sh[L];
-                        if (two) v1 = *reinterpret_cast<const double2*>(sp + 64);
-                        const bool edge = sh[L] && lane < 2;
-                        const double ve = edge ? sp[lane ? 94 : -1] : 0.0;
-                        double* d = dl[L][mat];
-                        st_out2(d, v0.x, v0.y, pol);
-                        if (two) st_out2(d + 64, v1.x, v1.y, pol);
-                        if (edge) st_out(d + (lane ? 94 : -1), ve, pol);
-                        dl[L][mat] = d + 98;
-                        continue;
+                    for (int mat = 0; mat < 2; ++mat) {
+                        double* dst = mat ? a.Kv : a.Mv;
+                        if constexpr (DBG & 1) continue;
+                        if (FAST || full[L]) {
+                            if (!FAST && !dst) continue;
+                            // this lane's 16-byte pair(s) of the run; with sh = 1 lanes 0 / 1 also
+                            // store the run's first / last element (offsets -1 / +94 from their pair)
+                            const double* sp = sl[L][mat];
+                            const double2 v0 = *reinterpret_cast<const double2*>(sp);
+                            double2 v1 = make_double2(0.0, 0.0);
+                            const bool two = lane + 32 < 49 - sh[L];
+                            if (two) v1 = *reinterpret_cast<const double2*>(sp + 64);
+                            const bool edge = sh[L] && lane < 2;
+                            const double ve = edge ? sp[lane ? 94 : -1] : 0.0;
+                            double* d = dl[L][mat];
+                            st_out2(d, v0.x, v0.y, pol);
+                            if (two) st_out2(d + 64, v1.x, v1.y, pol);
+                            if (edge) st_out(d + (lane ? 94 : -1), ve, pol);
+                            dl[L][mat] = d + 98;
+                            continue;
+                        }
+                        if (!dst) continue;
+                        store_pair_general(dst, a.csr ? (mat ? a.rpK : a.rpM) : nullptr, mat ? a.ldK : a.ldM, N,
+                                           a.hi, a.row_begin, a.row_end, os + (L * 2 + mat) * kF2iRun + sh[L], La + L,
+                                           i1, L == 0 || bval, lane, pol);
                     }
-                    store_pair_general(dst, a.csr ? (mat ? a.rpK : a.rpM) : nullptr, mat ? a.ldK : a.ldM, N, a.hi,
-                                       a.row_begin, a.row_end, os + (L * 2 + mat) * kF2iRun + sh[L], La + L, i1,
-                                       L == 0 || bval, lane, pol);
                 }
+                __syncwarp();                         // the staging is rewritten by the next pair
             }
-            __syncwarp();                         // the staging is rewritten by the next pair
-        }
+        };
+        if (full[0] && full[1] && a.Mv && a.Kv) steps(std::true_type{});
+        else steps(std::false_type{});
     }
 }
 
@@ -732,10 +745,13 @@ int launch_f2d_interior(const wgq_rules_s* R, const RowTables& T, const double* 
         return WGQ_OK;
     };
     int rc;
-    if (cw == 16) rc = go(k_f2d_interior<4, true>);
-    else if (cw < 16) rc = go(k_f2d_interior<4, false>);
-    else if (cw == 32) rc = go(k_f2d_interior<8, true>);
-    else rc = go(k_f2d_interior<8, false>);
+    if (cw == 16 && dbg == 1) rc = go(k_f2d_interior<4, true, 1>);
+    else if (cw == 16 && dbg == 2) rc = go(k_f2d_interior<4, true, 2>);
+    else if (cw == 16 && dbg == 3) rc = go(k_f2d_interior<4, true, 3>);
+    else if (cw == 16) rc = go(k_f2d_interior<4, true, 0>);
+    else if (cw < 16) rc = go(k_f2d_interior<4, false, 0>);
+    else if (cw == 32) rc = go(k_f2d_interior<8, true, 0>);
+    else rc = go(k_f2d_interior<8, false, 0>);
     if (rc != WGQ_OK) return rc;
     return cudaGetLastError() == cudaSuccess ? WGQ_OK : WGQ_ECUDA;
 }
