@@ -23,10 +23,12 @@
 //    polynomial on |r| <= ln2/128 (10 FP64 operations, < 1 ulp before rounding);
 //  * y stage on DMMA: the exp'd accumulator fragment is the B operand of T^T = Aw_y^T W^T as is
 //    (6 DMMA per 4 rows);
-//  * x stage on DFMA with the structural zeros of the class-I tables skipped (16 of 28 per term;
-//    coefficients from the kernel-parameter constant bank), lanes own (row, o2) columns;
-//  * the rows are staged in shared memory and written as contiguous runs with streaming stores.
-// The frame (rows with an index outside class I) goes through k_fourier2d (assemble.cu).
+//  * x stage on DMMA: the y stage's output fragment is the B operand as is, the class-I Aw_x^T
+//    fragment the y stage's A operand (12 DMMA per 4 rows);
+//  * the rows are staged in shared memory (a bank-permuted slot layout, kF2iSlot: conflict-free
+//    x-stage writes and run reads) and written as contiguous 16-byte runs with streaming stores.
+// The frame rows (an index outside class I) and the split GL shell rows are extra items of the
+// same launch (f2d_frame_item, f2d_shell_item).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -42,8 +44,24 @@ namespace {
 constexpr int kF2iWarps = 8;
 constexpr int kF2iMinBlocks = 2;
 constexpr int kF2iChunk = 16;              // row pairs per work item (the line pair's y data is loaded once)
-constexpr int kF2iRun = 100;                             // staging of one (line, matrix) run: 2 rows + shift + pad
-constexpr int kF2iWarpSmem = 4 * kF2iRun;                // output staging of 2 lines x M, K
+constexpr int kF2iRun = 112;                             // staging of one (line, matrix) run (56 16-byte slots)
+// output staging of 2 lines x M, K
+constexpr int kF2iWarpSmem = 4 * kF2iRun;
+
+// Interior-kernel staging layout: element s (= run element + shift sh) of a (line, matrix) run
+// lives in 16-byte slot kF2iSlot[sh][s >> 1], half s & 1.  The slots were searched
+// (tools/staging_layout.py) so that, for either shift, every x-stage write (lane (g, t) ->
+// elements g + 14 t + 7 j + 49 i + sh; 64-bit accesses are served per half-warp) hits 16 distinct
+// 8-byte banks per half-warp and every 16-byte run read (lane -> pair lane + sh, lane + 32 + sh;
+// served per quarter-warp) 8 distinct 16-byte bank groups per quarter-warp: 2 wavefronts per
+// x-stage write (the natural layout took 4) and the minimum for the reads.
+__constant__ int kF2iSlot[2][50] = {
+    {5,  3,  2,  1,  6,  7,  0,  4,  14, 15, 13, 10, 11, 12, 9,  8,  19, 16, 20, 21, 17, 18, 23, 22, 28,
+     25, 30, 31, 26, 24, 27, 29, 39, 34, 35, 37, 33, 36, 38, 32, 44, 40, 47, 46, 41, 42, 43, 45, 49, 48},
+    {51, 7,  3,  1,  0,  2,  5,  6,  4,  8,  12, 15, 9,  11, 10, 13, 14, 23, 22, 19, 20, 16, 17, 18, 21,
+     25, 28, 31, 26, 27, 24, 30, 29, 34, 37, 32, 33, 39, 36, 38, 35, 41, 46, 44, 42, 45, 40, 47, 43, 52}};
+constexpr int kF2iEdge0 = 2 * 51 + 1;     // element 0 of a shifted run (s = 1): pair 0, high half
+constexpr int kF2iEdge1 = 2 * 52;         // element 97 of a shifted run (s = 98): pair 49, low half
 
 struct F2iArgs {
     const double* ctab;  // k_coef_tables layout: ((kind * N + r) * kMaxNodes + k) * cw + j
@@ -97,20 +115,13 @@ __device__ __forceinline__ void st_out2(double* p, double v0, double v1, uint64_
                  : "memory");
 }
 
-// The general case: the two staged rows src[0..48], src[49..97] at d0, d1 (null: not stored).
-__device__ __forceinline__ void store_rows(double* d0, double* d1, const double* src, int lane, uint64_t pol) {
-    for (int e = lane; e < 98; e += 32) {
-        double* p = e < 49 ? d0 : d1;
-        if (p) st_out(p + (e < 49 ? e : e - 49), src[e], pol);
-    }
-}
-
 // The interior kernel's per-row store of one staged row pair (line Ln, rows i1, i1 + 1) of matrix
 // mat when the pair is not part of a contiguous run (ragged ranges, padded ld): kept out of line
 // so that its row checks and pointer arithmetic are not hoisted into the run path.
 __device__ __noinline__ void store_pair_general(double* dst, const int64_t* rp, int64_t ld, int64_t N, int hi,
-                                                int64_t row_begin, int64_t row_end, const double* src, int Ln, int i1,
-                                                bool line_ok, int lane, uint64_t pol);
+                                                int64_t row_begin, int64_t row_end, const double* src, int shv,
+                                                const int* slot, int Ln, int i1, bool line_ok, int lane,
+                                                uint64_t pol);
 
 // ---------------------------------------------------------------------------------------------
 // The frame: every 2D row with an index outside class I (and no GL-fallback wide direction),
@@ -393,8 +404,9 @@ __device__ __forceinline__ void f2d_shell_item(const F2fArgs& a, int64_t row, co
 }
 
 __device__ __noinline__ void store_pair_general(double* dst, const int64_t* rp, int64_t ld, int64_t N, int hi,
-                                                int64_t row_begin, int64_t row_end, const double* src, int Ln, int i1,
-                                                bool line_ok, int lane, uint64_t pol) {
+                                                int64_t row_begin, int64_t row_end, const double* src, int shv,
+                                                const int* slot, int Ln, int i1, bool line_ok, int lane,
+                                                uint64_t pol) {
     double* d[2];
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
@@ -403,7 +415,11 @@ __device__ __noinline__ void store_pair_general(double* dst, const int64_t* rp, 
         const int64_t orow = grow - row_begin;
         d[i] = !ok ? nullptr : dst + (rp ? rp[orow] : orow * ld);         // rp: CSR row starts
     }
-    store_rows(d[0], d[1], src, lane, pol);
+    for (int e = lane; e < 98; e += 32) {             // src: the run's staging (slot layout)
+        double* p = e < 49 ? d[0] : d[1];
+        const int se = e + shv;
+        if (p) st_out(p + (e < 49 ? e : e - 49), src[2 * slot[50 * shv + (se >> 1)] + (se & 1)], pol);
+    }
 }
 
 // EXACT: cw == 4 KS (every k-step column is a table column, no predicated loads); DBG: the
@@ -412,8 +428,10 @@ template <int KS, bool EXACT, int DBG>
 __global__ void __launch_bounds__(kF2iWarps * 32, kF2iMinBlocks) k_f2d_interior(const F2iArgs a, const F2fArgs fa) {
     constexpr int S = 7;
     __shared__ double tbl[64 * 16];
+    __shared__ int slot_s[2 * 50];
     extern __shared__ double stage[];      // per warp: T staging, output staging
     for (int e = threadIdx.x; e < 64 * 16; e += blockDim.x) tbl[e] = exp2((double)(e >> 4) * (1.0 / 64.0));
+    if (threadIdx.x < 100) slot_s[threadIdx.x] = kF2iSlot[threadIdx.x / 50][threadIdx.x % 50];
     __syncthreads();
     const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, warp = threadIdx.x >> 5;
     const double* tb = tbl + (lane & 15);
@@ -503,16 +521,23 @@ __global__ void __launch_bounds__(kF2iWarps * 32, kF2iMinBlocks) k_f2d_interior(
                 full[L] = false, sh[L] = 0;
         }
         double* dl[2][2];                 // per lane: its 16-byte pair of the (L, mat) run of this step
-        const double* sl[2][2];           // and of the staging
-        double* sb[2];                    // x-stage staging base of line L for lane (g, t)
+        int woff[2][2][2];                // staging offsets of the lane's x-stage outputs [L][row i][o2 = 2t + j]
+        int roff[2][2];                   // and of its 16-byte pairs lane + sh, lane + 32 + sh of line L's run
 #pragma unroll
         for (int L = 0; L < 2; ++L) {
+            const int r0 = L * 2 * kF2iRun;
 #pragma unroll
-            for (int mat = 0; mat < 2; ++mat) {
-                dl[L][mat] = base[L][mat] ? base[L][mat] + sh[L] + 2 * lane : nullptr;
-                sl[L][mat] = os + (L * 2 + mat) * kF2iRun + 2 * sh[L] + 2 * lane;
-            }
-            sb[L] = os + L * 2 * kF2iRun + sh[L] + g + 14 * t;
+            for (int mat = 0; mat < 2; ++mat) dl[L][mat] = base[L][mat] ? base[L][mat] + sh[L] + 2 * lane : nullptr;
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const int e = min(g + 14 * t + 7 * j + 49 * i + sh[L], 99);
+                    woff[L][i][j] = r0 + 2 * slot_s[50 * sh[L] + (e >> 1)] + (e & 1);
+                }
+            const int q1 = lane + 32 + sh[L];
+            roff[L][0] = r0 + 2 * slot_s[50 * sh[L] + lane + sh[L]];
+            roff[L][1] = r0 + 2 * slot_s[50 * sh[L] + (q1 < 50 ? q1 : lane + sh[L])];
         }
         // x-node g of the pair = (kx = g >> 1, row i1 + (g & 1)); prefetched one pair ahead (the
         // last step re-reads its own pair: no branch in the loop)
@@ -583,13 +608,12 @@ __global__ void __launch_bounds__(kF2iWarps * 32, kF2iMinBlocks) k_f2d_interior(
                         dmma(m0, m1, aMy, tM[L][i]);
                         dmma(k0, k1, aKy, tKx[L][i]);
                         dmma(k0, k1, aMy, tKy[L][i]);
-                        double* b = sb[L] + i * 49;
-                        if (g < S) {
-                            b[0] = m0;
-                            b[kF2iRun] = k0;
+                        if (g < S) {                     // (o1 = 7, o2 = 7: padding)
+                            os[woff[L][i][0]] = m0;
+                            os[woff[L][i][0] + kF2iRun] = k0;
                             if (t < 3) {
-                                b[7] = m1;
-                                b[kF2iRun + 7] = k1;
+                                os[woff[L][i][1]] = m1;
+                                os[woff[L][i][1] + kF2iRun] = k1;
                             }
                         }
                     }
@@ -606,13 +630,13 @@ __global__ void __launch_bounds__(kF2iWarps * 32, kF2iMinBlocks) k_f2d_interior(
                             if (!FAST && !dst) continue;
                             // this lane's 16-byte pair(s) of the run; with sh = 1 lanes 0 / 1 also
                             // store the run's first / last element (offsets -1 / +94 from their pair)
-                            const double* sp = sl[L][mat];
-                            const double2 v0 = *reinterpret_cast<const double2*>(sp);
-                            double2 v1 = make_double2(0.0, 0.0);
+                            const double* sp = os + mat * kF2iRun;
+                            const double2 v0 = *reinterpret_cast<const double2*>(sp + roff[L][0]);
                             const bool two = lane + 32 < 49 - sh[L];
-                            if (two) v1 = *reinterpret_cast<const double2*>(sp + 64);
+                            double2 v1 = make_double2(0.0, 0.0);
+                            if (two) v1 = *reinterpret_cast<const double2*>(sp + roff[L][1]);
                             const bool edge = sh[L] && lane < 2;
-                            const double ve = edge ? sp[lane ? 94 : -1] : 0.0;
+                            const double ve = edge ? sp[L * 2 * kF2iRun + (lane ? kF2iEdge1 : kF2iEdge0)] : 0.0;
                             double* d = dl[L][mat];
                             st_out2(d, v0.x, v0.y, pol);
                             if (two) st_out2(d + 64, v1.x, v1.y, pol);
@@ -622,8 +646,8 @@ __global__ void __launch_bounds__(kF2iWarps * 32, kF2iMinBlocks) k_f2d_interior(
                         }
                         if (!dst) continue;
                         store_pair_general(dst, a.csr ? (mat ? a.rpK : a.rpM) : nullptr, mat ? a.ldK : a.ldM, N,
-                                           a.hi, a.row_begin, a.row_end, os + (L * 2 + mat) * kF2iRun + sh[L], La + L,
-                                           i1, L == 0 || bval, lane, pol);
+                                           a.hi, a.row_begin, a.row_end, os + (L * 2 + mat) * kF2iRun, sh[L], slot_s,
+                                           La + L, i1, L == 0 || bval, lane, pol);
                     }
                 }
                 __syncwarp();                         // the staging is rewritten by the next pair
