@@ -121,37 +121,46 @@ struct Dir {
 // expansion of cos(2 pi k_m . x + theta_m) (R13), exact up to rounding.
 __global__ void k_coef_tables(const CoefDev c, int dim, const RowTables T3a, const RowTables T3b, const RowTables T3c,
                               int64_t ctabN, double* tab, int cw) {
+    // one thread per (table entry, mode) (FOURIER; one per entry for TRIG_SEP): the modes of an
+    // entry are independent, and a warp writes 32 consecutive 16-byte column pairs.  Every slot is
+    // written (zeros for node slots beyond the rule and rows beyond the direction's count).
+    const int nq = c.kind == WGQ_COEF_FOURIER_LOGN && c.n_modes > 0 ? c.n_modes : 1;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t e = tid / nq;
+    const int q = (int)(tid % nq);
     const int64_t per_ak = ctabN * kMaxNodes;
-    const int64_t ak = tid / per_ak;
+    const int64_t ak = e / per_ak;
     if (ak >= 2 * dim) return;
     const int a = (int)(ak / 2), kind = (int)(ak % 2);
     const RowTables& T = a == 0 ? T3a : (a == 1 ? T3b : T3c);     // direction a's rows
-    const int64_t r = (tid % per_ak) / kMaxNodes;
-    if (r >= T.N) return;
-    const int k = (int)(tid % kMaxNodes);
-    const int m = kind == WGQ_MASS ? T.mM[r] : T.mK[r];
-    if (k >= m) return;
-    const double x = (kind == WGQ_MASS ? T.xM : T.xK)[r * kMaxNodes + k];
-    double* out = tab + tid * cw;
-    if (c.kind == WGQ_COEF_TRIG_SEP) {
-        const double arg = 2.0 * (double)c.wavenum[a] * x;   // trig(pi * arg)
-        out[0] = c.trig[a] == WGQ_TRIG_SIN ? sinpi(arg) : cospi(arg);
-    } else {
-        for (int q = 0; q < c.n_modes; ++q) {
-            const double arg = 2.0 * c.modes[q][1 + a] * x;
-            double cp = cospi(arg), sp = sinpi(arg);
-            if (a == 0) {
-                double ct, st;
-                sincos(c.modes[q][4], &st, &ct);
-                const double cc = cp * ct - sp * st, ss = sp * ct + cp * st;
-                cp = c.modes[q][0] * cc;
-                sp = c.modes[q][0] * ss;
-            }
-            out[2 * q] = cp;
-            out[2 * q + 1] = sp;
+    const int64_t r = (e % per_ak) / kMaxNodes;
+    const int k = (int)(e % kMaxNodes);
+    const bool live = r < T.N && k < (kind == WGQ_MASS ? T.mM[r] : T.mK[r]);
+    double* out = tab + e * cw;
+    if (c.kind != WGQ_COEF_FOURIER_LOGN || c.n_modes == 0) {         // TRIG_SEP (cw = 1) or no modes
+        double v = 0.0;
+        if (live && c.kind == WGQ_COEF_TRIG_SEP) {
+            const double arg = 2.0 * (double)c.wavenum[a] * (kind == WGQ_MASS ? T.xM : T.xK)[r * kMaxNodes + k];
+            v = c.trig[a] == WGQ_TRIG_SIN ? sinpi(arg) : cospi(arg);       // trig(pi * arg)
+        }
+        out[0] = v;
+        return;
+    }
+    double cp = 0.0, sp = 0.0;
+    if (live) {
+        const double x = (kind == WGQ_MASS ? T.xM : T.xK)[r * kMaxNodes + k];
+        const double arg = 2.0 * c.modes[q][1 + a] * x;
+        cp = cospi(arg), sp = sinpi(arg);
+        if (a == 0) {
+            double ct, st;
+            sincos(c.modes[q][4], &st, &ct);
+            const double cc = cp * ct - sp * st, ss = sp * ct + cp * st;
+            cp = c.modes[q][0] * cc;
+            sp = c.modes[q][0] * ss;
         }
     }
+    out[2 * q] = cp;
+    out[2 * q + 1] = sp;
 }
 
 template <int D>
@@ -1010,7 +1019,8 @@ int launch_load_pd(const GenericArgs& a, const PW3& PW, double* b, bool special,
 
 // coefficient factor tables for an analytic kind (stream-ordered scratch) or nullptr
 // Coefficient factor tables (stream-ordered scratch the caller frees): [2 dim][ctabN][kMaxNodes][cw],
-// unused node slots zero (the 2D kernels read 4 nodes per row and weigh the missing ones by 0).
+// unused node slots zero (written by k_coef_tables; the 2D kernels read 4 nodes per row and weigh
+// the missing ones by 0).
 int coef_tables(const wgq_rules_s* R, GenericArgs& a, const wgq_coeff_t* c, cudaStream_t st, double** tab) {
     *tab = nullptr;
     if (c->kind != WGQ_COEF_TRIG_SEP && c->kind != WGQ_COEF_FOURIER_LOGN) return WGQ_OK;
@@ -1018,8 +1028,8 @@ int coef_tables(const wgq_rules_s* R, GenericArgs& a, const wgq_coeff_t* c, cuda
     if (a.cw == 0) a.cw = 1;
     const int64_t entries = 2 * (int64_t)R->dim * a.ctabN * kMaxNodes;
     if (cudaMallocAsync((void**)tab, (size_t)entries * a.cw * sizeof(double), st) != cudaSuccess) return WGQ_ENOMEM;
-    cudaMemsetAsync(*tab, 0, (size_t)entries * a.cw * sizeof(double), st);
-    k_coef_tables<<<(unsigned)((entries + 255) / 256), 256, 0, st>>>(a.coef, R->dim, a.T3[0], a.T3[1], a.T3[2], a.ctabN,
+    const int64_t threads = entries * (c->kind == WGQ_COEF_FOURIER_LOGN && a.coef.n_modes > 0 ? a.coef.n_modes : 1);
+    k_coef_tables<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(a.coef, R->dim, a.T3[0], a.T3[1], a.T3[2], a.ctabN,
                                                                       *tab, a.cw);
     a.ctab = *tab;
     return WGQ_OK;

@@ -19,8 +19,9 @@
 //    (y-node n = (ky = n/2, mass|stiffness)), tile B the stiffness x-nodes against the mass
 //    y-nodes of both lines (n = (ky = n/2, line a|b)).  Every product is a used sample: 12 DMMA
 //    per 4 rows, 6 samples per lane, lane-dense exp;
-//  * exp by a 64-entry table of 2^(j/64) (16 lane-private copies, conflict-free) and a degree-5
-//    polynomial on |r| <= ln2/128 (10 FP64 operations, < 1 ulp before rounding);
+//  * exp by a 256-entry table of 2^(j/256) (16 lane-private copies, conflict-free) and a degree-4
+//    polynomial on |r| <= ln2/512 (8 FP64 operations, remainder < 4e-17; the 64-entry table with a
+//    degree-5 polynomial took 10 and the FP64 pipe, shared by the DMMAs, is the binding unit);
 //  * y stage on DMMA: the exp'd accumulator fragment is the B operand of T^T = Aw_y^T W^T as is
 //    (6 DMMA per 4 rows);
 //  * x stage on DMMA: the y stage's output fragment is the B operand as is, the class-I Aw_x^T
@@ -88,21 +89,23 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // Taylor coefficients of e^r (degree 5) from the constant bank
 __constant__ double kExp5[6] = {1.0, 1.0, 0.5, 1.0 / 6.0, 1.0 / 24.0, 1.0 / 120.0};
 
-// exp(x), |x| < 700: x = k ln2/64 + r with k = rint(64 x / ln2) (the 1.5*2^52 shifter leaves k
-// in the low word), |r| <= ln2/128 (Cody-Waite two-part ln2/64), e^x = 2^(k>>6) 2^((k&63)/64) e^r.
-// tbl holds 2^(j/64) at [j * 16 + copy], tb = tbl + copy (copy = lane & 15): the 16 lanes of a
+// exp(x), |x| < 700: x = k ln2/256 + r with k = rint(256 x / ln2) (the 1.5*2^52 shifter leaves k
+// in the low word), |r| <= ln2/512 (Cody-Waite two-part ln2/256), e^x = 2^(k>>8) 2^((k&255)/256) e^r
+// with e^r by its degree-4 Taylor polynomial (remainder < r^5/120 < 4e-17).
+// tbl holds 2^(j/256) at [j * 16 + copy], tb = tbl + copy (copy = lane & 15): the 16 lanes of a
 // half-warp read 16 different banks.
+constexpr int kExpBits = 8;
 __device__ __forceinline__ double exp_tab(double x, const double* tb) {
-    const double s = fma(x, 92.332482616893656877, 6755399441055744.0);   // 64/ln2, 1.5*2^52
+    const double s = fma(x, 369.32993046757462750, 6755399441055744.0);   // 256/ln2, 1.5*2^52
     const double kd = s - 6755399441055744.0;
     const int k = __double2loint(s);
-    double r = fma(-kd, 6.93147180369123816490e-01 / 64.0, x);
-    r = fma(-kd, 1.90821492927058770002e-10 / 64.0, r);
-    double q = kExp5[5];
+    double r = fma(-kd, 6.93147180369123816490e-01 / 256.0, x);
+    r = fma(-kd, 1.90821492927058770002e-10 / 256.0, r);
+    double q = kExp5[4];
 #pragma unroll
-    for (int i = 4; i >= 0; --i) q = fma(q, r, kExp5[i]);
-    const double t = tb[(k & 63) << 4];
-    return q * __hiloint2double(__double2hiint(t) + ((k >> 6) << 20), __double2loint(t));
+    for (int i = 3; i >= 0; --i) q = fma(q, r, kExp5[i]);
+    const double t = tb[(k & 255) << 4];
+    return q * __hiloint2double(__double2hiint(t) + ((k >> 8) << 20), __double2loint(t));
 }
 
 __device__ __forceinline__ void st_out(double* p, double v, uint64_t pol) {
@@ -427,10 +430,11 @@ __device__ __noinline__ void store_pair_general(double* dst, const int64_t* rp, 
 template <int KS, bool EXACT, int DBG>
 __global__ void __launch_bounds__(kF2iWarps * 32, kF2iMinBlocks) k_f2d_interior(const F2iArgs a, const F2fArgs fa) {
     constexpr int S = 7;
-    __shared__ double tbl[64 * 16];
+    __shared__ double tbl[(1 << kExpBits) * 16];
     __shared__ int slot_s[2 * 50];
     extern __shared__ double stage[];      // per warp: T staging, output staging
-    for (int e = threadIdx.x; e < 64 * 16; e += blockDim.x) tbl[e] = exp2((double)(e >> 4) * (1.0 / 64.0));
+    for (int e = threadIdx.x; e < (1 << kExpBits) * 16; e += blockDim.x)
+        tbl[e] = exp2((double)(e >> 4) * (1.0 / (1 << kExpBits)));
     if (threadIdx.x < 100) slot_s[threadIdx.x] = kF2iSlot[threadIdx.x / 50][threadIdx.x % 50];
     __syncthreads();
     const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, warp = threadIdx.x >> 5;
