@@ -12,6 +12,8 @@
 // stores of a warp are contiguous 256-byte runs of the row (a7).
 #include <cuda_runtime.h>
 
+#include <cmath>
+
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -119,8 +121,14 @@ struct Dir {
 //   FOURIER_LOGN: (C, S)_m = (cos, sin)(2 pi k_{m,a} x + [a = 0] theta_m) * ([a = 0] ? a_m : 1)
 // so that c = c0 + amp prod_a F_a, resp. c = exp(sum_m Re prod_a (C + i S)_m): the angle-sum
 // expansion of cos(2 pi k_m . x + theta_m) (R13), exact up to rounding.
-__global__ void k_coef_tables(const CoefDev c, int dim, const RowTables T3a, const RowTables T3b, const RowTables T3c,
-                              int64_t ctabN, double* tab, int cw) {
+// cos / sin of the mode phases theta_m, computed once on the host (they fold into direction 0's
+// factors: a_m cos(2 pi k x + theta) = a_m (cos(2 pi k x) cos theta - sin(2 pi k x) sin theta))
+struct PhaseTab {
+    double c[WGQ_MAX_MODES], s[WGQ_MAX_MODES];
+};
+
+__global__ void k_coef_tables(const CoefDev c, const PhaseTab ph, int dim, const RowTables T3a, const RowTables T3b,
+                              const RowTables T3c, int64_t ctabN, double* tab, int cw) {
     // one thread per (table entry, mode) (FOURIER; one per entry for TRIG_SEP): the modes of an
     // entry are independent, and a warp writes 32 consecutive 16-byte column pairs.  Every slot is
     // written (zeros for node slots beyond the rule and rows beyond the direction's count).
@@ -152,8 +160,7 @@ __global__ void k_coef_tables(const CoefDev c, int dim, const RowTables T3a, con
         const double arg = 2.0 * c.modes[q][1 + a] * x;
         cp = cospi(arg), sp = sinpi(arg);
         if (a == 0) {
-            double ct, st;
-            sincos(c.modes[q][4], &st, &ct);
+            const double ct = ph.c[q], st = ph.s[q];
             const double cc = cp * ct - sp * st, ss = sp * ct + cp * st;
             cp = c.modes[q][0] * cc;
             sp = c.modes[q][0] * ss;
@@ -1029,8 +1036,13 @@ int coef_tables(const wgq_rules_s* R, GenericArgs& a, const wgq_coeff_t* c, cuda
     const int64_t entries = 2 * (int64_t)R->dim * a.ctabN * kMaxNodes;
     if (cudaMallocAsync((void**)tab, (size_t)entries * a.cw * sizeof(double), st) != cudaSuccess) return WGQ_ENOMEM;
     const int64_t threads = entries * (c->kind == WGQ_COEF_FOURIER_LOGN && a.coef.n_modes > 0 ? a.coef.n_modes : 1);
-    k_coef_tables<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(a.coef, R->dim, a.T3[0], a.T3[1], a.T3[2], a.ctabN,
-                                                                      *tab, a.cw);
+    PhaseTab ph{};
+    for (int q = 0; q < a.coef.n_modes && q < WGQ_MAX_MODES; ++q) {
+        ph.c[q] = std::cos(a.coef.modes[q][4]);
+        ph.s[q] = std::sin(a.coef.modes[q][4]);
+    }
+    k_coef_tables<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(a.coef, ph, R->dim, a.T3[0], a.T3[1], a.T3[2],
+                                                                      a.ctabN, *tab, a.cw);
     a.ctab = *tab;
     return WGQ_OK;
 }
