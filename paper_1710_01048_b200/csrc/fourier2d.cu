@@ -66,6 +66,7 @@ constexpr int kF2iEdge1 = 2 * 52;         // element 97 of a shifted run (s = 98
 
 struct F2iArgs {
     const double* ctab;  // k_coef_tables layout: ((kind * N + r) * kMaxNodes + k) * cw + j
+    unsigned long long* ticket;   // work-item counter (stream-ordered scratch, zeroed per launch)
     int cw;
     int64_t N, row_begin, row_end;
     int lo, hi;          // class-I index range [lo, hi] (both directions)
@@ -465,16 +466,15 @@ __global__ void __launch_bounds__(kF2iWarps * 32, kF2iMinBlocks) k_f2d_interior(
     const int chunks = (rpairs + kF2iChunk - 1) / kF2iChunk;
     const int64_t items = a.line1 >= a.line0 ? (int64_t)lpairs * chunks : 0;
     // the frame items first (their rows have per-row tables; a few per warp), then the interior
-    for (int64_t it0 = (int64_t)blockIdx.x * kF2iWarps + warp; it0 < fa.items + fa.nshell + items;
-         it0 += (int64_t)gridDim.x * kF2iWarps) {
+    // items are claimed from a ticket after the first one (frame, shell, then interior in
+    // chunk-major order): a warp that finishes early takes the next item, no static tail
+    const int64_t nwarps = (int64_t)gridDim.x * kF2iWarps;
+    for (int64_t it0 = (int64_t)blockIdx.x * kF2iWarps + warp; it0 < fa.items + fa.nshell + items;) {
         if (it0 < fa.items) {
             f2d_frame_item<KS>(fa, it0, tbl, os, lane, pol);
-            continue;
-        }
-        if (it0 < fa.items + fa.nshell) {
+        } else if (it0 < fa.items + fa.nshell) {
             f2d_shell_item<KS>(fa, fa.shell[it0 - fa.items], tbl, os, lane, pol);
-            continue;
-        }
+        } else {
         const int64_t it = it0 - fa.items - fa.nshell;
         const int lp = (int)(it % lpairs), ch = (int)(it / lpairs);
         const int La = a.line0 + 2 * lp;
@@ -659,6 +659,10 @@ __global__ void __launch_bounds__(kF2iWarps * 32, kF2iMinBlocks) k_f2d_interior(
         };
         if (full[0] && full[1] && a.Mv && a.Kv) steps(std::true_type{});
         else steps(std::false_type{});
+        }
+        unsigned long long nx = 0;
+        if (lane == 0) nx = atomicAdd(a.ticket, 1ull);
+        it0 = nwarps + (int64_t)__shfl_sync(0xffffffffu, nx, 0);
     }
 }
 
@@ -766,6 +770,8 @@ int launch_f2d_interior(const wgq_rules_s* R, const RowTables& T, const double* 
     int64_t blocks = std::min<int64_t>((items + kF2iWarps - 1) / kF2iWarps, (int64_t)sms * kF2iMinBlocks);
     blocks = std::max<int64_t>(blocks, 1);
     const size_t smem = (size_t)kF2iWarps * kF2iWarpSmem * sizeof(double);
+    if (cudaMallocAsync((void**)&a.ticket, sizeof(unsigned long long), st) != cudaSuccess) return WGQ_ENOMEM;
+    cudaMemsetAsync(a.ticket, 0, sizeof(unsigned long long), st);
     auto go = [&](auto kern) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
             return WGQ_ECUDA;
@@ -780,6 +786,7 @@ int launch_f2d_interior(const wgq_rules_s* R, const RowTables& T, const double* 
     else if (cw < 16) rc = go(k_f2d_interior<4, false, 0>);
     else if (cw == 32) rc = go(k_f2d_interior<8, true, 0>);
     else rc = go(k_f2d_interior<8, false, 0>);
+    cudaFreeAsync(a.ticket, st);
     if (rc != WGQ_OK) return rc;
     return cudaGetLastError() == cudaSuccess ? WGQ_OK : WGQ_ECUDA;
 }
