@@ -797,7 +797,7 @@ __global__ void __launch_bounds__(256) k_load_grid_line(const GenericArgs a, con
 // two vertex planes (their y stages and output planes are independent: ILP for the FP64 chains).
 constexpr int kLPW = 8;        // warps (= lines) per block
 constexpr int kLPR = 3;        // vertex columns / rows i1 per lane
-constexpr int kLPA2 = 3;       // plane pairs in flight ahead
+constexpr int kLPA2 = 2;       // plane pairs in flight ahead (3: 0.084 ms at C5, 2: 0.081, 1: 0.083)
 constexpr int kLPRR = 8;       // raw ring depth (power of two >= 2 kLPA2 + 2)
 constexpr int kLPSEG = 96;     // output planes per segment (bounds the staged z weights)
 static_assert(kLPRR >= 2 * kLPA2 + 2 && (kLPRR & (kLPRR - 1)) == 0, "load pencil raw ring depth");
