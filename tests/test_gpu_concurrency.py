@@ -13,7 +13,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("p,n,d,kind", [(3, 9, 3, "grid"), (2, 12, 2, "fourier"), (3, 8, 3, "trig")])
+@pytest.mark.parametrize("p,n,d,kind", [(3, 9, 3, "grid"), (2, 12, 2, "fourier"), (3, 20, 2, "fourier"), (3, 8, 3, "trig")])
 def test_threads_share_a_fresh_handle(p, n, d, kind):
     from paper_1710_01048_b200 import api, wgq
     desc = {"grid": {"kind": "grid"},
